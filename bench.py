@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""bench.py -- BC TEPS of the B200 hot path (one JSON line on rank 0).
+
+Default workload = BASELINE.json config 4: R-MAT scale 20, EF 16
+((a,b,c,d) = (.57,.19,.19,.05), seed 1, label permutation), 65,536 source
+vertices sampled uniformly without replacement among non-isolated vertices
+(sample seed 2).  A *step* is one pass of the whole hot path (forward sweep,
+backward sweep, BC update -- every SURVEY §8(a) row -- plus the NCCL BC
+all-reduce when N > 1) over `--sources-per-gpu` sources per GPU (weak
+scaling: at N = 8 one step is the full 65,536-source job).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config rmat20]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+    python bench.py --impl reference ...   # the CPU oracle, same metric/config
+
+value = sources processed by all ranks x m / max-over-ranks device time, m =
+unique undirected edges (Eq.7; reading R16 -- the paper's
+own published TEPS count 2m, reported beside as "teps_paper_convention").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BC TEPS (sources·m/s) at 1/2/4/8 B200; % HBM roofline; speedup vs CPU oracle"
+
+CONFIGS = {
+    # name: (generator, kwargs, total sources (None = all), sources per gpu per step, prune)
+    "rmat20": ("rmat", dict(scale=20, ef=16), 65536, 8192, False),
+    "rmat12": ("rmat", dict(scale=12, ef=16), None, 4096, False),
+    "rmat16": ("rmat", dict(scale=16, ef=16), None, 65536, False),
+    "rmat16p": ("rmat", dict(scale=16, ef=16), None, 65536, True),
+    "grid": ("grid", dict(R=512, C=512), None, 8192, False),
+    "rmat23": ("rmat", dict(scale=23, ef=16), 16384, 2048, False),
+}
+
+
+def make_graph(cfg):
+    import graphgen as gg
+
+    kind, kw, _, _, _ = CONFIGS[cfg]
+    if kind == "rmat":
+        return gg.rmat(kw["scale"], kw["ef"], seed=1, permute=True)
+    return gg.grid(kw["R"], kw["C"])
+
+
+def source_list(g, cfg):
+    import graphgen as gg
+
+    total = CONFIGS[cfg][2]
+    if total is None:
+        return np.arange(g.n, dtype=np.int32)
+    return gg.sample_sources(g, total, seed=2)
+
+
+def workload_name(cfg):
+    return {
+        "rmat20": "rmat20_ef16_sampled65536",
+        "rmat12": "rmat12_ef16_all_sources",
+        "rmat16": "rmat16_ef16_all_sources_prune_off",
+        "rmat16p": "rmat16_ef16_all_sources_prune_on",
+        "grid": "grid512x512_all_sources",
+        "rmat23": "rmat23_ef16_sampled16384",
+    }[cfg]
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def clocks_sampler_start(idx):
+    try:
+        f = open(os.path.join(ROOT, "gpurun_out", f"clocks_rank{idx}.csv") if os.path.isdir(
+            os.path.join(ROOT, "gpurun_out")) else os.devnull, "w")
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        p = subprocess.Popen(["nvidia-smi", "-i", str(idx), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                              "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        return p, f
+    except Exception:
+        return None, None
+
+
+def clocks_sampler_stop(h):
+    p, f = h
+    if p is None:
+        return None
+    p.terminate()
+    try:
+        out, _ = p.communicate(timeout=5)
+    except Exception:
+        p.kill()
+        out = ""
+    if f:
+        f.write(out)
+        f.close()
+    sm, mx, reasons = [], [], set()
+    for line in out.strip().splitlines():
+        parts = [x.strip() for x in line.split(",")]
+        if len(parts) < 9:
+            continue
+        try:
+            sm.append(float(parts[1]))
+            mx.append(float(parts[2]))
+        except ValueError:
+            continue
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for nm, val in zip(names, parts[5:9]):
+            if val.lower().startswith("active"):
+                reasons.add(nm)
+    if not sm:
+        return None
+    return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+            "samples": len(sm)}
+
+
+def cpu_baseline(g, sources, budget_s=15.0):
+    """The oracle as it stands, on this host's cores, on a bounded sample."""
+    import oracle
+
+    cores = oracle.num_threads()
+    rng = np.random.default_rng(7)
+    pool = rng.permutation(sources)
+    first = pool[:cores]
+    t0 = time.perf_counter()
+    oracle.bc(g, first, threads=cores)
+    t1 = time.perf_counter() - t0
+    done, tot_t = len(first), t1
+    rounds = int(max(0, budget_s - t1) / max(t1, 1e-3))
+    if rounds > 0:
+        more = pool[cores: cores * (1 + rounds)]
+        t0 = time.perf_counter()
+        oracle.bc(g, more, threads=cores)
+        tot_t += time.perf_counter() - t0
+        done += len(more)
+    return {"value": done * g.m / tot_t, "unit": "TEPS", "cores": cores, "kind": "oracle",
+            "sample": f"{done} of the workload's sources (uniform sample, seed 7), {tot_t:.1f} s"}
+
+
+def run_reference(args, cfg):
+    """--impl reference: the CPU oracle timed as it stands (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+
+    g = make_graph(cfg)
+    S = source_list(g, cfg)
+    cores = oracle.num_threads()
+    # bounded sample per step: one source per core (whole run stays within minutes)
+    per_step = cores if cfg not in ("rmat12",) else min(len(S), 16 * cores)
+    rng = np.random.default_rng(11)
+    pool = rng.permutation(S)
+    for i in range(args.warmup):
+        oracle.bc(g, pool[:per_step], threads=cores)
+    t0 = time.perf_counter()
+    done = 0
+    for i in range(args.steps):
+        chunk = pool[(i * per_step) % len(pool):][:per_step]
+        oracle.bc(g, chunk, threads=cores)
+        done += len(chunk)
+    t = time.perf_counter() - t0
+    v = done * g.m / t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TEPS", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": workload_name(cfg), "n": g.n, "m": g.m,
+                                            "sources_per_step": per_step},
+            "cpu_baseline": {"value": v, "unit": "TEPS", "cores": cores, "kind": "oracle",
+                             "sample": f"{per_step} sources per step (one per core), uniform sample seed 11"},
+            "e2e": {"value": v, "unit": "TEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def algorithmic_bytes(st, K):
+    """SURVEY §8(d-iii) model, split per kernel:
+    forward  = A(4/K + 1/8) + 8 D + 8 n_s     (col ids shared by K lanes, 1-bit level test per lane,
+                                                sigma read per DAG edge, sigma written per reached vertex)
+    backward = A(4/K + 1/8) + 8 D + 16 n_s    (coef read per DAG edge, sigma read + coef write per vertex)"""
+    A, D, N = st["adj_reached"], st["dag_edges"], st["reached"]
+    common = A * (4.0 / K + 1.0 / 8.0) + 8.0 * D
+    return common + 8.0 * N, common + 16.0 * N
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--config", default="rmat20", choices=sorted(CONFIGS))
+    ap.add_argument("--sources-per-gpu", type=int, default=0)
+    ap.add_argument("--lane-words", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = args.config
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1602_00963_b200 as bcb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    _, _, total, per_gpu_default, prune = CONFIGS[cfg]
+    per_gpu = args.sources_per_gpu or per_gpu_default
+
+    g = make_graph(cfg)
+    S = source_list(g, cfg)
+    per_gpu = min(per_gpu, len(S))
+    G = bcb.Graph.from_csr(g, device=local)
+    if prune:
+        G.prune_degree1()
+        import graphgen as gg  # noqa: F401
+        om, rm, _, _ = G.pruning()
+        S = S[rm[S] == 0]
+    if args.lane_words:
+        G.set_option(bcb.OPT_LANE_WORDS, args.lane_words)
+    stream = torch.cuda.current_stream()
+    out = torch.empty(g.n, dtype=torch.float64, device=f"cuda:{local}")
+
+    def step_sources(i):
+        start = ((i * world + rank) * per_gpu) % len(S)
+        idx = (start + np.arange(per_gpu)) % len(S)
+        return S[idx]
+
+    def one_step(i, profile=False):
+        G.compute(step_sources(i), out=out, stream=stream)
+        if world > 1:
+            dist.all_reduce(out)
+
+    for i in range(args.warmup):
+        one_step(i)
+    torch.cuda.synchronize()
+
+    G.set_option(bcb.OPT_PROFILE, 1)
+    sampler = clocks_sampler_start(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    agg = {"fwd_ms": 0.0, "bwd_ms": 0.0, "fwd_launches": 0, "bwd_launches": 0, "kernel_launches": 0,
+           "reached": 0, "adj_reached": 0, "dag_edges": 0, "num_sources": 0, "levels_total": 0, "batches": 0}
+    fwd_bytes = bwd_bytes = 0.0
+    lanes = 0
+    e0.record(stream)
+    for i in range(args.steps):
+        one_step(args.warmup + i)
+        st = G.stats()
+        lanes = st["lanes"]
+        for k in agg:
+            agg[k] += st[k]
+        fb, bb = algorithmic_bytes(st, st["lanes"])
+        fwd_bytes += fb
+        bwd_bytes += bb
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clocks_sampler_stop(sampler)
+    ms = e0.elapsed_time(e1)
+    G.set_option(bcb.OPT_PROFILE, 0)
+    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    sources_all = per_gpu * world * args.steps
+    value = sources_all * g.m / (ms_max / 1e3)
+
+    # ---- end to end through the C ABI with HOST buffers (sources H2D, BC D2H inside the region)
+    e2e = None
+    if not args.no_e2e:
+        host_out = np.empty(g.n, np.float64)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            G.compute(step_sources(args.warmup + i), out=host_out)
+            if world > 1:
+                tt = torch.from_numpy(host_out).to(f"cuda:{local}")
+                dist.all_reduce(tt)
+                host_out = tt.cpu().numpy()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        e2e = {"value": sources_all * g.m / dt, "unit": "TEPS", "h2d_bytes_per_step": 4 * per_gpu * world
+               + (8 * g.n * world if world > 1 else 0), "d2h_bytes_per_step": 8 * g.n * world}
+
+    if rank == 0:
+        pk, pk_kind = peaks()
+        dom = "bwd" if agg["bwd_ms"] >= agg["fwd_ms"] else "fwd"
+        dom_bytes = bwd_bytes if dom == "bwd" else fwd_bytes
+        dom_ms = agg[f"{dom}_ms"]
+        achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
+        traffic = None
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+            traffic = tr.get(cfg, {}).get(dom)
+        except Exception:
+            pass
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "kernel": f"lanes_level_kernel<{dom}>",
+                "peak_kind": pk_kind,
+                "kernel_share_of_step": dom_ms / (ms / 1.0) if ms > 0 else None,
+                "fwd": {"ms": agg["fwd_ms"], "alg_gb": fwd_bytes / 1e9,
+                        "gbs": fwd_bytes / (agg["fwd_ms"] / 1e3) / 1e9 if agg["fwd_ms"] else 0},
+                "bwd": {"ms": agg["bwd_ms"], "alg_gb": bwd_bytes / 1e9,
+                        "gbs": bwd_bytes / (agg["bwd_ms"] / 1e3) / 1e9 if agg["bwd_ms"] else 0}}
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(g, S)
+        line = {
+            "metric": METRIC, "value": value, "unit": "TEPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(cfg), "n": g.n, "m": g.m, "sources_total": len(S),
+                       "sources_per_gpu_per_step": per_gpu, "lanes_per_batch": lanes, "pruning": prune,
+                       "parallelism": f"source-sharded x{world} + NCCL BC all-reduce" if world > 1 else "1 GPU",
+                       "l2": "inputs exceed L2 (per step: CSR 4*2m B streamed + sigma/coef rows 8*K*n B); no flush"},
+            "teps_paper_convention": 2 * value,
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
+            "gpu_launches": agg["kernel_launches"],
+            "stats": {k: agg[k] for k in ("levels_total", "batches", "reached", "adj_reached", "dag_edges")},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    G.close()
+
+
+if __name__ == "__main__":
+    main()

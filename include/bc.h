@@ -1,0 +1,175 @@
+/*
+ * bc.h -- C ABI of the B200-native exact-Brandes betweenness-centrality hot
+ * path (libbcb200.so).  extern "C", plain pointers and sizes, no C++ or torch
+ * types, no exceptions cross this boundary.
+ *
+ * Problem statement (Sec. 2): G = (V, E) undirected and
+ * unweighted, n = |V|, m unordered pairs; the betweenness of v is
+ *     BC(v) = sum_{s != t != v} sigma_st(v) / sigma_st            (Eq.1)
+ *           = sum_{s != v} delta_s(v)                             (Eq.3)
+ * with the dependency recursion of Eq.(2).  Scores are
+ * UNNORMALISED over ORDERED pairs (Alg.1 adds delta_s(w) once per source; a
+ * path P3 has centre score 2).
+ *
+ * Threading: calls on one handle must be serialised by the caller.  Distinct
+ * handles may be used from distinct threads.  Every handle is bound to one
+ * CUDA device; the library sets that device for the duration of a call and
+ * restores the caller's current device afterwards.
+ *
+ * Errors: every call returns a bc_status; nothing is thrown.  On error the
+ * outputs are unspecified and bc_last_error() (thread-local) carries a
+ * one-line detail (for BC_ERR_CUDA it includes cudaGetErrorString()).
+ */
+#ifndef BC_B200_H
+#define BC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bc_graph bc_graph; /* opaque; owns all device memory it allocates */
+
+typedef enum {
+    BC_OK = 0,
+    BC_ERR_INVALID = 1,  /* bad argument: n<=0 or n>2^31-1, malformed CSR (when
+                            validating), source out of range, duplicate source,
+                            pruned-away source, unknown option, NULL handle    */
+    BC_ERR_NOMEM = 2,    /* cudaMalloc / host allocation failed               */
+    BC_ERR_CUDA = 3,     /* any other CUDA runtime failure                    */
+    BC_ERR_STATE = 4,    /* call not valid in the handle's state (e.g. second
+                            bc_prune_degree1: the paper's single pass,
+                            PAPER.md:580 footnote)                            */
+    BC_ERR_INTERNAL = 5
+} bc_status;
+
+/* bc_graph_create flags */
+#define BC_CREATE_VALIDATE 0x1u /* O(m) device check: rows sorted ascending,
+                                   symmetric, no self-loops, no duplicates   */
+
+/*
+ * bc_graph_create -- copy a simple undirected graph in CSR form to `device`
+ * (SPEC.md:22-28 invariants).
+ *   n        number of vertices, 1 <= n <= 2^31-1.
+ *   row_ptr  HOST int64[n+1], row_ptr[0] = 0, non-decreasing,
+ *            row_ptr[n] = 2m <= 2^31-1 (directed entries).
+ *   col_idx  HOST int32[row_ptr[n]]: the neighbours of v are
+ *            col_idx[row_ptr[v] .. row_ptr[v+1]), strictly ascending.
+ *   device   CUDA device ordinal the handle is bound to.
+ *   flags    0 or BC_CREATE_VALIDATE.  Without validation a CSR that is not
+ *            simple/symmetric gives undefined results (parallel edges would
+ *            count as distinct shortest paths).
+ *   out      receives the handle.
+ * Ownership: the caller keeps its host arrays (they are copied); the handle
+ * owns the device copies until bc_destroy.
+ */
+bc_status bc_graph_create(int64_t n, const int64_t *row_ptr, const int32_t *col_idx, int device,
+                          uint32_t flags, bc_graph **out);
+
+/*
+ * bc_prune_degree1 -- 1-degree reduction, Alg.6 and
+ * Eq.(4), run on the device in one pass (no cascaded
+ * tree removal, PAPER.md:580 footnote): every vertex u of degree 1 is
+ * removed, omega(v) counts v's removed neighbours, and the residual graph
+ * keeps the edges whose two endpoints both survive (a K2 component loses
+ * both endpoints).  Subsequent bc_compute calls run Brandes on the residual
+ * graph with the Eq.(5) recursion and the endpoint terms (R7-R13)
+ * and return the SAME scores as on the unpruned graph.
+ *   out_removed  nullable; receives the number of removed vertices.
+ * BC_ERR_STATE if the handle was already pruned.
+ */
+bc_status bc_prune_degree1(bc_graph *g, int64_t *out_removed);
+
+/*
+ * bc_compute -- exact BC restricted to a source set S (Eq.3 with s in S):
+ *     out_bc[v] = sum_{s in S, s != v} delta_s(v)
+ * computed on the device: per batch of sources, a level-synchronous forward
+ * sweep counting sigma and depth (Alg.2/Alg.3), then the
+ * backward successor-checking sweep (Alg.4/Alg.5) and the
+ * BC update (Alg.1 line 30).  Frontier edges are mapped to threads through a
+ * per-tile exclusive scan of frontier degrees plus a binary search
+ * (PAPER.md:310-330), many sources run concurrently as bit lanes.
+ *   sources      HOST int32[num_sources] distinct vertex ids, or NULL for all
+ *                vertices (unpruned) / all eligible vertices (pruned: not
+ *                removed and residual degree > 0 or omega > 0).  Isolated
+ *                sources contribute 0.
+ *   out_bc       double[n], HOST or DEVICE pointer (detected).  Overwritten,
+ *                never accumulated.
+ *   cuda_stream  cudaStream_t or NULL (library-internal stream).  With a
+ *                DEVICE out_bc the call is stream-ordered and returns once
+ *                the work is enqueued... except that the level loop polls a
+ *                per-level device flag, so the call returns after the last
+ *                backward level is enqueued; out_bc is valid once `stream`
+ *                reaches that point.  With a HOST out_bc the call is
+ *                synchronous.
+ * Pruned handles: S = {s} stands for s plus its removed degree-1 children
+ * (R13), i.e. the result equals the unpruned BC over S+; with
+ * S = all it is the exact BC.  A removed source is BC_ERR_INVALID.
+ */
+bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, double *out_bc,
+                     void *cuda_stream);
+
+/* bc_destroy -- free every resource of the handle; NULL-safe. */
+bc_status bc_destroy(bc_graph *g);
+
+const char *bc_status_string(bc_status s);
+const char *bc_last_error(void); /* thread-local detail of the last failure */
+
+/*
+ * bc_sssp -- verification only (not timed): one source on the ORIGINAL
+ * (unpruned) graph.  All outputs are HOST arrays of length n (each nullable):
+ *   depth           int32, -1 if unreachable                  (Alg.2 d[])
+ *   sigma           uint64 shortest-path counts (exact integer path)
+ *   sigma_overflow  uint8, 1 where sigma (or a predecessor's) exceeded 2^64-1
+ *   delta           double dependency delta_s(v) (0 for s and unreached)
+ * Synchronous.
+ */
+bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma,
+                  uint8_t *sigma_overflow, double *delta);
+
+/* Tuning options (bc_set_option).  Values are validated. */
+typedef enum {
+    BC_OPT_LANE_WORDS = 1, /* 0 = auto, else 1, 2 or 4: K = 64*value source lanes per batch */
+    BC_OPT_HUB_DEGREE = 2, /* vertices with degree > value are processed as split hubs (>= 32) */
+    BC_OPT_PROFILE = 3,    /* 1 = record CUDA events around the level kernels (bc_get_stats) */
+    BC_OPT_MODE = 4        /* 0 = auto, 1 = lanes (bit-lane batches), 2 = slices (CTA per source) */
+} bc_option;
+
+bc_status bc_set_option(bc_graph *g, int option, int64_t value);
+
+/* Statistics of the last bc_compute on this handle. */
+typedef struct {
+    int64_t num_sources;     /* traversal sources (residual degree > 0)          */
+    int64_t num_trivial;     /* endpoint-only sources (pruned, residual-isolated) */
+    int64_t batches;         /* source batches                                  */
+    int64_t lanes;           /* K, sources per batch                            */
+    int64_t levels_total;    /* sum over batches of forward levels               */
+    int64_t fwd_launches;    /* forward level-kernel launches                   */
+    int64_t bwd_launches;    /* backward level-kernel launches                  */
+    int64_t reached;         /* sum over sources of reached vertices (n_s, residual) */
+    int64_t adj_reached;     /* sum over sources of reached adjacency (A_s)     */
+    int64_t dag_edges;       /* sum over sources of DAG edges (D_s)              */
+    double fwd_ms;           /* summed forward level-kernel time (BC_OPT_PROFILE) */
+    double bwd_ms;           /* summed backward level-kernel time (BC_OPT_PROFILE) */
+    double total_ms;         /* whole bc_compute device time (BC_OPT_PROFILE)    */
+    int64_t kernel_launches; /* all library kernel launches of the call          */
+    int64_t dist_sum;        /* sum over sources of sum of depths of reached vertices */
+} bc_stats;
+
+bc_status bc_get_stats(const bc_graph *g, bc_stats *out);
+
+/* Pruning outputs for bit-exact parity with the Alg.6 oracle (HOST arrays,
+ * each nullable): omega uint32[n], removed uint8[n], residual CSR
+ * row_ptr int64[n+1] and col int32[capacity >= residual nnz]; *res_nnz gets
+ * the residual nnz.  BC_ERR_STATE if the handle is not pruned. */
+bc_status bc_get_pruning(const bc_graph *g, uint32_t *omega, uint8_t *removed, int64_t *res_row_ptr,
+                         int32_t *res_col, int64_t *res_nnz);
+
+/* Handle facts: n, original nnz, current (residual) nnz, device. */
+bc_status bc_graph_info(const bc_graph *g, int64_t *n, int64_t *nnz, int64_t *res_nnz, int *device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BC_B200_H */

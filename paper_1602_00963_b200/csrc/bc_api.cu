@@ -1,0 +1,874 @@
+// bc_api.cu -- C ABI (include/bc.h) of the B200 BC hot path: graph
+// residency, 1-degree pruning, the batched forward/backward level loop and
+// the verification entry point.  All arithmetic of the method runs in the
+// kernels of lanes.cuh / graph_kernels.cuh; this file only allocates,
+// validates arguments, sequences launches and copies results.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <algorithm>
+
+#include "bc.h"
+#include "util.cuh"
+#include "lanes.cuh"
+#include "graph_kernels.cuh"
+
+using namespace bcb;
+
+namespace {
+
+thread_local std::string g_err;
+
+bc_status fail(bc_status s, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define CU(call)                                                                                      \
+    do {                                                                                              \
+        cudaError_t e_ = (call);                                                                      \
+        if (e_ != cudaSuccess) {                                                                      \
+            (void)cudaGetLastError();                                                                 \
+            return fail(e_ == cudaErrorMemoryAllocation ? BC_ERR_NOMEM : BC_ERR_CUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                           \
+        }                                                                                             \
+    } while (0)
+
+#define CK(expr)                              \
+    do {                                      \
+        bc_status s_ = (expr);                \
+        if (s_ != BC_OK) return s_;           \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int d) {
+        cudaGetDevice(&prev);
+        if (prev != d) cudaSetDevice(d);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+template <typename T>
+bc_status dalloc(T **p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    CU(cudaMalloc((void **)p, count * sizeof(T)));
+    return BC_OK;
+}
+
+template <typename T>
+void dfree(T *&p) {
+    if (p) cudaFree((void *)p);
+    p = nullptr;
+}
+
+// A CSR resident on the device plus its hub decomposition.
+struct DevCSR {
+    int *rp = nullptr;
+    int *col = nullptr;
+    int64_t nnz = 0;
+    int nhub = 0, nseg = 0;
+    int *hub_ids = nullptr;
+    int *hub_seg_off = nullptr;
+    std::vector<int> h_deg;
+    void release() {
+        dfree(rp);
+        dfree(col);
+        dfree(hub_ids);
+        dfree(hub_seg_off);
+        nhub = nseg = 0;
+    }
+};
+
+struct LaneWS {
+    int W = 0;
+    bool verify = false;
+    void *S = nullptr;
+    uint64_t *seen = nullptr;
+    uint64_t *ovf = nullptr;
+    std::vector<uint64_t *> chunks;  // LCH levels each
+    void *hub_acc = nullptr;
+    uint64_t *hub_ovf = nullptr;
+    int hub_cap = 0;
+    double *lane_w1 = nullptr;
+    double *lane_ns = nullptr;
+    void release() {
+        dfree(S);
+        dfree(seen);
+        dfree(ovf);
+        for (auto &c : chunks) dfree(c);
+        chunks.clear();
+        dfree(hub_acc);
+        dfree(hub_ovf);
+        dfree(lane_w1);
+        dfree(lane_ns);
+        W = 0;
+        hub_cap = 0;
+    }
+};
+
+constexpr int LCH = 8;  // levels per mask chunk
+
+}  // namespace
+
+struct bc_graph {
+    int device = 0;
+    int64_t n = 0;
+    DevCSR orig, res;  // res.rp == nullptr while unpruned
+    bool pruned = false;
+    uint32_t *omega = nullptr;
+    uint8_t *removed = nullptr;
+    std::vector<uint32_t> h_omega;
+    std::vector<uint8_t> h_removed;
+    int hub_deg = 4096;
+    int lane_words_opt = 0;
+    int profile = 0;
+    int mode = 0;
+    int num_sms = 148;
+    cudaStream_t own_stream = nullptr;
+    LaneWS ws, vws;  // compute workspace, verification workspace (W = 1)
+    unsigned long long *d_stats = nullptr;  // [4]
+    int *d_work_ctr = nullptr;              // [4]
+    int *d_flags = nullptr;                 // [flag_cap]
+    int flag_cap = 0;
+    int *h_flag = nullptr;                  // pinned
+    int *d_src = nullptr;
+    int64_t src_cap = 0;
+    double *d_bc = nullptr;
+    int *d_tmp = nullptr;  // scan scratch
+    int64_t tmp_cap = 0;
+    bc_stats last{};
+    DevCSR &cur() { return pruned ? res : orig; }
+};
+
+namespace {
+
+// ---------------------------------------------------------------- scans
+bc_status ensure_tmp(bc_graph *g, int64_t count) {
+    if (g->tmp_cap >= count) return BC_OK;
+    dfree(g->d_tmp);
+    CK(dalloc(&g->d_tmp, (size_t)count));
+    g->tmp_cap = count;
+    return BC_OK;
+}
+
+// exclusive scan of n ints, total into *d_total (device int)
+bc_status dev_scan(bc_graph *g, const int *in, int *out, int64_t n, int *d_total, cudaStream_t st) {
+    int64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    if (ntiles == 0) ntiles = 1;
+    CK(ensure_tmp(g, ntiles));
+    scan_tiles_kernel<<<(unsigned)ntiles, BC_NT, 0, st>>>(in, out, g->d_tmp, n);
+    scan_sums_kernel<<<1, BC_NT, 0, st>>>(g->d_tmp, (int)ntiles, d_total);
+    scan_add_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, g->d_tmp, n);
+    CU(cudaGetLastError());
+    return BC_OK;
+}
+
+bc_status build_hubs(bc_graph *g, DevCSR &c, cudaStream_t st) {
+    dfree(c.hub_ids);
+    dfree(c.hub_seg_off);
+    c.nhub = c.nseg = 0;
+    const int n = (int)g->n;
+    int *flag = nullptr, *pos = nullptr, *tot = nullptr;
+    CK(dalloc(&flag, n));
+    CK(dalloc(&pos, n));
+    CK(dalloc(&tot, 2));
+    hub_flag_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, c.rp, g->hub_deg, flag);
+    CK(dev_scan(g, flag, pos, n, tot, st));
+    int nhub = 0;
+    CU(cudaMemcpyAsync(&nhub, tot, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    c.nhub = nhub;
+    CK(dalloc(&c.hub_ids, nhub));
+    CK(dalloc(&c.hub_seg_off, nhub + 1));
+    if (nhub > 0) {
+        hub_scatter_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, flag, pos, c.hub_ids);
+        int *cnt = nullptr;
+        CK(dalloc(&cnt, nhub));
+        hub_segcount_kernel<<<(nhub + 255) / 256, 256, 0, st>>>(nhub, c.hub_ids, c.rp, g->hub_deg, cnt);
+        CK(dev_scan(g, cnt, c.hub_seg_off, nhub, tot + 1, st));
+        CU(cudaMemcpyAsync(c.hub_seg_off + nhub, tot + 1, sizeof(int), cudaMemcpyDeviceToDevice, st));
+        int nseg = 0;
+        CU(cudaMemcpyAsync(&nseg, tot + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        c.nseg = nseg;
+        dfree(cnt);
+    }
+    CU(cudaGetLastError());
+    dfree(flag);
+    dfree(pos);
+    dfree(tot);
+    return BC_OK;
+}
+
+bc_status ensure_flags(bc_graph *g, int need) {
+    if (g->flag_cap >= need) return BC_OK;
+    int cap = std::max(need, 2 * g->flag_cap);
+    cap = std::max(cap, 64);
+    dfree(g->d_flags);
+    CK(dalloc(&g->d_flags, cap));
+    g->flag_cap = cap;
+    return BC_OK;
+}
+
+bc_status ensure_ws(bc_graph *g, LaneWS &ws, int W, bool verify, int nhub) {
+    const size_t n = (size_t)g->n;
+    const int K = 64 * W;
+    if (ws.W != W || ws.verify != verify) {
+        ws.release();
+        CK(dalloc((double **)&ws.S, n * K));  // 8-byte elements either way
+        CK(dalloc(&ws.seen, n * W));
+        if (verify) CK(dalloc(&ws.ovf, n * W));
+        CK(dalloc(&ws.lane_w1, K));
+        CK(dalloc(&ws.lane_ns, K));
+        ws.W = W;
+        ws.verify = verify;
+    }
+    if (ws.hub_cap < nhub) {
+        dfree(ws.hub_acc);
+        dfree(ws.hub_ovf);
+        CK(dalloc((double **)&ws.hub_acc, (size_t)nhub * K));
+        CU(cudaMemset(ws.hub_acc, 0, (size_t)nhub * K * 8));
+        if (verify) {
+            CK(dalloc(&ws.hub_ovf, (size_t)nhub * W));
+            CU(cudaMemset(ws.hub_ovf, 0, (size_t)nhub * W * 8));
+        }
+        ws.hub_cap = nhub;
+    }
+    return BC_OK;
+}
+
+uint64_t *level_ptr(bc_graph *g, LaneWS &ws, int L) {
+    return ws.chunks[L / LCH] + (size_t)(L % LCH) * (size_t)g->n * ws.W;
+}
+
+bc_status ensure_level(bc_graph *g, LaneWS &ws, int L) {
+    while ((int)ws.chunks.size() * LCH <= L) {
+        uint64_t *c = nullptr;
+        CK(dalloc(&c, (size_t)g->n * ws.W * LCH));
+        ws.chunks.push_back(c);
+    }
+    return BC_OK;
+}
+
+__global__ void lane_setup_kernel(const int *src, int nl, int K, const uint32_t *omega, double *w1) {
+    int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l < K) w1[l] = (l < nl && omega) ? 1.0 + (double)omega[src[l]] : 1.0;
+}
+
+// occupancy-derived grid for the level kernels
+template <typename F>
+int level_grid(bc_graph *g, F kern, int units) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BC_NT, 0);
+    if (occ < 1) occ = 1;
+    int grid = g->num_sms * occ;
+    return std::max(1, std::min(grid, units));
+}
+
+struct BatchCtx {
+    const DevCSR *csr;
+    const uint32_t *omega;  // nullable
+    const int *src;         // device, nl entries
+    int nl;
+    cudaStream_t st;
+    double *dbg_delta;      // lane-0 delta (verification)
+    bool run_backward;
+    bool endpoint;
+    std::vector<uint64_t *> *lvl_out;  // verification: level masks used (nullable)
+    int *levels_out;
+};
+
+// Run one batch (forward + backward) with K = 64*W lanes.
+template <int W, typename SigT>
+bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cudaEvent_t> *ev_f,
+                    std::vector<cudaEvent_t> *ev_b) {
+    constexpr int K = 64 * W;
+    const int n = (int)g->n;
+    cudaStream_t st = c.st;
+    LanesParams p{};
+    p.n = n;
+    p.rp = c.csr->rp;
+    p.col = c.csr->col;
+    p.omega = c.omega;
+    p.seen = ws.seen;
+    p.S = ws.S;
+    p.ovf = ws.ovf;
+    p.bc = g->d_bc;
+    p.lane_w1 = ws.lane_w1;
+    p.lane_ns = c.omega ? ws.lane_ns : nullptr;
+    p.stats = g->d_stats;
+    p.work_ctr = g->d_work_ctr;
+    for (int j = 0; j < 4; ++j) p.active[j] = 0;
+    for (int l = 0; l < c.nl; ++l) p.active[l >> 6] |= 1ull << (l & 63);
+    p.hub_deg = g->hub_deg;
+    p.nhub = c.csr->nhub;
+    p.hub_ids = c.csr->hub_ids;
+    p.hub_seg_off = c.csr->hub_seg_off;
+    p.nseg = c.csr->nseg;
+    p.seg_len = g->hub_deg;
+    p.hub_acc = ws.hub_acc;
+    p.hub_ovf = ws.hub_ovf;
+    p.ntiles = (n + TV - 1) / TV;
+    p.dbg_delta = nullptr;
+
+    const size_t mbytes = (size_t)n * W * sizeof(uint64_t);
+    CK(ensure_level(g, ws, 1));
+    lane_setup_kernel<<<(K + 255) / 256, 256, 0, st>>>(c.src, c.nl, K, c.omega, ws.lane_w1);
+    CU(cudaMemsetAsync(ws.seen, 0, mbytes, st));
+    if (ws.ovf) CU(cudaMemsetAsync(ws.ovf, 0, mbytes, st));
+    CU(cudaMemsetAsync(level_ptr(g, ws, 0), 0, mbytes, st));
+    CU(cudaMemsetAsync(level_ptr(g, ws, 1), 0, mbytes, st));
+    p.any_new = g->d_flags + 1;
+    lanes_init_kernel<W, SigT><<<c.nl, BC_NT, 0, st>>>(p, c.src, level_ptr(g, ws, 0), level_ptr(g, ws, 1));
+    CU(cudaGetLastError());
+    g->last.kernel_launches += 2;
+
+    auto kf = lanes_level_kernel<W, SigT, false>;
+    const int units = p.nseg + p.ntiles;
+    const int grid = level_grid(g, kf, units);
+    const int hub_grid = (c.csr->nhub * 32 + BC_NT - 1) / BC_NT;
+
+    int L = 1;
+    for (;;) {
+        CK(ensure_level(g, ws, L + 1));
+        CK(ensure_flags(g, L + 2));
+        CU(cudaMemsetAsync(level_ptr(g, ws, L + 1), 0, mbytes, st));
+        CU(cudaMemsetAsync(g->d_flags + L + 1, 0, sizeof(int), st));
+        p.level = L;
+        p.mask_cur = level_ptr(g, ws, L);
+        p.mask_nxt = level_ptr(g, ws, L + 1);
+        p.mask_nxt_ro = nullptr;
+        p.any_new = g->d_flags + L + 1;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (ev_f) {
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            cudaEventRecord(e0, st);
+        }
+        kf<<<grid, BC_NT, 0, st>>>(p);
+        if (p.nhub > 0) lanes_hub_finalize<W, SigT, false><<<hub_grid, BC_NT, 0, st>>>(p);
+        if (ev_f) {
+            cudaEventRecord(e1, st);
+            ev_f->push_back(e0);
+            ev_f->push_back(e1);
+        }
+        CU(cudaGetLastError());
+        g->last.fwd_launches += 1;
+        g->last.kernel_launches += 1 + (p.nhub > 0);
+        CU(cudaMemcpyAsync(g->h_flag, g->d_flags + L + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        if (*g->h_flag == 0) break;
+        ++L;
+    }
+    const int Lmax = L;
+    g->last.levels_total += Lmax;
+    if (c.levels_out) *c.levels_out = Lmax;
+    if (c.lvl_out) {
+        c.lvl_out->clear();
+        for (int l = 0; l <= Lmax; ++l) c.lvl_out->push_back(level_ptr(g, ws, l));
+    }
+    if constexpr (std::is_same<SigT, double>::value) {
+        if (c.run_backward) {
+            auto kb = lanes_level_kernel<W, SigT, true>;
+            const int gridb = level_grid(g, kb, units);
+            p.dbg_delta = c.dbg_delta;
+            for (int l = Lmax; l >= 1; --l) {
+                p.level = l;
+                p.mask_cur = level_ptr(g, ws, l);
+                p.mask_nxt_ro = level_ptr(g, ws, l + 1);  // zero for l == Lmax
+                p.mask_nxt = nullptr;
+                p.any_new = g->d_flags;  // unused
+                cudaEvent_t e0 = nullptr, e1 = nullptr;
+                if (ev_b) {
+                    cudaEventCreate(&e0);
+                    cudaEventCreate(&e1);
+                    cudaEventRecord(e0, st);
+                }
+                kb<<<gridb, BC_NT, 0, st>>>(p);
+                if (p.nhub > 0) lanes_hub_finalize<W, SigT, true><<<hub_grid, BC_NT, 0, st>>>(p);
+                if (ev_b) {
+                    cudaEventRecord(e1, st);
+                    ev_b->push_back(e0);
+                    ev_b->push_back(e1);
+                }
+                CU(cudaGetLastError());
+                g->last.bwd_launches += 1;
+                g->last.kernel_launches += 1 + (p.nhub > 0);
+            }
+            if (c.endpoint && c.omega) {
+                lanes_endpoint_kernel<<<(c.nl + 255) / 256, 256, 0, st>>>(c.src, c.nl, c.omega, ws.lane_ns,
+                                                                         g->d_bc);
+                g->last.kernel_launches += 1;
+            }
+        }
+    }
+    CU(cudaGetLastError());
+    return BC_OK;
+}
+
+template <typename SigT>
+bc_status run_batch_w(bc_graph *g, LaneWS &ws, int W, const BatchCtx &c, std::vector<cudaEvent_t> *ef,
+                      std::vector<cudaEvent_t> *eb) {
+    switch (W) {
+        case 1: return run_batch<1, SigT>(g, ws, c, ef, eb);
+        case 2: return run_batch<2, SigT>(g, ws, c, ef, eb);
+        case 4: return run_batch<4, SigT>(g, ws, c, ef, eb);
+        default: return fail(BC_ERR_INTERNAL, "bad lane words %d", W);
+    }
+}
+
+bool is_device_ptr(const void *p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+double sum_events(std::vector<cudaEvent_t> &ev) {
+    double tot = 0;
+    for (size_t i = 0; i + 1 < ev.size(); i += 2) {
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, ev[i], ev[i + 1]) == cudaSuccess) tot += ms;
+        cudaEventDestroy(ev[i]);
+        cudaEventDestroy(ev[i + 1]);
+    }
+    (void)cudaGetLastError();
+    ev.clear();
+    return tot;
+}
+
+}  // namespace
+
+// =====================================================================
+extern "C" {
+
+const char *bc_status_string(bc_status s) {
+    switch (s) {
+        case BC_OK: return "BC_OK";
+        case BC_ERR_INVALID: return "BC_ERR_INVALID";
+        case BC_ERR_NOMEM: return "BC_ERR_NOMEM";
+        case BC_ERR_CUDA: return "BC_ERR_CUDA";
+        case BC_ERR_STATE: return "BC_ERR_STATE";
+        case BC_ERR_INTERNAL: return "BC_ERR_INTERNAL";
+    }
+    return "BC_ERR_UNKNOWN";
+}
+
+const char *bc_last_error(void) { return g_err.c_str(); }
+
+bc_status bc_destroy(bc_graph *g) {
+    if (!g) return BC_OK;
+    {
+        DeviceGuard dg(g->device);
+        cudaDeviceSynchronize();
+        g->orig.release();
+        g->res.release();
+        dfree(g->omega);
+        dfree(g->removed);
+        g->ws.release();
+        g->vws.release();
+        dfree(g->d_stats);
+        dfree(g->d_work_ctr);
+        dfree(g->d_flags);
+        dfree(g->d_src);
+        dfree(g->d_bc);
+        dfree(g->d_tmp);
+        if (g->h_flag) cudaFreeHost(g->h_flag);
+        if (g->own_stream) cudaStreamDestroy(g->own_stream);
+    }
+    delete g;
+    return BC_OK;
+}
+
+static bc_status create_impl(bc_graph *g, int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                             uint32_t flags) {
+    const int64_t nnz = row_ptr[n];
+    CU(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
+    cudaStream_t st = g->own_stream;
+    CU(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device));
+    CK(dalloc(&g->d_stats, 4));
+    CK(dalloc(&g->d_work_ctr, 4));
+    CU(cudaMemset(g->d_work_ctr, 0, 4 * sizeof(int)));
+    CK(ensure_flags(g, 64));
+    CU(cudaMallocHost((void **)&g->h_flag, sizeof(int)));
+    CK(dalloc(&g->d_bc, (size_t)n));
+    // CSR: int64 row_ptr -> int32 on device
+    long long *rp64 = nullptr;
+    CK(dalloc(&rp64, (size_t)n + 1));
+    CU(cudaMemcpy(rp64, row_ptr, ((size_t)n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+    CK(dalloc(&g->orig.rp, (size_t)n + 1));
+    rp64_to_32_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, st>>>(rp64, g->orig.rp, n + 1);
+    CK(dalloc(&g->orig.col, (size_t)nnz));
+    if (nnz > 0)
+        CU(cudaMemcpyAsync(g->orig.col, col_idx, (size_t)nnz * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    g->orig.nnz = nnz;
+    CU(cudaStreamSynchronize(st));
+    dfree(rp64);
+    if (flags & BC_CREATE_VALIDATE) {
+        int *err = nullptr;
+        CK(dalloc(&err, 1));
+        CU(cudaMemsetAsync(err, 0, sizeof(int), st));
+        validate_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>((int)n, g->orig.rp, g->orig.col, err);
+        int herr = 0;
+        CU(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        dfree(err);
+        if (herr) return fail(BC_ERR_INVALID, "CSR validation failed (flags 0x%x: 2=range 4=self-loop 8=unsorted/dup 16=asymmetric)", herr);
+    }
+    g->orig.h_deg.resize(n);
+    for (int64_t v = 0; v < n; ++v) g->orig.h_deg[v] = (int)(row_ptr[v + 1] - row_ptr[v]);
+    CK(build_hubs(g, g->orig, st));
+    return BC_OK;
+}
+
+bc_status bc_graph_create(int64_t n, const int64_t *row_ptr, const int32_t *col_idx, int device, uint32_t flags,
+                          bc_graph **out) {
+    if (!out) return fail(BC_ERR_INVALID, "out is NULL");
+    *out = nullptr;
+    if (n <= 0 || n > 2147483647LL) return fail(BC_ERR_INVALID, "n=%lld out of range [1, 2^31-1]", (long long)n);
+    if (!row_ptr) return fail(BC_ERR_INVALID, "row_ptr is NULL");
+    if (row_ptr[0] != 0) return fail(BC_ERR_INVALID, "row_ptr[0] != 0");
+    for (int64_t v = 0; v < n; ++v)
+        if (row_ptr[v + 1] < row_ptr[v]) return fail(BC_ERR_INVALID, "row_ptr decreasing at %lld", (long long)v);
+    if (row_ptr[n] > 2147483647LL) return fail(BC_ERR_INVALID, "row_ptr[n]=%lld exceeds 2^31-1", (long long)row_ptr[n]);
+    if (row_ptr[n] > 0 && !col_idx) return fail(BC_ERR_INVALID, "col_idx is NULL");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        (void)cudaGetLastError();
+        return fail(BC_ERR_CUDA, "no CUDA device available");
+    }
+    if (device < 0 || device >= ndev) return fail(BC_ERR_INVALID, "device %d out of range", device);
+    bc_graph *g = new (std::nothrow) bc_graph();
+    if (!g) return fail(BC_ERR_NOMEM, "host allocation failed");
+    g->device = device;
+    g->n = n;
+    bc_status s;
+    {
+        DeviceGuard dg(device);
+        s = create_impl(g, n, row_ptr, col_idx, flags);
+    }
+    if (s != BC_OK) {
+        std::string keep = g_err;
+        bc_destroy(g);
+        g_err = keep;
+        return s;
+    }
+    *out = g;
+    return BC_OK;
+}
+
+bc_status bc_prune_degree1(bc_graph *g, int64_t *out_removed) {
+    if (!g) return fail(BC_ERR_INVALID, "NULL handle");
+    if (g->pruned) return fail(BC_ERR_STATE, "graph already pruned (single pass, PAPER.md:580)");
+    DeviceGuard dg(g->device);
+    cudaStream_t st = g->own_stream;
+    const int n = (int)g->n;
+    CK(dalloc(&g->omega, n));
+    CK(dalloc(&g->removed, n));
+    int *rdeg = nullptr, *tot = nullptr;
+    CK(dalloc(&rdeg, n));
+    CK(dalloc(&tot, 1));
+    const unsigned wblocks = (unsigned)(((int64_t)n * 32 + 255) / 256);
+    prune_count_kernel<<<wblocks, 256, 0, st>>>(n, g->orig.rp, g->orig.col, g->omega, g->removed, rdeg);
+    CK(dalloc(&g->res.rp, (size_t)n + 1));
+    CK(dev_scan(g, rdeg, g->res.rp, n, tot, st));
+    CU(cudaMemcpyAsync(g->res.rp + n, tot, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    int rnnz = 0;
+    CU(cudaMemcpyAsync(&rnnz, tot, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    CK(dalloc(&g->res.col, (size_t)rnnz));
+    prune_compact_kernel<<<wblocks, 256, 0, st>>>(n, g->orig.rp, g->orig.col, g->res.rp, g->res.col);
+    CU(cudaGetLastError());
+    g->res.nnz = rnnz;
+    g->h_omega.resize(n);
+    g->h_removed.resize(n);
+    std::vector<int> rd(n);
+    CU(cudaMemcpyAsync(g->h_omega.data(), g->omega, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(g->h_removed.data(), g->removed, (size_t)n, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(rd.data(), rdeg, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    g->res.h_deg = rd;
+    dfree(rdeg);
+    dfree(tot);
+    g->pruned = true;
+    CK(build_hubs(g, g->res, st));
+    if (out_removed) {
+        int64_t r = 0;
+        for (int v = 0; v < n; ++v) r += g->h_removed[v];
+        *out_removed = r;
+    }
+    return BC_OK;
+}
+
+bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
+    if (!g) return fail(BC_ERR_INVALID, "NULL handle");
+    switch (option) {
+        case BC_OPT_LANE_WORDS:
+            if (value != 0 && value != 1 && value != 2 && value != 4)
+                return fail(BC_ERR_INVALID, "lane words must be 0, 1, 2 or 4");
+            g->lane_words_opt = (int)value;
+            return BC_OK;
+        case BC_OPT_HUB_DEGREE: {
+            if (value < 32 || value > (1 << 30)) return fail(BC_ERR_INVALID, "hub degree out of range");
+            if (g->hub_deg == (int)value) return BC_OK;
+            DeviceGuard dg(g->device);
+            g->hub_deg = (int)value;
+            CK(build_hubs(g, g->orig, g->own_stream));
+            if (g->pruned) CK(build_hubs(g, g->res, g->own_stream));
+            return BC_OK;
+        }
+        case BC_OPT_PROFILE:
+            g->profile = value ? 1 : 0;
+            return BC_OK;
+        case BC_OPT_MODE:
+            if (value < 0 || value > 2) return fail(BC_ERR_INVALID, "mode must be 0, 1 or 2");
+            g->mode = (int)value;
+            return BC_OK;
+    }
+    return fail(BC_ERR_INVALID, "unknown option %d", option);
+}
+
+bc_status bc_get_stats(const bc_graph *g, bc_stats *out) {
+    if (!g || !out) return fail(BC_ERR_INVALID, "NULL argument");
+    *out = g->last;
+    return BC_OK;
+}
+
+bc_status bc_graph_info(const bc_graph *g, int64_t *n, int64_t *nnz, int64_t *res_nnz, int *device) {
+    if (!g) return fail(BC_ERR_INVALID, "NULL handle");
+    if (n) *n = g->n;
+    if (nnz) *nnz = g->orig.nnz;
+    if (res_nnz) *res_nnz = g->pruned ? g->res.nnz : g->orig.nnz;
+    if (device) *device = g->device;
+    return BC_OK;
+}
+
+bc_status bc_get_pruning(const bc_graph *g, uint32_t *omega, uint8_t *removed, int64_t *res_row_ptr,
+                         int32_t *res_col, int64_t *res_nnz) {
+    if (!g) return fail(BC_ERR_INVALID, "NULL handle");
+    if (!g->pruned) return fail(BC_ERR_STATE, "graph is not pruned");
+    DeviceGuard dg(g->device);
+    const int64_t n = g->n;
+    if (omega) memcpy(omega, g->h_omega.data(), (size_t)n * 4);
+    if (removed) memcpy(removed, g->h_removed.data(), (size_t)n);
+    if (res_row_ptr) {
+        std::vector<int> rp(n + 1);
+        CU(cudaMemcpy(rp.data(), g->res.rp, (size_t)(n + 1) * 4, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i <= n; ++i) res_row_ptr[i] = rp[i];
+    }
+    if (res_col && g->res.nnz > 0)
+        CU(cudaMemcpy(res_col, g->res.col, (size_t)g->res.nnz * 4, cudaMemcpyDeviceToHost));
+    if (res_nnz) *res_nnz = g->res.nnz;
+    return BC_OK;
+}
+
+bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, double *out_bc, void *cuda_stream) {
+    if (!g) return fail(BC_ERR_INVALID, "NULL handle");
+    if (!out_bc) return fail(BC_ERR_INVALID, "out_bc is NULL");
+    if (num_sources < 0 || (num_sources > 0 && !sources)) return fail(BC_ERR_INVALID, "bad source list");
+    DeviceGuard dg(g->device);
+    const int64_t n = g->n;
+    DevCSR &csr = g->cur();
+    // ---- resolve and validate the source set (host-side argument checks)
+    std::vector<int> trav, triv;
+    if (!sources) {
+        for (int64_t v = 0; v < n; ++v) {
+            if (g->pruned && g->h_removed[v]) continue;
+            if (csr.h_deg[v] > 0) trav.push_back((int)v);
+            else if (g->pruned && g->h_omega[v] > 0) triv.push_back((int)v);
+        }
+    } else {
+        std::vector<uint8_t> mark((size_t)n, 0);
+        for (int64_t i = 0; i < num_sources; ++i) {
+            const int s = sources[i];
+            if (s < 0 || s >= n) return fail(BC_ERR_INVALID, "source %d out of range", s);
+            if (mark[s]) return fail(BC_ERR_INVALID, "duplicate source %d", s);
+            mark[s] = 1;
+            if (g->pruned && g->h_removed[s]) return fail(BC_ERR_INVALID, "source %d was removed by 1-degree pruning", s);
+            if (csr.h_deg[s] > 0) trav.push_back(s);
+            else if (g->pruned && g->h_omega[s] > 0) triv.push_back(s);
+        }
+    }
+    const bool dev_out = is_device_ptr(out_bc);
+    cudaStream_t st = cuda_stream ? (cudaStream_t)cuda_stream : g->own_stream;
+    g->last = bc_stats{};
+    g->last.num_sources = (int64_t)trav.size();
+    g->last.num_trivial = (int64_t)triv.size();
+    int W = g->lane_words_opt;
+    if (W == 0) W = trav.size() > 128 ? 4 : (trav.size() > 64 ? 2 : 1);
+    const int K = 64 * W;
+    g->last.lanes = K;
+    CK(ensure_ws(g, g->ws, W, false, csr.nhub));
+    const int64_t need = (int64_t)(trav.size() + triv.size());
+    if (g->src_cap < need) {
+        dfree(g->d_src);
+        CK(dalloc(&g->d_src, (size_t)need));
+        g->src_cap = need;
+    }
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (g->profile) {
+        cudaEventCreate(&t0);
+        cudaEventCreate(&t1);
+        cudaEventRecord(t0, st);
+    }
+    if (!trav.empty())
+        CU(cudaMemcpyAsync(g->d_src, trav.data(), trav.size() * 4, cudaMemcpyHostToDevice, st));
+    if (!triv.empty())
+        CU(cudaMemcpyAsync(g->d_src + trav.size(), triv.data(), triv.size() * 4, cudaMemcpyHostToDevice, st));
+    CU(cudaMemsetAsync(g->d_bc, 0, (size_t)n * 8, st));
+    CU(cudaMemsetAsync(g->d_stats, 0, 4 * sizeof(unsigned long long), st));
+    std::vector<cudaEvent_t> ef, eb;
+    for (size_t off = 0; off < trav.size(); off += K) {
+        BatchCtx c{};
+        c.csr = &csr;
+        c.omega = g->pruned ? g->omega : nullptr;
+        c.src = g->d_src + off;
+        c.nl = (int)std::min<size_t>(K, trav.size() - off);
+        c.st = st;
+        c.run_backward = true;
+        c.endpoint = true;
+        CK(run_batch_w<double>(g, g->ws, W, c, g->profile ? &ef : nullptr, g->profile ? &eb : nullptr));
+        g->last.batches += 1;
+    }
+    if (!triv.empty()) {
+        trivial_sources_kernel<<<(unsigned)((triv.size() + 255) / 256), 256, 0, st>>>(
+            g->d_src + trav.size(), (int)triv.size(), g->omega, g->d_bc);
+        g->last.kernel_launches += 1;
+    }
+    CU(cudaGetLastError());
+    unsigned long long hst[4] = {0, 0, 0, 0};
+    CU(cudaMemcpyAsync(hst, g->d_stats, sizeof(hst), cudaMemcpyDeviceToHost, st));
+    if (dev_out) {
+        CU(cudaMemcpyAsync(out_bc, g->d_bc, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
+    } else {
+        CU(cudaMemcpyAsync(out_bc, g->d_bc, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+    }
+    if (g->profile) cudaEventRecord(t1, st);
+    CU(cudaStreamSynchronize(st));
+    g->last.reached = (int64_t)hst[0];
+    g->last.adj_reached = (int64_t)hst[1];
+    g->last.dag_edges = (int64_t)hst[2];
+    g->last.dist_sum = (int64_t)hst[3];
+    if (g->profile) {
+        g->last.fwd_ms = sum_events(ef);
+        g->last.bwd_ms = sum_events(eb);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, t0, t1);
+        g->last.total_ms = ms;
+        cudaEventDestroy(t0);
+        cudaEventDestroy(t1);
+    }
+    return BC_OK;
+}
+
+__global__ static void gather_lane0_kernel(const void *S, int K, int n, const uint64_t *ovf, int W,
+                                           unsigned long long *sig, uint8_t *ov, const int *depth) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) {
+        const bool r = depth[v] >= 0;
+        sig[v] = r ? reinterpret_cast<const unsigned long long *>(S)[(size_t)v * K] : 0ull;
+        if (ov) ov[v] = (r && ovf) ? (uint8_t)(ovf[(size_t)v * W] & 1ull) : 0;
+    }
+}
+
+bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma, uint8_t *sigma_overflow,
+                  double *delta) {
+    if (!g) return fail(BC_ERR_INVALID, "NULL handle");
+    if (source < 0 || source >= g->n) return fail(BC_ERR_INVALID, "source %d out of range", source);
+    DeviceGuard dg(g->device);
+    const int n = (int)g->n;
+    cudaStream_t st = g->own_stream;
+    bc_stats keep = g->last;
+    CK(ensure_ws(g, g->vws, 1, true, g->orig.nhub));
+    if (g->src_cap < 1) {
+        dfree(g->d_src);
+        CK(dalloc(&g->d_src, 1));
+        g->src_cap = 1;
+    }
+    int *d_depth = nullptr;
+    unsigned long long *d_sig = nullptr;
+    uint8_t *d_ov = nullptr;
+    double *d_delta = nullptr;
+    CK(dalloc(&d_depth, n));
+    CK(dalloc(&d_sig, n));
+    CK(dalloc(&d_ov, n));
+    CK(dalloc(&d_delta, n));
+    CU(cudaMemcpyAsync(g->d_src, &source, 4, cudaMemcpyHostToDevice, st));
+    CU(cudaMemsetAsync(d_depth, 0xff, (size_t)n * 4, st));
+    CU(cudaMemsetAsync(d_delta, 0, (size_t)n * 8, st));
+    CU(cudaMemsetAsync(g->vws.S, 0, (size_t)n * 64 * 8, st));
+    bc_status s = BC_OK;
+    if (g->orig.h_deg[source] > 0) {
+        BatchCtx c{};
+        c.csr = &g->orig;
+        c.omega = nullptr;
+        c.src = g->d_src;
+        c.nl = 1;
+        c.st = st;
+        c.run_backward = false;
+        std::vector<uint64_t *> lv;
+        c.lvl_out = &lv;
+        int Lmax = 0;
+        c.levels_out = &Lmax;
+        s = run_batch<1, unsigned long long>(g, g->vws, c, nullptr, nullptr);
+        if (s == BC_OK) {
+            for (int l = 0; l <= Lmax; ++l)
+                depth_from_mask_kernel<<<(n + 255) / 256, 256, 0, st>>>(lv[l], n, 1, l, d_depth);
+            gather_lane0_kernel<<<(n + 255) / 256, 256, 0, st>>>(g->vws.S, 64, n, g->vws.ovf, 1, d_sig, d_ov, d_depth);
+            // fp64 pass for delta (uses the compute workspace at W = 1)
+            s = ensure_ws(g, g->ws, 1, false, g->orig.nhub);
+            if (s == BC_OK) {
+                CU(cudaMemsetAsync(g->d_bc, 0, (size_t)n * 8, st));
+                BatchCtx c2 = c;
+                c2.run_backward = true;
+                c2.endpoint = false;
+                c2.dbg_delta = d_delta;
+                c2.lvl_out = nullptr;
+                c2.levels_out = nullptr;
+                s = run_batch<1, double>(g, g->ws, c2, nullptr, nullptr);
+            }
+        }
+    } else {
+        CU(cudaMemsetAsync(d_sig, 0, (size_t)n * 8, st));
+        CU(cudaMemsetAsync(d_ov, 0, (size_t)n, st));
+        const int zero = 0;
+        CU(cudaMemcpyAsync(d_depth + source, &zero, 4, cudaMemcpyHostToDevice, st));
+        const unsigned long long one = 1;
+        CU(cudaMemcpyAsync(d_sig + source, &one, 8, cudaMemcpyHostToDevice, st));
+    }
+    if (s == BC_OK) {
+        CU(cudaGetLastError());
+        if (g->orig.h_deg[source] > 0) {
+            // gather above already ran; nothing else
+        }
+        if (depth) CU(cudaMemcpyAsync(depth, d_depth, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+        if (sigma) CU(cudaMemcpyAsync(sigma, d_sig, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+        if (sigma_overflow) CU(cudaMemcpyAsync(sigma_overflow, d_ov, (size_t)n, cudaMemcpyDeviceToHost, st));
+        if (delta) CU(cudaMemcpyAsync(delta, d_delta, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+    }
+    dfree(d_depth);
+    dfree(d_sig);
+    dfree(d_ov);
+    dfree(d_delta);
+    g->last = keep;
+    return s;
+}
+
+}  // extern "C"

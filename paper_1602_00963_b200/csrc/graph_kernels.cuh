@@ -1,0 +1,153 @@
+// graph_kernels.cuh -- device-side graph setup: CSR conversion and
+// validation, 1-degree pruning (Alg.6) and the hub list.
+#pragma once
+#include "util.cuh"
+
+namespace bcb {
+
+__global__ void rp64_to_32_kernel(const long long *rp64, int *rp32, long long n1) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n1) rp32[i] = (int)rp64[i];
+}
+
+// BC_CREATE_VALIDATE: rows strictly ascending, in range, no self-loops,
+// symmetric (binary search of v in adj(u)).  err |= bit on failure.
+__global__ void validate_kernel(int n, const int *rp, const int *col, int *err) {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = lane_id();
+    if (gw >= n) return;
+    const int v = gw;
+    const int a = rp[v], b = rp[v + 1];
+    int bad = 0;
+    if (b < a) bad |= 1;
+    for (int e = a + lane; e < b; e += 32) {
+        const int u = col[e];
+        if (u < 0 || u >= n) { bad |= 2; continue; }
+        if (u == v) bad |= 4;
+        if (e > a && col[e - 1] >= u) bad |= 8;
+        int lo = rp[u], hi = rp[u + 1] - 1, found = 0;
+        while (lo <= hi) {
+            int mid = (lo + hi) >> 1;
+            int c = col[mid];
+            if (c == v) { found = 1; break; }
+            if (c < v) lo = mid + 1;
+            else hi = mid - 1;
+        }
+        if (!found) bad |= 16;
+    }
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (lane == 0 && bad) atomicOr(err, bad);
+}
+
+// Alg.6 lines 3-9: u with a single edge is removed (R), omega of its
+// neighbour incremented.  Warp per vertex v: omega(v) = #neighbours of
+// degree 1; residual degree = #neighbours kept (0 if v itself is removed).
+__global__ void prune_count_kernel(int n, const int *rp, const int *col, uint32_t *omega, uint8_t *removed,
+                                   int *rdeg) {
+    const int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = lane_id();
+    if (v >= n) return;
+    const int a = rp[v], b = rp[v + 1];
+    const bool self_removed = (b - a) == 1;
+    int om = 0, keep = 0;
+    for (int e = a + lane; e < b; e += 32) {
+        const int u = col[e];
+        const bool u_removed = (rp[u + 1] - rp[u]) == 1;
+        om += u_removed;
+        keep += !u_removed;
+    }
+    om = __reduce_add_sync(0xffffffffu, om);
+    keep = __reduce_add_sync(0xffffffffu, keep);
+    if (lane == 0) {
+        omega[v] = (uint32_t)om;
+        removed[v] = self_removed ? 1 : 0;
+        rdeg[v] = self_removed ? 0 : keep;
+    }
+}
+
+// Alg.6 lines 10-11 + PAPER.md:590-591: residual edge list E' keeps (u,v)
+// when neither endpoint was removed; order within a row is preserved.
+__global__ void prune_compact_kernel(int n, const int *rp, const int *col, const int *rrp, int *rcol) {
+    const int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = lane_id();
+    if (v >= n) return;
+    const int a = rp[v], b = rp[v + 1];
+    if (b - a == 1) return;  // removed vertex: empty residual row
+    int out = rrp[v];
+    for (int e0 = a; e0 < b; e0 += 32) {
+        const int e = e0 + lane;
+        int u = 0;
+        bool keep = false;
+        if (e < b) {
+            u = col[e];
+            keep = (rp[u + 1] - rp[u]) != 1;
+        }
+        unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (keep) rcol[out + __popc(m & ((1u << lane) - 1u))] = u;
+        out += __popc(m);
+    }
+}
+
+// --- exclusive scan of int (values and total < 2^31), three phases
+constexpr int SCAN_ITEMS = 4;
+constexpr int SCAN_TILE = BC_NT * SCAN_ITEMS;
+
+__global__ void __launch_bounds__(BC_NT) scan_tiles_kernel(const int *in, int *out, int *tile_sums, long long n) {
+    __shared__ int sm[2 * BC_NW + 2];
+    const long long base = (long long)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+    int v[SCAN_ITEMS], s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        v[i] = (base + i < n) ? in[base + i] : 0;
+        s += v[i];
+    }
+    int ex, dummy, tot, dt;
+    block_excl_scan2(s, 0, ex, dummy, tot, dt, sm);
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        if (base + i < n) out[base + i] = ex;
+        ex += v[i];
+    }
+    if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(BC_NT) scan_sums_kernel(int *sums, int nt, int *total) {
+    __shared__ int sm[2 * BC_NW + 2];
+    int carry = 0;
+    for (int base = 0; base < nt; base += BC_NT) {
+        int i = base + threadIdx.x;
+        int v = i < nt ? sums[i] : 0;
+        int ex, d, tot, dt;
+        block_excl_scan2(v, 0, ex, d, tot, dt, sm);
+        if (i < nt) sums[i] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void scan_add_kernel(int *out, const int *sums, long long n) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] += sums[i / SCAN_TILE];
+}
+
+// hubs: vertices of degree > hub_deg; flags for a scan-based compaction
+__global__ void hub_flag_kernel(int n, const int *rp, int hub_deg, int *flag) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) flag[v] = (rp[v + 1] - rp[v]) > hub_deg ? 1 : 0;
+}
+
+__global__ void hub_scatter_kernel(int n, const int *flag, const int *pos, int *hub_ids) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n && flag[v]) hub_ids[pos[v]] = v;
+}
+
+__global__ void hub_segcount_kernel(int nhub, const int *hub_ids, const int *rp, int seg_len, int *cnt) {
+    const int h = blockIdx.x * blockDim.x + threadIdx.x;
+    if (h < nhub) {
+        const int x = hub_ids[h];
+        const int d = rp[x + 1] - rp[x];
+        cnt[h] = (d + seg_len - 1) / seg_len;
+    }
+}
+
+}  // namespace bcb

@@ -1,0 +1,639 @@
+// lanes.cuh -- multi-source ("bit-lane") Brandes level kernels for sm_100a.
+//
+// A batch holds K = 64*W sources; source j of the batch is lane j.  Per
+// vertex v the batch keeps
+//   lvl[L][v]  : W x uint64 -- lanes whose BFS puts v at depth L
+//   seen[v]    : W x uint64 -- lanes that have discovered v
+//   S[v][K]    : sigma_s(v) (forward), overwritten in place by
+//                coef_s(v) = (1 + omega(v) + delta_s(v)) / sigma_s(v)
+//                during the backward sweep (one array, two phases).
+//
+// Forward level L -> L+1 (Alg.2 / Alg.3; Alg.1 lines
+// 9-22): every vertex x with undiscovered lanes u = active & ~seen[x] pulls
+// from its neighbours v: c = u & lvl[L][v]; for each lane in c,
+// sigma(x) += sigma(v).  New lanes = lanes with sigma(x) > 0; they form
+// lvl[L+1][x].  Discovery is owner-computes (one CTA owns x), so neither the
+// depth nor sigma needs an atomic (reading R4 of DESIGN.md replaces Alg.3's
+// racy bmap test-and-set).
+//
+// Backward level L (Alg.4 / Alg.5, successor checking,
+// reading R2): every x with m = lvl[L][x] != 0 sums over successors v
+// (lanes in c = m & lvl[L+1][v]) acc += coef(v); then
+//   delta(x) = sigma(x) * acc                  (updateDep)
+//   coef(x)  = (1 + omega(x) + delta(x)) / sigma(x)        (Eq.5, line 1)
+//   BC[x]   += sum_lanes (1 + omega(s)) * (delta(x) + omega(x))    (R13)
+//
+// Edge-to-thread mapping ("active-edge parallelism"): a
+// CTA takes a tile of TV consecutive vertex ids, keeps the active ones,
+// block-scans their degrees into a shared-memory CD array (the frontier
+// offsets of the tile) and splits the tile's items evenly over its warps;
+// an item e is mapped to its vertex by binary search in CD.  Items are read
+// 32 consecutive per warp instruction (coalesced col reads) and several
+// steps are in flight per thread.  Vertices of degree > hub_deg are "hubs":
+// their adjacency is cut into segments (separate work units, any CTA) whose
+// partial sums meet in a per-hub scratch row via fp64 red.add, finalised by
+// lanes_hub_finalize.
+#pragma once
+#include <type_traits>
+#include "util.cuh"
+
+namespace bcb {
+
+constexpr int TV = BC_NT;  // vertices per tile
+
+template <typename T> struct Vec2;
+template <> struct Vec2<double> { using t = double2; };
+template <> struct Vec2<unsigned long long> { using t = ulonglong2; };
+
+struct LanesParams {
+    int n;
+    const int *rp;               // residual CSR row_ptr (int32, n+1)
+    const int *col;              // residual CSR columns
+    const uint32_t *omega;       // omega per vertex, nullable (unpruned)
+    const uint64_t *mask_cur;    // lvl[L]
+    const uint64_t *mask_nxt_ro; // backward: lvl[L+1]
+    uint64_t *mask_nxt;          // forward: lvl[L+1], pre-zeroed
+    uint64_t *seen;
+    void *S;                     // [n][K] SigT
+    uint64_t *ovf;               // verify variant: per-lane sigma overflow bits [n][W]
+    double *bc;
+    const double *lane_w1;       // [K] 1 + omega(source of lane)
+    double *lane_ns;             // [K] n_s accumulators, nullable
+    unsigned long long *stats;   // [4] reached, adjacency reached, dag edges, depth sum
+    int level;                   // L (forward: lvl[L] -> lvl[L+1]; backward: lvl[L])
+    int *any_new;
+    int *work_ctr;               // self-resetting dynamic tile counter
+    uint64_t active[4];          // lanes in use
+    int hub_deg;
+    int nhub;
+    const int *hub_ids;
+    const int *hub_seg_off;      // [nhub+1] prefix of segment counts
+    int nseg;
+    int seg_len;
+    void *hub_acc;               // [nhub][K] SigT, zero between levels
+    uint64_t *hub_ovf;           // verify: [nhub][W]
+    int ntiles;
+    double *dbg_delta;           // backward: delta of lane 0 (verification), nullable
+};
+
+template <int W, typename SigT>
+struct LanesSmem {
+    int vert[TV];
+    int cd[TV + 1];
+    int rs[TV];
+    uint64_t u[TV * W];
+    SigT part[BC_NW * 2 * 64 * W];
+    uint32_t povf[BC_NW * 2 * 32];
+    int scan[2 * BC_NW + 2];
+    int unit;
+};
+
+template <int W, typename SigT, bool BWD>
+struct LanesKernel {
+    static constexpr int K = 64 * W;
+    static constexpr int LPT = 2 * W;           // lanes per thread
+    static constexpr int R = (W == 1) ? 4 : 2;  // item steps in flight per warp
+    static constexpr int U = (W == 1) ? 4 : 2;  // sigma rows in flight per warp
+    static constexpr bool VERIFY = std::is_same<SigT, unsigned long long>::value;
+    static constexpr int GROUP = 32 / W;        // threads sharing one mask word
+    using V = typename Vec2<SigT>::t;
+    using Smem = LanesSmem<W, SigT>;
+
+    const LanesParams &p;
+    Smem &sm;
+    const int lane, wid, my_word, my_off;
+    const uint64_t lm;
+    double w1[LPT];
+    double ns_loc[LPT];
+    unsigned long long st_reach = 0, st_adj = 0, st_dag = 0, st_dsum = 0;
+    int any_new_loc = 0;
+
+    __device__ LanesKernel(const LanesParams &pp, Smem &s)
+        : p(pp), sm(s), lane(lane_id()), wid(warp_id()), my_word((lane_id() * LPT) >> 6),
+          my_off((lane_id() * LPT) & 63), lm((1ull << LPT) - 1ull) {
+#pragma unroll
+        for (int i = 0; i < LPT; ++i) {
+            w1[i] = BWD ? p.lane_w1[lane * LPT + i] : 0.0;
+            ns_loc[i] = 0.0;
+        }
+    }
+
+    __device__ __forceinline__ SigT *S() const { return reinterpret_cast<SigT *>(p.S); }
+
+    // ---- forward commit: x discovered in the lanes where acc != 0 (or overflowed)
+    __device__ void commit_fwd(int x, int deg, const SigT (&acc)[LPT], uint32_t aovf) {
+        uint32_t nb = aovf;
+#pragma unroll
+        for (int i = 0; i < LPT; ++i)
+            if (acc[i] != SigT(0)) nb |= 1u << i;
+        if (nb) {
+            SigT *row = S() + (size_t)x * K + lane * LPT;
+#pragma unroll
+            for (int pr = 0; pr < W; ++pr) {
+                uint32_t b = (nb >> (2 * pr)) & 3u;
+                if (b == 3u) {
+                    V t;
+                    t.x = acc[2 * pr];
+                    t.y = acc[2 * pr + 1];
+                    reinterpret_cast<V *>(row)[pr] = t;
+                } else if (b == 1u) {
+                    row[2 * pr] = acc[2 * pr];
+                } else if (b == 2u) {
+                    row[2 * pr + 1] = acc[2 * pr + 1];
+                }
+            }
+            any_new_loc = 1;
+            int pc = __popc(nb);
+            st_reach += pc;
+            st_adj += (unsigned long long)pc * deg;
+            st_dsum += (unsigned long long)pc * (unsigned)(p.level + 1);
+            if (p.lane_ns) {
+                double wx = 1.0 + (p.omega ? (double)p.omega[x] : 0.0);
+#pragma unroll
+                for (int i = 0; i < LPT; ++i)
+                    if (nb >> i & 1u) ns_loc[i] += wx;
+            }
+        }
+        uint64_t wv = (uint64_t)nb << my_off;
+        uint64_t ov = (uint64_t)aovf << my_off;
+#pragma unroll
+        for (int o = 1; o < GROUP; o <<= 1) {
+            wv |= __shfl_xor_sync(0xffffffffu, wv, o);
+            if (VERIFY) ov |= __shfl_xor_sync(0xffffffffu, ov, o);
+        }
+        if ((lane & (GROUP - 1)) == 0 && wv) {
+            size_t wi = (size_t)x * W + my_word;
+            p.mask_nxt[wi] = wv;
+            p.seen[wi] |= wv;
+            if (VERIFY && ov) p.ovf[wi] |= ov;
+        }
+    }
+
+    // ---- backward commit: finalise x at level L in the lanes of mb
+    __device__ void commit_bwd(int x, uint32_t mb, const SigT (&acc)[LPT]) {
+        double contrib = 0.0;
+        if (mb) {
+            double om = p.omega ? (double)p.omega[x] : 0.0;
+            SigT *row = S() + (size_t)x * K + lane * LPT;
+#pragma unroll
+            for (int pr = 0; pr < W; ++pr) {
+                uint32_t b = (mb >> (2 * pr)) & 3u;
+                if (!b) continue;
+                V sg = reinterpret_cast<const V *>(row)[pr];
+                if (b & 1u) {
+                    double sig = (double)sg.x;
+                    double delta = sig * (double)acc[2 * pr];
+                    row[2 * pr] = (SigT)((1.0 + om + delta) / sig);
+                    contrib += w1[2 * pr] * (delta + om);
+                    if (p.dbg_delta && lane == 0 && pr == 0) p.dbg_delta[x] = delta;
+                }
+                if (b & 2u) {
+                    double sig = (double)sg.y;
+                    double delta = sig * (double)acc[2 * pr + 1];
+                    row[2 * pr + 1] = (SigT)((1.0 + om + delta) / sig);
+                    contrib += w1[2 * pr + 1] * (delta + om);
+                }
+            }
+        }
+        contrib = warp_sum(contrib);
+        if (lane == 0 && contrib != 0.0) p.bc[x] += contrib;
+    }
+
+    __device__ void commit_slot(int s, const SigT (&acc)[LPT], uint32_t aovf) {
+        if (BWD) {
+            uint32_t mb = (uint32_t)((sm.u[s * W + my_word] >> my_off) & lm);
+            commit_bwd(sm.vert[s], mb, acc);
+        } else {
+            commit_fwd(sm.vert[s], sm.cd[s + 1] - sm.cd[s], acc, aovf);
+        }
+    }
+
+    // flush the running accumulator of slot s (warp-uniform)
+    __device__ void flush(int s, int first, int ws, int we, bool hub_mode, const SigT (&acc)[LPT],
+                          uint32_t aovf) {
+        bool owned = !hub_mode && sm.cd[s] >= ws && sm.cd[s + 1] <= we;
+        if (owned) {
+            commit_slot(s, acc, aovf);
+        } else {
+            int idx = (s == first) ? 0 : 1;
+            SigT *dst = sm.part + (wid * 2 + idx) * K + lane * LPT;
+#pragma unroll
+            for (int i = 0; i < LPT; ++i) dst[i] = acc[i];
+            if (VERIFY) sm.povf[(wid * 2 + idx) * 32 + lane] = aovf;
+        }
+    }
+
+    // One warp walks items [ws, we) of the current tile (slots in sm).
+    __device__ void warp_walk(int nslots, int ws, int we, bool hub_mode) {
+        const uint64_t *mread = BWD ? p.mask_nxt_ro : p.mask_cur;
+        int cur = slot_of(sm.cd, nslots, ws);
+        const int first = cur;
+        const int last = slot_of(sm.cd, nslots, we - 1);
+        SigT acc[LPT];
+#pragma unroll
+        for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
+        uint32_t aovf = 0;
+        const uint64_t pol = policy_evict_first();
+
+        for (int e0 = ws; e0 < we; e0 += 32 * R) {
+            int sl[R], vv[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                int e = e0 + k * 32 + lane;
+                sl[k] = -1;
+                vv[k] = 0;
+                if (e < we) {
+                    int s = slot_of(sm.cd, nslots, e);
+                    sl[k] = s;
+                    vv[k] = ld_stream(p.col + sm.rs[s] + (e - sm.cd[s]), pol);
+                }
+            }
+            uint64_t cc[R][W];
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+#pragma unroll
+                for (int j = 0; j < W; ++j) {
+                    cc[k][j] = 0;
+                    if (sl[k] >= 0) cc[k][j] = sm.u[sl[k] * W + j] & __ldg(mread + (size_t)vv[k] * W + j);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                bool h = false;
+#pragma unroll
+                for (int j = 0; j < W; ++j) h |= (cc[k][j] != 0);
+                unsigned hm = __ballot_sync(0xffffffffu, h);
+                while (hm) {
+                    int src[U], hs[U], hv[U];
+                    uint32_t mb[U];
+#pragma unroll
+                    for (int q = 0; q < U; ++q) {
+                        src[q] = hm ? (__ffs(hm) - 1) : -1;
+                        if (hm) hm &= hm - 1;
+                    }
+#pragma unroll
+                    for (int q = 0; q < U; ++q) {
+                        hs[q] = -1;
+                        hv[q] = 0;
+                        mb[q] = 0;
+                        if (src[q] >= 0) {
+                            hs[q] = __shfl_sync(0xffffffffu, sl[k], src[q]);
+                            hv[q] = __shfl_sync(0xffffffffu, vv[k], src[q]);
+                            uint64_t w = 0;
+#pragma unroll
+                            for (int j = 0; j < W; ++j) {
+                                uint64_t cw = __shfl_sync(0xffffffffu, cc[k][j], src[q]);
+                                if (j == my_word) w = cw;
+                            }
+                            mb[q] = (uint32_t)((w >> my_off) & lm);
+                        }
+                    }
+                    V val[U][W];
+                    uint32_t po[U];
+#pragma unroll
+                    for (int q = 0; q < U; ++q) {
+                        const V *rowv = reinterpret_cast<const V *>(S() + (size_t)hv[q] * K + lane * LPT);
+#pragma unroll
+                        for (int pr = 0; pr < W; ++pr) {
+                            val[q][pr].x = SigT(0);
+                            val[q][pr].y = SigT(0);
+                            if ((mb[q] >> (2 * pr)) & 3u) val[q][pr] = __ldg(rowv + pr);
+                        }
+                        po[q] = 0;
+                        if (VERIFY && mb[q])
+                            po[q] = mb[q] & (uint32_t)((__ldg(p.ovf + (size_t)hv[q] * W + my_word) >> my_off) & lm);
+                    }
+#pragma unroll
+                    for (int q = 0; q < U; ++q) {
+                        if (src[q] < 0) continue;
+                        if (hs[q] != cur) {
+                            while (cur < hs[q]) {
+                                flush(cur, first, ws, we, hub_mode, acc, aovf);
+                                ++cur;
+#pragma unroll
+                                for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
+                                aovf = 0;
+                            }
+                        }
+#pragma unroll
+                        for (int pr = 0; pr < W; ++pr) {
+                            if (mb[q] >> (2 * pr) & 1u) {
+                                SigT o = acc[2 * pr];
+                                acc[2 * pr] = o + val[q][pr].x;
+                                if (VERIFY && acc[2 * pr] < o) aovf |= 1u << (2 * pr);
+                            }
+                            if (mb[q] >> (2 * pr + 1) & 1u) {
+                                SigT o = acc[2 * pr + 1];
+                                acc[2 * pr + 1] = o + val[q][pr].y;
+                                if (VERIFY && acc[2 * pr + 1] < o) aovf |= 1u << (2 * pr + 1);
+                            }
+                        }
+                        aovf |= po[q];
+                        if (!BWD) st_dag += __popc(mb[q]);
+                    }
+                }
+            }
+        }
+        while (cur <= last) {
+            flush(cur, first, ws, we, hub_mode, acc, aovf);
+            ++cur;
+#pragma unroll
+            for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
+            aovf = 0;
+        }
+    }
+
+    __device__ __forceinline__ static int bnd(int j, int nitems) {
+        return (int)(((long long)j * nitems) / BC_NW);
+    }
+
+    // ---- a tile of TV consecutive vertices
+    __device__ void tile(int t) {
+        const int x = t * TV + threadIdx.x;
+        int deg = 0, act = 0;
+        uint64_t u[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) u[j] = 0;
+        int rs = 0;
+        if (x < p.n) {
+            rs = p.rp[x];
+            deg = p.rp[x + 1] - rs;
+            if (deg > 0 && deg <= p.hub_deg) {
+#pragma unroll
+                for (int j = 0; j < W; ++j) {
+                    if (BWD) u[j] = p.mask_cur[(size_t)x * W + j];
+                    else u[j] = p.active[j] & ~p.seen[(size_t)x * W + j];
+                    act |= (u[j] != 0);
+                }
+            }
+        }
+        int slot, cd, nslots, nitems;
+        block_excl_scan2(act, act ? deg : 0, slot, cd, nslots, nitems, sm.scan);
+        if (act) {
+            sm.vert[slot] = x;
+            sm.cd[slot] = cd;
+            sm.rs[slot] = rs;
+#pragma unroll
+            for (int j = 0; j < W; ++j) sm.u[slot * W + j] = u[j];
+        }
+        if (threadIdx.x == 0) sm.cd[nslots] = nitems;
+        __syncthreads();
+        if (nslots == 0) return;
+        const int ws = bnd(wid, nitems), we = bnd(wid + 1, nitems);
+        if (ws < we) warp_walk(nslots, ws, we, false);
+        __syncthreads();
+        // slots split across warps: warp j finalises the slot holding boundary j
+        if (wid >= 1) {
+            const int b = bnd(wid, nitems);
+            if (b > 0 && b < nitems) {
+                const int s = slot_of(sm.cd, nslots, b);
+                if (sm.cd[s] < b && (wid == 1 || bnd(wid - 1, nitems) <= sm.cd[s])) {
+                    SigT acc[LPT];
+#pragma unroll
+                    for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
+                    uint32_t aovf = 0;
+                    for (int w = 0; w < BC_NW; ++w) {
+                        int a0 = bnd(w, nitems), a1 = bnd(w + 1, nitems);
+                        if (a0 >= a1 || a1 <= sm.cd[s] || a0 >= sm.cd[s + 1]) continue;
+                        int idx = (sm.cd[s] <= a0) ? 0 : 1;
+                        const SigT *src = sm.part + (w * 2 + idx) * K + lane * LPT;
+#pragma unroll
+                        for (int i = 0; i < LPT; ++i) {
+                            SigT o = acc[i];
+                            acc[i] = o + src[i];
+                            if (VERIFY && acc[i] < o) aovf |= 1u << i;
+                        }
+                        if (VERIFY) aovf |= sm.povf[(w * 2 + idx) * 32 + lane];
+                    }
+                    commit_slot(s, acc, aovf);
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- one segment of a hub's adjacency
+    __device__ void hub_segment(int unit) {
+        if (threadIdx.x == 0) {
+            int lo = 0, hi = p.nhub - 1;
+            while (lo < hi) {
+                int mid = (lo + hi + 1) >> 1;
+                if (p.hub_seg_off[mid] <= unit) lo = mid;
+                else hi = mid - 1;
+            }
+            sm.scan[0] = lo;
+        }
+        __syncthreads();
+        const int h = sm.scan[0];
+        __syncthreads();
+        const int x = p.hub_ids[h];
+        const int seg = unit - p.hub_seg_off[h];
+        const int a = p.rp[x] + seg * p.seg_len;
+        const int b = min(p.rp[x + 1], a + p.seg_len);
+        uint64_t u[W];
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            if (BWD) u[j] = p.mask_cur[(size_t)x * W + j];
+            else u[j] = p.active[j] & ~p.seen[(size_t)x * W + j];
+            any |= (u[j] != 0);
+        }
+        if (!any) return;  // uniform
+        if (threadIdx.x == 0) {
+            sm.vert[0] = x;
+            sm.cd[0] = 0;
+            sm.cd[1] = b - a;
+            sm.rs[0] = a;
+#pragma unroll
+            for (int j = 0; j < W; ++j) sm.u[j] = u[j];
+        }
+        __syncthreads();
+        const int nitems = b - a;
+        const int ws = bnd(wid, nitems), we = bnd(wid + 1, nitems);
+        if (ws < we) warp_walk(1, ws, we, true);
+        __syncthreads();
+        // lane-wise reduction over warps, then one red.add per lane into the hub row
+        for (int l = threadIdx.x; l < K; l += BC_NT) {
+            SigT sum = SigT(0);
+            bool ovf = false;
+            const int tl = l / LPT, ti = l % LPT;
+            for (int w = 0; w < BC_NW; ++w) {
+                if (bnd(w, nitems) >= bnd(w + 1, nitems)) continue;
+                SigT o = sum;
+                sum = o + sm.part[(w * 2) * K + l];
+                if (VERIFY && sum < o) ovf = true;
+                if (VERIFY && (sm.povf[(w * 2) * 32 + tl] >> ti & 1u)) ovf = true;
+            }
+            if (sum != SigT(0)) {
+                SigT *dst = reinterpret_cast<SigT *>(p.hub_acc) + (size_t)h * K + l;
+                SigT old = atomicAdd(dst, sum);
+                if (VERIFY && old + sum < old) ovf = true;
+            }
+            if (VERIFY && ovf) atomicOr((unsigned long long *)(p.hub_ovf + (size_t)h * W + (l >> 6)), 1ull << (l & 63));
+        }
+        __syncthreads();
+    }
+
+    __device__ void epilogue() {
+        unsigned long long a = warp_sum_u64(st_reach), b = warp_sum_u64(st_adj), c = warp_sum_u64(st_dag),
+                           d = warp_sum_u64(st_dsum);
+        if (lane == 0) {
+            if (a) atomicAdd(p.stats + 0, a);
+            if (b) atomicAdd(p.stats + 1, b);
+            if (c) atomicAdd(p.stats + 2, c);
+            if (d) atomicAdd(p.stats + 3, d);
+        }
+        int anyw = __any_sync(0xffffffffu, any_new_loc);
+        if (lane == 0 && anyw) *p.any_new = 1;
+        if (!BWD && p.lane_ns) {
+            double *red = reinterpret_cast<double *>(sm.part);
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < LPT; ++i) red[wid * K + lane * LPT + i] = ns_loc[i];
+            __syncthreads();
+            for (int l = threadIdx.x; l < K; l += BC_NT) {
+                double s = 0.0;
+                for (int w = 0; w < BC_NW; ++w) s += red[w * K + l];
+                if (s != 0.0) atomicAdd(p.lane_ns + l, s);
+            }
+        }
+    }
+};
+
+template <int W, typename SigT, bool BWD>
+__global__ void __launch_bounds__(BC_NT) lanes_level_kernel(LanesParams p) {
+    __shared__ LanesSmem<W, SigT> sm;
+    LanesKernel<W, SigT, BWD> k(p, sm);
+    const int total = p.nseg + p.ntiles;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            int t = atomicAdd(p.work_ctr, 1);
+            if (t == total + (int)gridDim.x - 1) *p.work_ctr = 0;  // last fetch resets
+            sm.unit = t;
+        }
+        __syncthreads();
+        const int unit = sm.unit;
+        __syncthreads();
+        if (unit >= total) break;
+        if (unit < p.nseg) k.hub_segment(unit);
+        else k.tile(unit - p.nseg);
+    }
+    k.epilogue();
+}
+
+// One warp per hub: commit the hub's summed row (forward) or finalise it
+// (backward).  Resets the scratch row for the next level.
+template <int W, typename SigT, bool BWD>
+__global__ void __launch_bounds__(BC_NT) lanes_hub_finalize(LanesParams p) {
+    using KK = LanesKernel<W, SigT, BWD>;
+    constexpr int K = KK::K, LPT = KK::LPT;
+    __shared__ LanesSmem<W, SigT> sm;
+    KK k(p, sm);
+    const int h = (blockIdx.x * BC_NT + threadIdx.x) >> 5;
+    if (h < p.nhub) {
+        const int x = p.hub_ids[h];
+        SigT *row = reinterpret_cast<SigT *>(p.hub_acc) + (size_t)h * K + k.lane * LPT;
+        SigT acc[LPT];
+#pragma unroll
+        for (int i = 0; i < LPT; ++i) {
+            acc[i] = row[i];
+            if (acc[i] != SigT(0)) row[i] = SigT(0);
+        }
+        if (BWD) {
+            uint32_t mb = (uint32_t)((p.mask_cur[(size_t)x * W + k.my_word] >> k.my_off) & k.lm);
+            k.commit_bwd(x, mb, acc);
+        } else {
+            uint32_t aovf = 0;
+            if (KK::VERIFY) {
+                uint64_t *ow = p.hub_ovf + (size_t)h * W + k.my_word;
+                aovf = (uint32_t)((*ow >> k.my_off) & k.lm);
+                __syncwarp();
+                if ((k.lane & (KK::GROUP - 1)) == 0) *ow = 0;
+            }
+            k.commit_fwd(x, p.rp[x + 1] - p.rp[x], acc, aovf);
+        }
+    }
+    k.epilogue();
+}
+
+// Levels 0 and 1 of every lane (Alg.2 lines 7-12 plus the first expansion):
+// one CTA per lane pushes sigma = 1 to the source's neighbours.
+template <int W, typename SigT>
+__global__ void __launch_bounds__(BC_NT) lanes_init_kernel(LanesParams p, const int *src, uint64_t *mask0,
+                                                            uint64_t *mask1) {
+    constexpr int K = 64 * W;
+    __shared__ double red_d[BC_NW];
+    __shared__ unsigned long long red_u[BC_NW];
+    const int l = blockIdx.x;
+    const int s = src[l];
+    const int word = l >> 6;
+    const uint64_t bit = 1ull << (l & 63);
+    SigT *S = reinterpret_cast<SigT *>(p.S);
+    const int rs = p.rp[s], re = p.rp[s + 1];
+    if (threadIdx.x == 0) {
+        atomicOr((unsigned long long *)(mask0 + (size_t)s * W + word), (unsigned long long)bit);
+        atomicOr((unsigned long long *)(p.seen + (size_t)s * W + word), (unsigned long long)bit);
+        S[(size_t)s * K + l] = SigT(1);
+    }
+    double cnt = 0.0;
+    unsigned long long adj = 0;
+    for (int e = rs + threadIdx.x; e < re; e += BC_NT) {
+        const int w = p.col[e];
+        atomicOr((unsigned long long *)(mask1 + (size_t)w * W + word), (unsigned long long)bit);
+        atomicOr((unsigned long long *)(p.seen + (size_t)w * W + word), (unsigned long long)bit);
+        S[(size_t)w * K + l] = SigT(1);
+        cnt += 1.0 + (p.omega ? (double)p.omega[w] : 0.0);
+        adj += (unsigned long long)(p.rp[w + 1] - p.rp[w]);
+    }
+    cnt = warp_sum(cnt);
+    adj = warp_sum_u64(adj);
+    if (lane_id() == 0) {
+        red_d[warp_id()] = cnt;
+        red_u[warp_id()] = adj;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double c = 0.0;
+        unsigned long long a = 0;
+        for (int w = 0; w < BC_NW; ++w) {
+            c += red_d[w];
+            a += red_u[w];
+        }
+        const int deg = re - rs;
+        if (p.lane_ns) p.lane_ns[l] = 1.0 + (p.omega ? (double)p.omega[s] : 0.0) + c;
+        atomicAdd(p.stats + 0, (unsigned long long)(1 + deg));
+        atomicAdd(p.stats + 1, (unsigned long long)deg + a);
+        atomicAdd(p.stats + 2, (unsigned long long)deg);
+        atomicAdd(p.stats + 3, (unsigned long long)deg);
+        if (deg > 0) *p.any_new = 1;
+    }
+}
+
+// Endpoint term of the attributed 1-degree form (R13): BC[s] += omega(s)(n_s - 2).
+__global__ void lanes_endpoint_kernel(const int *src, int nlanes, const uint32_t *omega, const double *lane_ns,
+                                      double *bc) {
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l < nlanes) {
+        const int s = src[l];
+        const double om = (double)omega[s];
+        if (om != 0.0) bc[s] += om * (lane_ns[l] - 2.0);
+    }
+}
+
+// Residual-isolated sources with omega > 0 (R10): n_s = 1 + omega(s).
+__global__ void trivial_sources_kernel(const int *src, int ns, const uint32_t *omega, double *bc) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < ns) {
+        const int s = src[i];
+        const double om = (double)omega[s];
+        bc[s] += om * (om - 1.0);
+    }
+}
+
+// verification: depth of lane 0 from the level masks
+__global__ void depth_from_mask_kernel(const uint64_t *mask, int n, int W, int L, int *depth) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n && (mask[(size_t)v * W] & 1ull)) depth[v] = L;
+}
+
+}  // namespace bcb

@@ -1,0 +1,234 @@
+"""Parity of the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerance: per vertex |gpu - oracle| <= 1e-9 * |oracle|
+with exact zeros where the oracle is exactly zero (every BC term is
+non-negative, so there is no cancellation; measured fp64 error is ~1e-15).
+Integer outputs (depth, sigma < 2^64, overflow flags, omega, removed flags,
+residual CSR) are compared bit-exactly."""
+import numpy as np
+import pytest
+
+import graphgen as gg
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-9
+
+
+def _bcb():
+    import paper_1602_00963_b200 as bcb
+
+    return bcb
+
+
+def assert_bc_close(got, want, rtol=RTOL):
+    got = np.asarray(got)
+    want = np.asarray(want)
+    assert got.shape == want.shape
+    if got.size == 0:
+        return
+    zero = want == 0.0
+    assert np.all(got[zero] == 0.0), f"nonzero where oracle is exactly 0: {np.nonzero(got[zero])[0][:10]}"
+    rel = np.abs(got - want) / np.where(zero, 1.0, np.abs(want))
+    i = int(np.argmax(rel))
+    assert rel.max() <= rtol, f"max rel err {rel.max():.3e} at {i}: gpu {got[i]!r} oracle {want[i]!r}"
+
+
+def small_suite():
+    out = []
+    for i in range(24):
+        n = 3 + (i * 5) % 40
+        out.append(gg.erdos_renyi(n, (0.05, 0.1, 0.3)[i % 3], seed=700 + i))
+    for i in range(12):
+        out.append(gg.rmat(4 + i % 5, (2, 8, 16)[i % 3], seed=800 + i))
+    for i in range(8):
+        out.append(gg.with_isolated(gg.disjoint_union(gg.random_tree(5 + i, seed=i), gg.path(2), gg.star(4),
+                                                      gg.cycle(5 + i)), i % 3))
+    out += [gg.path(2), gg.path(3), gg.path(17), gg.cycle(9), gg.complete(6), gg.star(7),
+            gg.complete_bipartite(3, 5), gg.hypercube(5), gg.petersen(), gg.grid(7, 9), gg.from_pairs(5, [])]
+    return out
+
+
+SUITE = small_suite()
+
+
+@pytest.mark.parametrize("words", [1, 2, 4])
+@pytest.mark.parametrize("hub", [32, 4096])
+def test_small_suite_all_sources(words, hub):
+    bcb = _bcb()
+    for g in SUITE:
+        with bcb.Graph.from_csr(g, validate=True) as G:
+            G.set_option(bcb.OPT_LANE_WORDS, words)
+            G.set_option(bcb.OPT_HUB_DEGREE, hub)
+            assert_bc_close(G.compute(), oracle.bc(g))
+
+
+@pytest.mark.parametrize("hub", [32, 4096])
+def test_small_suite_pruned(hub):
+    bcb = _bcb()
+    for g in SUITE:
+        with bcb.Graph.from_csr(g) as G:
+            G.set_option(bcb.OPT_HUB_DEGREE, hub)
+            G.prune_degree1()
+            assert_bc_close(G.compute(), oracle.bc(g))
+            om, rm, rrp, rcol = oracle.prune_degree1(g)
+            gom, grm, grp, gcol = G.pruning()
+            assert np.array_equal(gom, om) and np.array_equal(grm, rm)
+            assert np.array_equal(grp, rrp) and np.array_equal(gcol, rcol)
+
+
+def test_pruned_partial_sources_equal_S_plus():
+    bcb = _bcb()
+    rng = np.random.default_rng(3)
+    for g in SUITE[:30]:
+        om, rm, rrp, rcol = oracle.prune_degree1(g)
+        res_deg = np.diff(rrp)
+        elig = [v for v in range(g.n) if not rm[v] and (res_deg[v] > 0 or om[v] > 0)]
+        if not elig:
+            continue
+        S = sorted(rng.choice(elig, size=max(1, len(elig) // 2), replace=False).tolist())
+        Splus = set(S)
+        for s in S:
+            Splus.update(int(u) for u in g.col[g.row_ptr[s]:g.row_ptr[s + 1]] if rm[u])
+        with bcb.Graph.from_csr(g) as G:
+            G.prune_degree1()
+            assert_bc_close(G.compute(S), oracle.bc(g, sorted(Splus)))
+
+
+def test_multibatch_ragged_tail_and_additivity():
+    bcb = _bcb()
+    g = gg.rmat(11, 16, seed=4)
+    S = g.non_isolated()[:300]  # 256 + 44 at K = 256, 64*4 + 44 at K = 64
+    want = oracle.bc(g, S)
+    with bcb.Graph.from_csr(g) as G:
+        for words in (1, 4):
+            G.set_option(bcb.OPT_LANE_WORDS, words)
+            got = G.compute(S)
+            assert_bc_close(got, want)
+        parts = sum(G.compute(S[r::3]) for r in range(3))
+        assert_bc_close(parts, want)
+
+
+def test_config1_rmat12_all_sources():
+    """BASELINE config 1: R-MAT scale 12 EF16, all 4096 sources."""
+    bcb = _bcb()
+    g = gg.rmat(12, 16, seed=1)
+    want = oracle.bc(g)
+    with bcb.Graph.from_csr(g, validate=True) as G:
+        got = G.compute()
+        assert_bc_close(got, want)
+        st = G.stats()
+        # sum BC = sum_s sum_t (d(s,t) - 1)  (SURVEY §8c-iii invariant, from the GPU's own depths)
+        inv = st["dist_sum"] - (st["reached"] - st["num_sources"])
+        assert abs(got.sum() - inv) <= 1e-9 * inv
+        G.prune_degree1()
+        assert_bc_close(G.compute(), want)
+
+
+def test_config3_rmat16_sampled_pruning_on_off():
+    """BASELINE config 3 shape (R-MAT 16 EF16), pruning off and on, against
+    the unpruned oracle on a 1024-source sample (full set: see bench)."""
+    bcb = _bcb()
+    g = gg.rmat(16, 16, seed=1)
+    S = gg.sample_sources(g, 1024, seed=2)
+    want = oracle.bc(g, S)
+    with bcb.Graph.from_csr(g) as G:
+        assert_bc_close(G.compute(S), want)
+        G.prune_degree1()
+        om, rm, rrp, rcol = oracle.prune_degree1(g)
+        gom, grm, grp, gcol = G.pruning()
+        assert np.array_equal(gom, om) and np.array_equal(grm, rm) and np.array_equal(grp, rrp)
+        assert np.array_equal(gcol, rcol)
+        Sr = [int(s) for s in S if not rm[s]]
+        Splus = set(Sr)
+        for s in Sr:
+            Splus.update(int(u) for u in g.col[g.row_ptr[s]:g.row_ptr[s + 1]] if rm[u])
+        assert_bc_close(G.compute(Sr), oracle.bc(g, sorted(Splus)))
+
+
+def test_grid_lanes_small():
+    bcb = _bcb()
+    g = gg.grid(24, 31)
+    with bcb.Graph.from_csr(g) as G:
+        assert_bc_close(G.compute(), oracle.bc(g))
+
+
+def test_sssp_integer_parity():
+    bcb = _bcb()
+    graphs = [gg.rmat(12, 16, seed=1), gg.grid(40, 40), gg.petersen(), gg.with_isolated(gg.path(9), 3)]
+    for g in graphs:
+        with bcb.Graph.from_csr(g) as G:
+            G.set_option(bcb.OPT_HUB_DEGREE, 64)
+            for s in (0, g.n // 3, g.n - 1):
+                d, su, ov, sf, de = oracle.sssp(g, s)
+                gd, gs, go, gde = G.sssp(s)
+                assert np.array_equal(gd, d)
+                ok = ov == 0
+                assert np.array_equal(go, ov)
+                assert np.array_equal(gs[ok & (d >= 0)], su[ok & (d >= 0)])
+                m = (d > 0)
+                assert_bc_close(gde[m], de[m])
+
+
+def test_sssp_hypercube_sigma_beyond_2p53():
+    bcb = _bcb()
+    g = gg.hypercube(20)
+    d, su, ov, sf, de = oracle.sssp(g, 0)
+    with bcb.Graph.from_csr(g) as G:
+        gd, gs, go, gde = G.sssp(0)
+    assert np.array_equal(gd, d) and np.array_equal(gs, su) and not go.any()
+    assert int(gs.max()) > 2 ** 53
+
+
+def test_config4_rmat20_sampled_launch_config():
+    """BASELINE config 4 (R-MAT 20 EF16) in the bench's launch configuration
+    (K = 256 lanes, default hub split), on a sampled source set the oracle
+    can finish; by additivity this checks those sources' contributions."""
+    bcb = _bcb()
+    g = gg.rmat(20, 16, seed=1)
+    S = gg.sample_sources(g, 65536, seed=2)[:96]
+    want = oracle.bc(g, S)
+    with bcb.Graph.from_csr(g) as G:
+        G.set_option(bcb.OPT_LANE_WORDS, 4)
+        got = G.compute(S)
+    assert_bc_close(got, want)
+
+
+def test_edge_cases_and_errors():
+    bcb = _bcb()
+    g = gg.with_isolated(gg.path(5), 2)
+    with bcb.Graph.from_csr(g) as G:
+        assert np.all(G.compute([]) == 0.0)
+        assert np.all(G.compute([5, 6]) == 0.0)  # isolated sources contribute 0
+        for bad in ([0, 0], [7], [-1]):
+            with pytest.raises(bcb.BCError) as ei:
+                G.compute(bad)
+            assert ei.value.name == "BC_ERR_INVALID"
+        G.prune_degree1()
+        with pytest.raises(bcb.BCError) as ei:
+            G.compute([0])  # removed 1-degree vertex
+        assert ei.value.name == "BC_ERR_INVALID"
+        with pytest.raises(bcb.BCError) as ei:
+            G.prune_degree1()
+        assert ei.value.name == "BC_ERR_STATE"
+    with bcb.Graph.from_csr(gg.from_pairs(1, [])) as G:
+        assert G.compute().tolist() == [0.0]
+    bad = gg.CSR(3, np.array([0, 1, 2, 2]), np.array([1, 1], np.int32))  # asymmetric
+    with pytest.raises(bcb.BCError):
+        bcb.Graph.from_csr(bad, validate=True)
+
+
+def test_device_output_on_torch_stream():
+    import torch
+
+    bcb = _bcb()
+    g = gg.rmat(10, 8, seed=6)
+    want = oracle.bc(g)
+    with bcb.Graph.from_csr(g) as G:
+        s = torch.cuda.Stream()
+        out = torch.empty(g.n, dtype=torch.float64, device="cuda")
+        with torch.cuda.stream(s):
+            G.compute(None, out=out)
+        s.synchronize()
+        assert_bc_close(out.cpu().numpy(), want)
