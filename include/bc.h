@@ -133,7 +133,9 @@ typedef enum {
     BC_OPT_LANE_WORDS = 1, /* 0 = auto, else 1, 2 or 4: K = 64*value source lanes per batch */
     BC_OPT_HUB_DEGREE = 2, /* vertices with degree > value are processed as split hubs (>= 32) */
     BC_OPT_PROFILE = 3,    /* 1 = record CUDA events around the level kernels (bc_get_stats) */
-    BC_OPT_MODE = 4        /* 0 = auto, 1 = lanes (bit-lane batches), 2 = slices (CTA per source) */
+    BC_OPT_MODE = 4,       /* 0 = auto, 1 = lanes (bit-lane batches), 2 = slices (CTA per source) */
+    BC_OPT_RELABEL = 5,    /* 1 (default) = traverse a degree-descending relabelled copy of the graph */
+    BC_OPT_SOURCE_ORDER = 6 /* batch schedule: 0 = given order, 1 = degree, 2 (default) = anchor clusters */
 } bc_option;
 
 bc_status bc_set_option(bc_graph *g, int option, int64_t value);
@@ -155,6 +157,10 @@ typedef struct {
     double total_ms;         /* whole bc_compute device time (BC_OPT_PROFILE)    */
     int64_t kernel_launches; /* all library kernel launches of the call          */
     int64_t dist_sum;        /* sum over sources of sum of depths of reached vertices */
+    int64_t fwd_items;       /* adjacency items scanned by forward level kernels (per batch, not per lane) */
+    int64_t fwd_hits;        /* items with >= 1 contributing lane, forward      */
+    int64_t bwd_items;       /* adjacency items scanned by backward level kernels */
+    int64_t bwd_hits;        /* items with >= 1 contributing lane, backward     */
 } bc_stats;
 
 bc_status bc_get_stats(const bc_graph *g, bc_stats *out);

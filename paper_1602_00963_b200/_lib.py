@@ -12,7 +12,7 @@ import subprocess
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-SO = os.path.join(PKG, "libbcb200.so")
+SO = os.environ.get("BC_SO") or os.path.join(PKG, "libbcb200.so")
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 
@@ -59,6 +59,8 @@ class bc_stats(ctypes.Structure):
         ("bwd_launches", ctypes.c_int64), ("reached", ctypes.c_int64), ("adj_reached", ctypes.c_int64),
         ("dag_edges", ctypes.c_int64), ("fwd_ms", ctypes.c_double), ("bwd_ms", ctypes.c_double),
         ("total_ms", ctypes.c_double), ("kernel_launches", ctypes.c_int64), ("dist_sum", ctypes.c_int64),
+        ("fwd_items", ctypes.c_int64), ("fwd_hits", ctypes.c_int64), ("bwd_items", ctypes.c_int64),
+        ("bwd_hits", ctypes.c_int64),
     ]
 
     def as_dict(self):

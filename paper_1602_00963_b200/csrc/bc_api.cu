@@ -14,6 +14,7 @@
 #include "util.cuh"
 #include "lanes.cuh"
 #include "graph_kernels.cuh"
+#include <cub/device/device_radix_sort.cuh>
 
 using namespace bcb;
 
@@ -82,13 +83,26 @@ struct DevCSR {
     int nhub = 0, nseg = 0;
     int *hub_ids = nullptr;
     int *hub_seg_off = nullptr;
+    int ntiles = 0;
+    int *tile_vs = nullptr;       // [ntiles+1] vertex ranges of the level-kernel tiles
+    int *perm = nullptr;          // compute CSR only: new id -> original id
+    int *inv = nullptr;           // compute CSR only: original id -> new id
+    uint32_t *omega = nullptr;    // compute CSR only: omega in this CSR's labels (pruned)
     std::vector<int> h_deg;
+    std::vector<int> h_inv;       // compute CSR only: original id -> new id
     void release() {
         dfree(rp);
         dfree(col);
         dfree(hub_ids);
         dfree(hub_seg_off);
-        nhub = nseg = 0;
+        dfree(tile_vs);
+        dfree(perm);
+        dfree(inv);
+        dfree(omega);
+        nhub = nseg = ntiles = 0;
+        nnz = 0;
+        h_deg.clear();
+        h_inv.clear();
     }
 };
 
@@ -119,14 +133,19 @@ struct LaneWS {
     }
 };
 
-constexpr int LCH = 8;  // levels per mask chunk
+constexpr int LCH = 8;           // levels per mask chunk
+constexpr int TILE_ITEMS = 8192; // non-hub adjacency items per level-kernel tile (soft cap)
 
 }  // namespace
 
 struct bc_graph {
     int device = 0;
     int64_t n = 0;
-    DevCSR orig, res;  // res.rp == nullptr while unpruned
+    DevCSR orig, res;  // original labels; res.rp == nullptr while unpruned
+    DevCSR run;        // the CSR the level kernels traverse: cur() relabelled by degree
+    bool run_valid = false;
+    int relabel = 1;
+    int src_order = 2;  // 0 given, 1 degree, 2 anchor clusters
     bool pruned = false;
     uint32_t *omega = nullptr;
     uint8_t *removed = nullptr;
@@ -146,7 +165,8 @@ struct bc_graph {
     int *h_flag = nullptr;                  // pinned
     int *d_src = nullptr;
     int64_t src_cap = 0;
-    double *d_bc = nullptr;
+    double *d_bc = nullptr;   // BC in compute (relabelled) ids
+    double *d_bc2 = nullptr;  // BC in original ids (host-output staging)
     int *d_tmp = nullptr;  // scan scratch
     int64_t tmp_cap = 0;
     bc_stats last{};
@@ -173,6 +193,36 @@ bc_status dev_scan(bc_graph *g, const int *in, int *out, int64_t n, int *d_total
     scan_sums_kernel<<<1, BC_NT, 0, st>>>(g->d_tmp, (int)ntiles, d_total);
     scan_add_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, g->d_tmp, n);
     CU(cudaGetLastError());
+    return BC_OK;
+}
+
+bc_status build_hubs(bc_graph *g, DevCSR &c, cudaStream_t st);
+
+// hubs + item-bounded tiles of <= TV consecutive vertices (host-side cut of
+// the degree sequence; it is layout metadata, not part of the method)
+bc_status build_layout(bc_graph *g, DevCSR &c, cudaStream_t st) {
+    CK(build_hubs(g, c, st));
+    std::vector<int> vs;
+    vs.push_back(0);
+    int cnt = 0;
+    int64_t items = 0;
+    const int64_t n = g->n;
+    for (int64_t v = 0; v < n; ++v) {
+        const int d = c.h_deg[v] > g->hub_deg ? 0 : c.h_deg[v];
+        if (cnt == TV || (cnt > 0 && items + d > TILE_ITEMS)) {
+            vs.push_back((int)v);
+            cnt = 0;
+            items = 0;
+        }
+        ++cnt;
+        items += d;
+    }
+    vs.push_back((int)n);
+    dfree(c.tile_vs);
+    c.ntiles = (int)vs.size() - 1;
+    CK(dalloc(&c.tile_vs, vs.size()));
+    CU(cudaMemcpyAsync(c.tile_vs, vs.data(), vs.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));
     return BC_OK;
 }
 
@@ -210,6 +260,96 @@ bc_status build_hubs(bc_graph *g, DevCSR &c, cudaStream_t st) {
     dfree(flag);
     dfree(pos);
     dfree(tot);
+    return BC_OK;
+}
+
+// The compute CSR: cur() relabelled by descending degree (stable, ties by
+// id), so hub rows are contiguous at the front of every per-vertex array.
+bc_status build_run(bc_graph *g) {
+    cudaStream_t st = g->own_stream;
+    DevCSR &c = g->cur();
+    DevCSR &r = g->run;
+    r.release();
+    g->run_valid = false;
+    const int n = (int)g->n;
+    CK(dalloc(&r.perm, n));
+    CK(dalloc(&r.inv, n));
+    int maxdeg = 0;
+    for (int d : c.h_deg) maxdeg = std::max(maxdeg, d);
+    unsigned *keys_in = nullptr, *keys_out = nullptr;
+    int *vals_in = nullptr;
+    CK(dalloc(&keys_in, n));
+    CK(dalloc(&keys_out, n));
+    CK(dalloc(&vals_in, n));
+    relabel_keys_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, c.rp, maxdeg, keys_in, vals_in);
+    if (g->relabel && maxdeg > 0) {
+        const int end_bit = 32 - __builtin_clz((unsigned)maxdeg);
+        size_t tmp_bytes = 0;
+        CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in, keys_out, vals_in, r.perm, n, 0, end_bit, st));
+        void *tmp = nullptr;
+        CU(cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 16)));
+        CU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, vals_in, r.perm, n, 0, end_bit, st));
+        CU(cudaStreamSynchronize(st));
+        cudaFree(tmp);
+    } else {
+        CU(cudaMemcpyAsync(r.perm, vals_in, (size_t)n * sizeof(int), cudaMemcpyDeviceToDevice, st));
+    }
+    invert_perm_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, r.perm, r.inv);
+    int *deg_new = nullptr, *tot = nullptr;
+    CK(dalloc(&deg_new, n));
+    CK(dalloc(&tot, 1));
+    permuted_degree_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, r.perm, c.rp, deg_new);
+    CK(dalloc(&r.rp, (size_t)n + 1));
+    CK(dev_scan(g, deg_new, r.rp, n, tot, st));
+    CU(cudaMemcpyAsync(r.rp + n, tot, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    r.nnz = c.nnz;
+    CK(dalloc(&r.col, (size_t)r.nnz));
+    relabel_cols_kernel<<<(unsigned)(((int64_t)n * 32 + 255) / 256), 256, 0, st>>>(n, r.perm, r.inv, c.rp, c.col,
+                                                                                   r.rp, r.col);
+    if (g->pruned) {
+        CK(dalloc(&r.omega, n));
+        gather_u32_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, r.perm, g->omega, r.omega);
+    }
+    std::vector<int> hperm(n);
+    CU(cudaMemcpyAsync(hperm.data(), r.perm, (size_t)n * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    CU(cudaGetLastError());
+    r.h_deg.resize(n);
+    r.h_inv.resize(n);
+    for (int i = 0; i < n; ++i) {
+        r.h_deg[i] = c.h_deg[hperm[i]];
+        r.h_inv[hperm[i]] = i;
+    }
+    dfree(keys_in);
+    dfree(keys_out);
+    dfree(vals_in);
+    dfree(deg_new);
+    dfree(tot);
+    CK(build_layout(g, r, st));
+    g->run_valid = true;
+    return BC_OK;
+}
+
+// Reorder d_src[0..ns) (compute ids, degree order) by anchor key, stably.
+bc_status cluster_sources(bc_graph *g, DevCSR &run, int ns, cudaStream_t st) {
+    unsigned *kin = nullptr, *kout = nullptr;
+    int *vout = nullptr;
+    CK(dalloc(&kin, ns));
+    CK(dalloc(&kout, ns));
+    CK(dalloc(&vout, ns));
+    anchor_key_kernel<<<(unsigned)(((int64_t)ns * 32 + 255) / 256), 256, 0, st>>>(g->d_src, ns, run.rp, run.col, kin);
+    const int end_bit = std::max(1, 32 - __builtin_clz((unsigned)std::max<int64_t>(1, g->n)));
+    size_t tmp_bytes = 0;
+    CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kin, kout, g->d_src, vout, ns, 0, end_bit, st));
+    void *tmp = nullptr;
+    CU(cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 16)));
+    CU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, g->d_src, vout, ns, 0, end_bit, st));
+    CU(cudaMemcpyAsync(g->d_src, vout, (size_t)ns * 4, cudaMemcpyDeviceToDevice, st));
+    CU(cudaStreamSynchronize(st));
+    cudaFree(tmp);
+    dfree(kin);
+    dfree(kout);
+    dfree(vout);
     return BC_OK;
 }
 
@@ -270,10 +410,11 @@ __global__ void lane_setup_kernel(const int *src, int nl, int K, const uint32_t 
 
 // occupancy-derived grid for the level kernels
 template <typename F>
-int level_grid(bc_graph *g, F kern, int units) {
+int level_grid(bc_graph *g, F kern, int units, size_t smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BC_NT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BC_NT, smem);
     if (occ < 1) occ = 1;
     int grid = g->num_sms * occ;
     return std::max(1, std::min(grid, units));
@@ -322,7 +463,8 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
     p.seg_len = g->hub_deg;
     p.hub_acc = ws.hub_acc;
     p.hub_ovf = ws.hub_ovf;
-    p.ntiles = (n + TV - 1) / TV;
+    p.ntiles = c.csr->ntiles;
+    p.tile_vs = c.csr->tile_vs;
     p.dbg_delta = nullptr;
 
     const size_t mbytes = (size_t)n * W * sizeof(uint64_t);
@@ -339,7 +481,16 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
 
     auto kf = lanes_level_kernel<W, SigT, false>;
     const int units = p.nseg + p.ntiles;
-    const int grid = level_grid(g, kf, units);
+    constexpr size_t SMEM = sizeof(LanesSmem<W, SigT>);
+    const int grid = level_grid(g, kf, units, SMEM);
+    {
+        auto kh = lanes_hub_finalize<W, SigT, false>;
+        cudaFuncSetAttribute(kh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+        auto kb = lanes_level_kernel<W, SigT, true>;
+        cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+        auto khb = lanes_hub_finalize<W, SigT, true>;
+        cudaFuncSetAttribute(khb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    }
     const int hub_grid = (c.csr->nhub * 32 + BC_NT - 1) / BC_NT;
 
     int L = 1;
@@ -359,8 +510,8 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
             cudaEventCreate(&e1);
             cudaEventRecord(e0, st);
         }
-        kf<<<grid, BC_NT, 0, st>>>(p);
-        if (p.nhub > 0) lanes_hub_finalize<W, SigT, false><<<hub_grid, BC_NT, 0, st>>>(p);
+        kf<<<grid, BC_NT, SMEM, st>>>(p);
+        if (p.nhub > 0) lanes_hub_finalize<W, SigT, false><<<hub_grid, BC_NT, SMEM, st>>>(p);
         if (ev_f) {
             cudaEventRecord(e1, st);
             ev_f->push_back(e0);
@@ -384,7 +535,7 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
     if constexpr (std::is_same<SigT, double>::value) {
         if (c.run_backward) {
             auto kb = lanes_level_kernel<W, SigT, true>;
-            const int gridb = level_grid(g, kb, units);
+            const int gridb = level_grid(g, kb, units, SMEM);
             p.dbg_delta = c.dbg_delta;
             for (int l = Lmax; l >= 1; --l) {
                 p.level = l;
@@ -398,8 +549,8 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
                     cudaEventCreate(&e1);
                     cudaEventRecord(e0, st);
                 }
-                kb<<<gridb, BC_NT, 0, st>>>(p);
-                if (p.nhub > 0) lanes_hub_finalize<W, SigT, true><<<hub_grid, BC_NT, 0, st>>>(p);
+                kb<<<gridb, BC_NT, SMEM, st>>>(p);
+                if (p.nhub > 0) lanes_hub_finalize<W, SigT, true><<<hub_grid, BC_NT, SMEM, st>>>(p);
                 if (ev_b) {
                     cudaEventRecord(e1, st);
                     ev_b->push_back(e0);
@@ -488,6 +639,7 @@ bc_status bc_destroy(bc_graph *g) {
         dfree(g->d_flags);
         dfree(g->d_src);
         dfree(g->d_bc);
+        dfree(g->d_bc2);
         dfree(g->d_tmp);
         if (g->h_flag) cudaFreeHost(g->h_flag);
         if (g->own_stream) cudaStreamDestroy(g->own_stream);
@@ -502,7 +654,7 @@ static bc_status create_impl(bc_graph *g, int64_t n, const int64_t *row_ptr, con
     CU(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
     cudaStream_t st = g->own_stream;
     CU(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device));
-    CK(dalloc(&g->d_stats, 4));
+    CK(dalloc(&g->d_stats, 8));
     CK(dalloc(&g->d_work_ctr, 4));
     CU(cudaMemset(g->d_work_ctr, 0, 4 * sizeof(int)));
     CK(ensure_flags(g, 64));
@@ -533,7 +685,8 @@ static bc_status create_impl(bc_graph *g, int64_t n, const int64_t *row_ptr, con
     }
     g->orig.h_deg.resize(n);
     for (int64_t v = 0; v < n; ++v) g->orig.h_deg[v] = (int)(row_ptr[v + 1] - row_ptr[v]);
-    CK(build_hubs(g, g->orig, st));
+    CK(build_layout(g, g->orig, st));
+    CK(build_run(g));
     return BC_OK;
 }
 
@@ -607,7 +760,7 @@ bc_status bc_prune_degree1(bc_graph *g, int64_t *out_removed) {
     dfree(rdeg);
     dfree(tot);
     g->pruned = true;
-    CK(build_hubs(g, g->res, st));
+    CK(build_run(g));
     if (out_removed) {
         int64_t r = 0;
         for (int v = 0; v < n; ++v) r += g->h_removed[v];
@@ -629,8 +782,20 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
             if (g->hub_deg == (int)value) return BC_OK;
             DeviceGuard dg(g->device);
             g->hub_deg = (int)value;
-            CK(build_hubs(g, g->orig, g->own_stream));
-            if (g->pruned) CK(build_hubs(g, g->res, g->own_stream));
+            CK(build_layout(g, g->orig, g->own_stream));
+            CK(build_run(g));
+            return BC_OK;
+        }
+        case BC_OPT_SOURCE_ORDER:
+            if (value < 0 || value > 2) return fail(BC_ERR_INVALID, "source order must be 0, 1 or 2");
+            g->src_order = (int)value;
+            return BC_OK;
+        case BC_OPT_RELABEL: {
+            int v = value ? 1 : 0;
+            if (v == g->relabel) return BC_OK;
+            DeviceGuard dg(g->device);
+            g->relabel = v;
+            CK(build_run(g));
             return BC_OK;
         }
         case BC_OPT_PROFILE:
@@ -707,6 +872,13 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     }
     const bool dev_out = is_device_ptr(out_bc);
     cudaStream_t st = cuda_stream ? (cudaStream_t)cuda_stream : g->own_stream;
+    if (!g->run_valid) CK(build_run(g));
+    DevCSR &run = g->run;
+    // batch schedule: compute ids, ascending = degree descending (sources with
+    // similar BFS depth profiles share a batch and sit in adjacent lanes)
+    for (auto &v : trav) v = run.h_inv[v];
+    for (auto &v : triv) v = run.h_inv[v];
+    if (g->src_order >= 1) std::stable_sort(trav.begin(), trav.end());
     g->last = bc_stats{};
     g->last.num_sources = (int64_t)trav.size();
     g->last.num_trivial = (int64_t)triv.size();
@@ -714,7 +886,7 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     if (W == 0) W = trav.size() > 128 ? 4 : (trav.size() > 64 ? 2 : 1);
     const int K = 64 * W;
     g->last.lanes = K;
-    CK(ensure_ws(g, g->ws, W, false, csr.nhub));
+    CK(ensure_ws(g, g->ws, W, false, std::max(run.nhub, g->orig.nhub)));
     const int64_t need = (int64_t)(trav.size() + triv.size());
     if (g->src_cap < need) {
         dfree(g->d_src);
@@ -727,17 +899,19 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
         cudaEventCreate(&t1);
         cudaEventRecord(t0, st);
     }
-    if (!trav.empty())
+    if (!trav.empty()) {
         CU(cudaMemcpyAsync(g->d_src, trav.data(), trav.size() * 4, cudaMemcpyHostToDevice, st));
+        if (g->src_order == 2 && trav.size() > (size_t)K) CK(cluster_sources(g, run, (int)trav.size(), st));
+    }
     if (!triv.empty())
         CU(cudaMemcpyAsync(g->d_src + trav.size(), triv.data(), triv.size() * 4, cudaMemcpyHostToDevice, st));
     CU(cudaMemsetAsync(g->d_bc, 0, (size_t)n * 8, st));
-    CU(cudaMemsetAsync(g->d_stats, 0, 4 * sizeof(unsigned long long), st));
+    CU(cudaMemsetAsync(g->d_stats, 0, 8 * sizeof(unsigned long long), st));
     std::vector<cudaEvent_t> ef, eb;
     for (size_t off = 0; off < trav.size(); off += K) {
         BatchCtx c{};
-        c.csr = &csr;
-        c.omega = g->pruned ? g->omega : nullptr;
+        c.csr = &run;
+        c.omega = g->pruned ? run.omega : nullptr;
         c.src = g->d_src + off;
         c.nl = (int)std::min<size_t>(K, trav.size() - off);
         c.st = st;
@@ -748,23 +922,30 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     }
     if (!triv.empty()) {
         trivial_sources_kernel<<<(unsigned)((triv.size() + 255) / 256), 256, 0, st>>>(
-            g->d_src + trav.size(), (int)triv.size(), g->omega, g->d_bc);
+            g->d_src + trav.size(), (int)triv.size(), run.omega, g->d_bc);
         g->last.kernel_launches += 1;
     }
     CU(cudaGetLastError());
-    unsigned long long hst[4] = {0, 0, 0, 0};
+    unsigned long long hst[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     CU(cudaMemcpyAsync(hst, g->d_stats, sizeof(hst), cudaMemcpyDeviceToHost, st));
     if (dev_out) {
-        CU(cudaMemcpyAsync(out_bc, g->d_bc, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
+        unpermute_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((int)n, run.inv, g->d_bc, out_bc);
     } else {
-        CU(cudaMemcpyAsync(out_bc, g->d_bc, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+        if (!g->d_bc2) CK(dalloc(&g->d_bc2, (size_t)n));
+        unpermute_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((int)n, run.inv, g->d_bc, g->d_bc2);
+        CU(cudaMemcpyAsync(out_bc, g->d_bc2, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
     }
+    g->last.kernel_launches += 1;
     if (g->profile) cudaEventRecord(t1, st);
     CU(cudaStreamSynchronize(st));
     g->last.reached = (int64_t)hst[0];
     g->last.adj_reached = (int64_t)hst[1];
     g->last.dag_edges = (int64_t)hst[2];
     g->last.dist_sum = (int64_t)hst[3];
+    g->last.fwd_items = (int64_t)hst[4];
+    g->last.fwd_hits = (int64_t)hst[5];
+    g->last.bwd_items = (int64_t)hst[6];
+    g->last.bwd_hits = (int64_t)hst[7];
     if (g->profile) {
         g->last.fwd_ms = sum_events(ef);
         g->last.bwd_ms = sum_events(eb);
@@ -795,7 +976,7 @@ bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma, 
     const int n = (int)g->n;
     cudaStream_t st = g->own_stream;
     bc_stats keep = g->last;
-    CK(ensure_ws(g, g->vws, 1, true, g->orig.nhub));
+    CK(ensure_ws(g, g->vws, 1, true, std::max(g->orig.nhub, g->run.nhub)));
     if (g->src_cap < 1) {
         dfree(g->d_src);
         CK(dalloc(&g->d_src, 1));
@@ -832,7 +1013,7 @@ bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma, 
                 depth_from_mask_kernel<<<(n + 255) / 256, 256, 0, st>>>(lv[l], n, 1, l, d_depth);
             gather_lane0_kernel<<<(n + 255) / 256, 256, 0, st>>>(g->vws.S, 64, n, g->vws.ovf, 1, d_sig, d_ov, d_depth);
             // fp64 pass for delta (uses the compute workspace at W = 1)
-            s = ensure_ws(g, g->ws, 1, false, g->orig.nhub);
+            s = ensure_ws(g, g->ws, 1, false, std::max(g->orig.nhub, g->run.nhub));
             if (s == BC_OK) {
                 CU(cudaMemsetAsync(g->d_bc, 0, (size_t)n * 8, st));
                 BatchCtx c2 = c;

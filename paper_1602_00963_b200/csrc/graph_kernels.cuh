@@ -151,3 +151,68 @@ __global__ void hub_segcount_kernel(int nhub, const int *hub_ids, const int *rp,
 }
 
 }  // namespace bcb
+
+namespace bcb {
+
+// --- degree-descending relabelling of the compute CSR:
+// hubs get the lowest ids, so their sigma/coef rows are contiguous at the
+// front of S (L2-friendly) and tiles can be cut by item count.
+__global__ void relabel_keys_kernel(int n, const int *rp, int maxdeg, unsigned *keys, int *vals) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) {
+        keys[v] = (unsigned)(maxdeg - (rp[v + 1] - rp[v]));
+        vals[v] = v;
+    }
+}
+
+__global__ void invert_perm_kernel(int n, const int *perm, int *inv) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) inv[perm[i]] = i;
+}
+
+__global__ void permuted_degree_kernel(int n, const int *perm, const int *rp, int *deg_new) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) deg_new[i] = rp[perm[i] + 1] - rp[perm[i]];
+}
+
+// warp per new vertex i: row i of the new CSR = inv-mapped row perm[i]
+__global__ void relabel_cols_kernel(int n, const int *perm, const int *inv, const int *rp, const int *col,
+                                    const int *rp_new, int *col_new) {
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= n) return;
+    const int u = perm[i];
+    const int a = rp[u], b = rp[u + 1], o = rp_new[i];
+    for (int e = a + lane_id(); e < b; e += 32) col_new[o + (e - a)] = inv[col[e]];
+}
+
+__global__ void gather_u32_kernel(int n, const int *perm, const uint32_t *src, uint32_t *dst) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[perm[i]];
+}
+
+__global__ void map_ids_kernel(long long cnt, const int *inv, const int *in, int *out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < cnt) out[i] = inv[in[i]];
+}
+
+// Batch scheduling key of a source (compute ids; smaller id = higher degree):
+// its highest-degree closed neighbour.  Sources sharing that anchor are at
+// distance <= 2, so their BFS depth profiles differ by <= 2 everywhere and a
+// batch of them keeps its lanes in step (dense level masks, few levels).
+__global__ void anchor_key_kernel(const int *src, int ns, const int *rp, const int *col, unsigned *key) {
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= ns) return;
+    const int s = src[i];
+    int m = s;
+    for (int e = rp[s] + lane_id(); e < rp[s + 1]; e += 32) m = min(m, col[e]);
+    m = __reduce_min_sync(0xffffffffu, m);
+    if (lane_id() == 0) key[i] = (unsigned)m;
+}
+
+// out[v] (original label) = bc_new[inv[v]]
+__global__ void unpermute_kernel(int n, const int *inv, const double *bc_new, double *out) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) out[v] = bc_new[inv[v]];
+}
+
+}  // namespace bcb

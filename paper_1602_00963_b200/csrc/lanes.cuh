@@ -24,7 +24,7 @@
 //   BC[x]   += sum_lanes (1 + omega(s)) * (delta(x) + omega(x))    (R13)
 //
 // Edge-to-thread mapping ("active-edge parallelism"): a
-// CTA takes a tile of TV consecutive vertex ids, keeps the active ones,
+// CTA takes a tile of <= TV consecutive vertex ids, keeps the active ones,
 // block-scans their degrees into a shared-memory CD array (the frontier
 // offsets of the tile) and splits the tile's items evenly over its warps;
 // an item e is mapped to its vertex by binary search in CD.  Items are read
@@ -73,6 +73,7 @@ struct LanesParams {
     void *hub_acc;               // [nhub][K] SigT, zero between levels
     uint64_t *hub_ovf;           // verify: [nhub][W]
     int ntiles;
+    const int *tile_vs;          // [ntiles+1] tile t = vertices [tile_vs[t], tile_vs[t+1]), <= TV of them
     double *dbg_delta;           // backward: delta of lane 0 (verification), nullable
 };
 
@@ -105,7 +106,7 @@ struct LanesKernel {
     const uint64_t lm;
     double w1[LPT];
     double ns_loc[LPT];
-    unsigned long long st_reach = 0, st_adj = 0, st_dag = 0, st_dsum = 0;
+    unsigned long long st_reach = 0, st_adj = 0, st_dag = 0, st_dsum = 0, st_items = 0, st_hits = 0;
     int any_new_loc = 0;
 
     __device__ LanesKernel(const LanesParams &pp, Smem &s)
@@ -235,6 +236,7 @@ struct LanesKernel {
         uint32_t aovf = 0;
         const uint64_t pol = policy_evict_first();
 
+        st_items += (lane == 0) ? (unsigned long long)(we - ws) : 0ull;
         for (int e0 = ws; e0 < we; e0 += 32 * R) {
             int sl[R], vv[R];
 #pragma unroll
@@ -330,6 +332,7 @@ struct LanesKernel {
                         }
                         aovf |= po[q];
                         if (!BWD) st_dag += __popc(mb[q]);
+                        st_hits += (lane == 0);
                     }
                 }
             }
@@ -347,15 +350,16 @@ struct LanesKernel {
         return (int)(((long long)j * nitems) / BC_NW);
     }
 
-    // ---- a tile of TV consecutive vertices
+    // ---- a tile of <= TV consecutive vertices (bounded by items, see build_layout)
     __device__ void tile(int t) {
-        const int x = t * TV + threadIdx.x;
+        const int v0 = p.tile_vs[t], v1 = p.tile_vs[t + 1];
+        const int x = v0 + threadIdx.x;
         int deg = 0, act = 0;
         uint64_t u[W];
 #pragma unroll
         for (int j = 0; j < W; ++j) u[j] = 0;
         int rs = 0;
-        if (x < p.n) {
+        if (x < v1) {
             rs = p.rp[x];
             deg = p.rp[x + 1] - rs;
             if (deg > 0 && deg <= p.hub_deg) {
@@ -483,6 +487,11 @@ struct LanesKernel {
             if (c) atomicAdd(p.stats + 2, c);
             if (d) atomicAdd(p.stats + 3, d);
         }
+        const unsigned long long it = warp_sum_u64(st_items), ht = warp_sum_u64(st_hits);
+        if (lane == 0) {
+            if (it) atomicAdd(p.stats + (BWD ? 6 : 4), it);
+            if (ht) atomicAdd(p.stats + (BWD ? 7 : 5), ht);
+        }
         int anyw = __any_sync(0xffffffffu, any_new_loc);
         if (lane == 0 && anyw) *p.any_new = 1;
         if (!BWD && p.lane_ns) {
@@ -500,9 +509,14 @@ struct LanesKernel {
     }
 };
 
+#ifndef BC_MINB
+#define BC_MINB 2  // min resident CTAs per SM for the level kernels (register cap)
+#endif
+
 template <int W, typename SigT, bool BWD>
-__global__ void __launch_bounds__(BC_NT) lanes_level_kernel(LanesParams p) {
-    __shared__ LanesSmem<W, SigT> sm;
+__global__ void __launch_bounds__(BC_NT, BC_MINB) lanes_level_kernel(LanesParams p) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    LanesSmem<W, SigT> &sm = *reinterpret_cast<LanesSmem<W, SigT> *>(smraw);
     LanesKernel<W, SigT, BWD> k(p, sm);
     const int total = p.nseg + p.ntiles;
     for (;;) {
@@ -527,7 +541,8 @@ template <int W, typename SigT, bool BWD>
 __global__ void __launch_bounds__(BC_NT) lanes_hub_finalize(LanesParams p) {
     using KK = LanesKernel<W, SigT, BWD>;
     constexpr int K = KK::K, LPT = KK::LPT;
-    __shared__ LanesSmem<W, SigT> sm;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    LanesSmem<W, SigT> &sm = *reinterpret_cast<LanesSmem<W, SigT> *>(smraw);
     KK k(p, sm);
     const int h = (blockIdx.x * BC_NT + threadIdx.x) >> 5;
     if (h < p.nhub) {

@@ -55,12 +55,14 @@ SUITE = small_suite()
 
 @pytest.mark.parametrize("words", [1, 2, 4])
 @pytest.mark.parametrize("hub", [32, 4096])
-def test_small_suite_all_sources(words, hub):
+@pytest.mark.parametrize("relabel", [0, 1])
+def test_small_suite_all_sources(words, hub, relabel):
     bcb = _bcb()
     for g in SUITE:
         with bcb.Graph.from_csr(g, validate=True) as G:
             G.set_option(bcb.OPT_LANE_WORDS, words)
             G.set_option(bcb.OPT_HUB_DEGREE, hub)
+            G.set_option(bcb.OPT_RELABEL, relabel)
             assert_bc_close(G.compute(), oracle.bc(g))
 
 

@@ -19,6 +19,8 @@ ap.add_argument("--lane-words", type=int, default=4)
 ap.add_argument("--hub", type=int, default=0)
 ap.add_argument("--repeat", type=int, default=1)
 ap.add_argument("--prune", action="store_true")
+ap.add_argument("--relabel", type=int, default=1)
+ap.add_argument("--order", type=int, default=2)
 ap.add_argument("--sort", default="none", choices=["none", "deg", "degasc"])
 a = ap.parse_args()
 g = gg.grid(a.grid, a.grid) if a.grid else gg.rmat(a.scale, a.ef, seed=1)
@@ -29,6 +31,8 @@ if a.prune:
     om, rm, _, _ = G.pruning()
     S = S[rm[S] == 0]
 G.set_option(bcb.OPT_LANE_WORDS, a.lane_words)
+G.set_option(bcb.OPT_RELABEL, a.relabel)
+G.set_option(bcb.OPT_SOURCE_ORDER, a.order)
 if a.sort != "none":
     d = g.degrees[S]
     S = S[np.argsort(-d if a.sort == "deg" else d, kind="stable")]
@@ -42,4 +46,5 @@ for r in range(a.repeat):
     st = G.stats()
     print(f"n={g.n} m={g.m} sources={len(S)} wall={dt*1e3:.1f}ms fwd={st['fwd_ms']:.2f}ms bwd={st['bwd_ms']:.2f}ms "
           f"levels={st['levels_total']} launches={st['kernel_launches']} TEPS={len(S)*g.m/dt/1e9:.1f}G "
-          f"A={st['adj_reached']} D={st['dag_edges']} N={st['reached']}")
+          f"A={st['adj_reached']} D={st['dag_edges']} N={st['reached']} fi={st['fwd_items']} fh={st['fwd_hits']} "
+          f"bi={st['bwd_items']} bh={st['bwd_hits']}")
