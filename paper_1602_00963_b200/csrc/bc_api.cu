@@ -109,7 +109,7 @@ struct DevCSR {
 struct LaneWS {
     int W = 0;
     bool verify = false;
-    void *S = nullptr;
+    std::vector<void *> slev;  // per-level sigma/coef rows, n*K 8-byte values each
     uint64_t *seen = nullptr;
     uint64_t *ovf = nullptr;
     std::vector<uint64_t *> chunks;  // LCH levels each
@@ -119,7 +119,8 @@ struct LaneWS {
     double *lane_w1 = nullptr;
     double *lane_ns = nullptr;
     void release() {
-        dfree(S);
+        for (auto &q : slev) dfree(q);
+        slev.clear();
         dfree(seen);
         dfree(ovf);
         for (auto &c : chunks) dfree(c);
@@ -368,7 +369,6 @@ bc_status ensure_ws(bc_graph *g, LaneWS &ws, int W, bool verify, int nhub) {
     const int K = 64 * W;
     if (ws.W != W || ws.verify != verify) {
         ws.release();
-        CK(dalloc((double **)&ws.S, n * K));  // 8-byte elements either way
         CK(dalloc(&ws.seen, n * W));
         if (verify) CK(dalloc(&ws.ovf, n * W));
         CK(dalloc(&ws.lane_w1, K));
@@ -399,6 +399,14 @@ bc_status ensure_level(bc_graph *g, LaneWS &ws, int L) {
         uint64_t *c = nullptr;
         CK(dalloc(&c, (size_t)g->n * ws.W * LCH));
         ws.chunks.push_back(c);
+    }
+    while ((int)ws.slev.size() <= L) {
+        double *q = nullptr;
+        bc_status st = dalloc(&q, (size_t)g->n * 64 * ws.W);
+        if (st != BC_OK)
+            return fail(st, "cannot allocate level-%d sigma rows (%.1f GB per level; lower BC_OPT_LANE_WORDS): %s",
+                        (int)ws.slev.size(), (double)g->n * 512.0 * ws.W / 1e9, g_err.c_str());
+        ws.slev.push_back(q);
     }
     return BC_OK;
 }
@@ -446,7 +454,6 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
     p.col = c.csr->col;
     p.omega = c.omega;
     p.seen = ws.seen;
-    p.S = ws.S;
     p.ovf = ws.ovf;
     p.bc = g->d_bc;
     p.lane_w1 = ws.lane_w1;
@@ -476,8 +483,13 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
     CU(cudaMemsetAsync(level_ptr(g, ws, 1), 0, mbytes, st));
     p.any_new = g->d_flags + 1;
     lanes_init_kernel<W, SigT><<<c.nl, BC_NT, 0, st>>>(p, c.src, level_ptr(g, ws, 0), level_ptr(g, ws, 1));
+    {
+        const unsigned mb = (unsigned)(((int64_t)n * 32 + 255) / 256);
+        lanes_materialize_kernel<W, SigT><<<mb, 256, 0, st>>>(n, level_ptr(g, ws, 0), (SigT *)ws.slev[0]);
+        lanes_materialize_kernel<W, SigT><<<mb, 256, 0, st>>>(n, level_ptr(g, ws, 1), (SigT *)ws.slev[1]);
+    }
     CU(cudaGetLastError());
-    g->last.kernel_launches += 2;
+    g->last.kernel_launches += 4;
 
     auto kf = lanes_level_kernel<W, SigT, false>;
     const int units = p.nseg + p.ntiles;
@@ -500,6 +512,8 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
         CU(cudaMemsetAsync(level_ptr(g, ws, L + 1), 0, mbytes, st));
         CU(cudaMemsetAsync(g->d_flags + L + 1, 0, sizeof(int), st));
         p.level = L;
+        p.S_cur = ws.slev[L];
+        p.S_nxt = ws.slev[L + 1];
         p.mask_cur = level_ptr(g, ws, L);
         p.mask_nxt = level_ptr(g, ws, L + 1);
         p.mask_nxt_ro = nullptr;
@@ -539,6 +553,8 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
             p.dbg_delta = c.dbg_delta;
             for (int l = Lmax; l >= 1; --l) {
                 p.level = l;
+                p.S_cur = ws.slev[l];
+                p.S_nxt = ws.slev[l + 1];
                 p.mask_cur = level_ptr(g, ws, l);
                 p.mask_nxt_ro = level_ptr(g, ws, l + 1);  // zero for l == Lmax
                 p.mask_nxt = nullptr;
@@ -958,16 +974,6 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     return BC_OK;
 }
 
-__global__ static void gather_lane0_kernel(const void *S, int K, int n, const uint64_t *ovf, int W,
-                                           unsigned long long *sig, uint8_t *ov, const int *depth) {
-    const int v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v < n) {
-        const bool r = depth[v] >= 0;
-        sig[v] = r ? reinterpret_cast<const unsigned long long *>(S)[(size_t)v * K] : 0ull;
-        if (ov) ov[v] = (r && ovf) ? (uint8_t)(ovf[(size_t)v * W] & 1ull) : 0;
-    }
-}
-
 bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma, uint8_t *sigma_overflow,
                   double *delta) {
     if (!g) return fail(BC_ERR_INVALID, "NULL handle");
@@ -993,7 +999,6 @@ bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma, 
     CU(cudaMemcpyAsync(g->d_src, &source, 4, cudaMemcpyHostToDevice, st));
     CU(cudaMemsetAsync(d_depth, 0xff, (size_t)n * 4, st));
     CU(cudaMemsetAsync(d_delta, 0, (size_t)n * 8, st));
-    CU(cudaMemsetAsync(g->vws.S, 0, (size_t)n * 64 * 8, st));
     bc_status s = BC_OK;
     if (g->orig.h_deg[source] > 0) {
         BatchCtx c{};
@@ -1011,7 +1016,11 @@ bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma, 
         if (s == BC_OK) {
             for (int l = 0; l <= Lmax; ++l)
                 depth_from_mask_kernel<<<(n + 255) / 256, 256, 0, st>>>(lv[l], n, 1, l, d_depth);
-            gather_lane0_kernel<<<(n + 255) / 256, 256, 0, st>>>(g->vws.S, 64, n, g->vws.ovf, 1, d_sig, d_ov, d_depth);
+            CU(cudaMemsetAsync(d_sig, 0, (size_t)n * 8, st));
+            CU(cudaMemsetAsync(d_ov, 0, (size_t)n, st));
+            for (int l = 0; l <= Lmax; ++l)
+                gather_level_lane0_kernel<unsigned long long><<<(n + 255) / 256, 256, 0, st>>>(
+                    n, lv[l], 1, (const unsigned long long *)g->vws.slev[l], 64, g->vws.ovf, d_sig, d_ov);
             // fp64 pass for delta (uses the compute workspace at W = 1)
             s = ensure_ws(g, g->ws, 1, false, std::max(g->orig.nhub, g->run.nhub));
             if (s == BC_OK) {

@@ -4,9 +4,13 @@
 // vertex v the batch keeps
 //   lvl[L][v]  : W x uint64 -- lanes whose BFS puts v at depth L
 //   seen[v]    : W x uint64 -- lanes that have discovered v
-//   S[v][K]    : sigma_s(v) (forward), overwritten in place by
+//   S_L[v][K]  : per level L, the row of v holds sigma_s(v) in the lanes
+//                where v is at depth L and exact zeros elsewhere (written
+//                whole by the commit that discovers v at L); the backward
+//                sweep overwrites it in place with
 //                coef_s(v) = (1 + omega(v) + delta_s(v)) / sigma_s(v)
-//                during the backward sweep (one array, two phases).
+//                (zeros outside level L).  Zero-filled level rows let a
+//                gather add whole lane pairs without per-lane masking.
 //
 // Forward level L -> L+1 (Alg.2 / Alg.3; Alg.1 lines
 // 9-22): every vertex x with undiscovered lanes u = active & ~seen[x] pulls
@@ -54,7 +58,8 @@ struct LanesParams {
     const uint64_t *mask_nxt_ro; // backward: lvl[L+1]
     uint64_t *mask_nxt;          // forward: lvl[L+1], pre-zeroed
     uint64_t *seen;
-    void *S;                     // [n][K] SigT
+    void *S_cur;                 // level-L rows [n][K] SigT (fwd: read sigma; bwd: sigma -> coef in place)
+    void *S_nxt;                 // level-(L+1) rows (fwd: written; bwd: read coef)
     uint64_t *ovf;               // verify variant: per-lane sigma overflow bits [n][W]
     double *bc;
     const double *lane_w1;       // [K] 1 + omega(source of lane)
@@ -85,16 +90,24 @@ struct LanesSmem {
     uint64_t u[TV * W];
     SigT part[BC_NW * 2 * 64 * W];
     uint32_t povf[BC_NW * 2 * 32];
+    double ns[64 * W];  // per-lane n_s partial sums of this CTA (pruned graphs)
     int scan[2 * BC_NW + 2];
     int unit;
 };
+
+#ifndef BC_U4
+#define BC_U4 2  // sigma rows in flight per warp at W = 4
+#endif
+#ifndef BC_R4
+#define BC_R4 2  // item steps in flight per warp at W = 4
+#endif
 
 template <int W, typename SigT, bool BWD>
 struct LanesKernel {
     static constexpr int K = 64 * W;
     static constexpr int LPT = 2 * W;           // lanes per thread
-    static constexpr int R = (W == 1) ? 4 : 2;  // item steps in flight per warp
-    static constexpr int U = (W == 1) ? 4 : 2;  // sigma rows in flight per warp
+    static constexpr int R = (W == 1) ? 4 : (W == 2 ? 2 : BC_R4);  // item steps in flight per warp
+    static constexpr int U = (W == 1) ? 4 : (W == 2 ? 2 : BC_U4);  // sigma rows in flight per warp
     static constexpr bool VERIFY = std::is_same<SigT, unsigned long long>::value;
     static constexpr int GROUP = 32 / W;        // threads sharing one mask word
     using V = typename Vec2<SigT>::t;
@@ -104,45 +117,44 @@ struct LanesKernel {
     Smem &sm;
     const int lane, wid, my_word, my_off;
     const uint64_t lm;
-    double w1[LPT];
-    double ns_loc[LPT];
     unsigned long long st_reach = 0, st_adj = 0, st_dag = 0, st_dsum = 0, st_items = 0, st_hits = 0;
     int any_new_loc = 0;
 
     __device__ LanesKernel(const LanesParams &pp, Smem &s)
         : p(pp), sm(s), lane(lane_id()), wid(warp_id()), my_word((lane_id() * LPT) >> 6),
           my_off((lane_id() * LPT) & 63), lm((1ull << LPT) - 1ull) {
-#pragma unroll
-        for (int i = 0; i < LPT; ++i) {
-            w1[i] = BWD ? p.lane_w1[lane * LPT + i] : 0.0;
-            ns_loc[i] = 0.0;
+        if (!BWD && p.lane_ns) {
+            for (int l = threadIdx.x; l < K; l += BC_NT) sm.ns[l] = 0.0;
+            __syncthreads();
         }
     }
 
-    __device__ __forceinline__ SigT *S() const { return reinterpret_cast<SigT *>(p.S); }
+    __device__ __forceinline__ SigT *Scur() const { return reinterpret_cast<SigT *>(p.S_cur); }
+    __device__ __forceinline__ SigT *Snxt() const { return reinterpret_cast<SigT *>(p.S_nxt); }
 
-    // ---- forward commit: x discovered in the lanes where acc != 0 (or overflowed)
-    __device__ void commit_fwd(int x, int deg, const SigT (&acc)[LPT], uint32_t aovf) {
+    // write this thread's LPT-lane slice of a row: v[i] where bit i of keep, else 0
+    __device__ __forceinline__ void store_slice(SigT *row, uint32_t keep, const SigT (&v)[LPT]) {
+#pragma unroll
+        for (int pr = 0; pr < W; ++pr) {
+            V t;
+            t.x = (keep >> (2 * pr) & 1u) ? v[2 * pr] : SigT(0);
+            t.y = (keep >> (2 * pr + 1) & 1u) ? v[2 * pr + 1] : SigT(0);
+            reinterpret_cast<V *>(row)[pr] = t;
+        }
+    }
+
+    // ---- forward commit: x discovered in its undiscovered lanes (ub) where
+    // acc != 0 (or overflowed); the level-(L+1) row of x is written whole.
+    __device__ void commit_fwd(int x, int deg, uint32_t ub, const SigT (&acc)[LPT], uint32_t aovf) {
         uint32_t nb = aovf;
 #pragma unroll
         for (int i = 0; i < LPT; ++i)
             if (acc[i] != SigT(0)) nb |= 1u << i;
+        nb &= ub;
+        aovf &= ub;
+        const bool any = __any_sync(0xffffffffu, nb != 0);
+        if (any) store_slice(Snxt() + (size_t)x * K + lane * LPT, nb, acc);
         if (nb) {
-            SigT *row = S() + (size_t)x * K + lane * LPT;
-#pragma unroll
-            for (int pr = 0; pr < W; ++pr) {
-                uint32_t b = (nb >> (2 * pr)) & 3u;
-                if (b == 3u) {
-                    V t;
-                    t.x = acc[2 * pr];
-                    t.y = acc[2 * pr + 1];
-                    reinterpret_cast<V *>(row)[pr] = t;
-                } else if (b == 1u) {
-                    row[2 * pr] = acc[2 * pr];
-                } else if (b == 2u) {
-                    row[2 * pr + 1] = acc[2 * pr + 1];
-                }
-            }
             any_new_loc = 1;
             int pc = __popc(nb);
             st_reach += pc;
@@ -152,7 +164,7 @@ struct LanesKernel {
                 double wx = 1.0 + (p.omega ? (double)p.omega[x] : 0.0);
 #pragma unroll
                 for (int i = 0; i < LPT; ++i)
-                    if (nb >> i & 1u) ns_loc[i] += wx;
+                    if (nb >> i & 1u) atomicAdd(&sm.ns[lane * LPT + i], wx);
             }
         }
         uint64_t wv = (uint64_t)nb << my_off;
@@ -170,30 +182,33 @@ struct LanesKernel {
         }
     }
 
-    // ---- backward commit: finalise x at level L in the lanes of mb
+    // ---- backward commit: finalise x at level L in the lanes of mb; the
+    // level-L row of x becomes its coef row (zeros outside level L)
     __device__ void commit_bwd(int x, uint32_t mb, const SigT (&acc)[LPT]) {
         double contrib = 0.0;
-        if (mb) {
-            double om = p.omega ? (double)p.omega[x] : 0.0;
-            SigT *row = S() + (size_t)x * K + lane * LPT;
+        if constexpr (!VERIFY) {
+            if (__any_sync(0xffffffffu, mb != 0)) {
+                const double om = p.omega ? (double)p.omega[x] : 0.0;
+                double *row = Scur() + (size_t)x * K + lane * LPT;
+                double cf[LPT];
 #pragma unroll
-            for (int pr = 0; pr < W; ++pr) {
-                uint32_t b = (mb >> (2 * pr)) & 3u;
-                if (!b) continue;
-                V sg = reinterpret_cast<const V *>(row)[pr];
-                if (b & 1u) {
-                    double sig = (double)sg.x;
-                    double delta = sig * (double)acc[2 * pr];
-                    row[2 * pr] = (SigT)((1.0 + om + delta) / sig);
-                    contrib += w1[2 * pr] * (delta + om);
-                    if (p.dbg_delta && lane == 0 && pr == 0) p.dbg_delta[x] = delta;
+                for (int pr = 0; pr < W; ++pr) {
+                    double2 sg = make_double2(0.0, 0.0);
+                    if ((mb >> (2 * pr)) & 3u) sg = reinterpret_cast<const double2 *>(row)[pr];
+                    const double sgv[2] = {sg.x, sg.y};
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int i = 2 * pr + h;
+                        cf[i] = 0.0;
+                        if (mb >> i & 1u) {
+                            const double delta = sgv[h] * acc[i];
+                            cf[i] = (1.0 + om + delta) / sgv[h];
+                            contrib += p.lane_w1[lane * LPT + i] * (delta + om);
+                            if (i == 0 && lane == 0 && p.dbg_delta) p.dbg_delta[x] = delta;
+                        }
+                    }
                 }
-                if (b & 2u) {
-                    double sig = (double)sg.y;
-                    double delta = sig * (double)acc[2 * pr + 1];
-                    row[2 * pr + 1] = (SigT)((1.0 + om + delta) / sig);
-                    contrib += w1[2 * pr + 1] * (delta + om);
-                }
+                store_slice(row, mb, cf);
             }
         }
         contrib = warp_sum(contrib);
@@ -205,7 +220,8 @@ struct LanesKernel {
             uint32_t mb = (uint32_t)((sm.u[s * W + my_word] >> my_off) & lm);
             commit_bwd(sm.vert[s], mb, acc);
         } else {
-            commit_fwd(sm.vert[s], sm.cd[s + 1] - sm.cd[s], acc, aovf);
+            const uint32_t ub = (uint32_t)((sm.u[s * W + my_word] >> my_off) & lm);
+            commit_fwd(sm.vert[s], sm.cd[s + 1] - sm.cd[s], ub, acc, aovf);
         }
     }
 
@@ -292,9 +308,10 @@ struct LanesKernel {
                     }
                     V val[U][W];
                     uint32_t po[U];
+                    const SigT *Sread = BWD ? Snxt() : Scur();
 #pragma unroll
                     for (int q = 0; q < U; ++q) {
-                        const V *rowv = reinterpret_cast<const V *>(S() + (size_t)hv[q] * K + lane * LPT);
+                        const V *rowv = reinterpret_cast<const V *>(Sread + (size_t)hv[q] * K + lane * LPT);
 #pragma unroll
                         for (int pr = 0; pr < W; ++pr) {
                             val[q][pr].x = SigT(0);
@@ -317,18 +334,16 @@ struct LanesKernel {
                                 aovf = 0;
                             }
                         }
+                        // rows are zero outside their level: add whole pairs unmasked
+                        // (lanes outside c only collect values the commit discards)
 #pragma unroll
                         for (int pr = 0; pr < W; ++pr) {
-                            if (mb[q] >> (2 * pr) & 1u) {
-                                SigT o = acc[2 * pr];
-                                acc[2 * pr] = o + val[q][pr].x;
-                                if (VERIFY && acc[2 * pr] < o) aovf |= 1u << (2 * pr);
-                            }
-                            if (mb[q] >> (2 * pr + 1) & 1u) {
-                                SigT o = acc[2 * pr + 1];
-                                acc[2 * pr + 1] = o + val[q][pr].y;
-                                if (VERIFY && acc[2 * pr + 1] < o) aovf |= 1u << (2 * pr + 1);
-                            }
+                            SigT o = acc[2 * pr];
+                            acc[2 * pr] = o + val[q][pr].x;
+                            if (VERIFY && acc[2 * pr] < o) aovf |= 1u << (2 * pr);
+                            o = acc[2 * pr + 1];
+                            acc[2 * pr + 1] = o + val[q][pr].y;
+                            if (VERIFY && acc[2 * pr + 1] < o) aovf |= 1u << (2 * pr + 1);
                         }
                         aovf |= po[q];
                         if (!BWD) st_dag += __popc(mb[q]);
@@ -495,16 +510,9 @@ struct LanesKernel {
         int anyw = __any_sync(0xffffffffu, any_new_loc);
         if (lane == 0 && anyw) *p.any_new = 1;
         if (!BWD && p.lane_ns) {
-            double *red = reinterpret_cast<double *>(sm.part);
             __syncthreads();
-#pragma unroll
-            for (int i = 0; i < LPT; ++i) red[wid * K + lane * LPT + i] = ns_loc[i];
-            __syncthreads();
-            for (int l = threadIdx.x; l < K; l += BC_NT) {
-                double s = 0.0;
-                for (int w = 0; w < BC_NW; ++w) s += red[w * K + l];
-                if (s != 0.0) atomicAdd(p.lane_ns + l, s);
-            }
+            for (int l = threadIdx.x; l < K; l += BC_NT)
+                if (sm.ns[l] != 0.0) atomicAdd(p.lane_ns + l, sm.ns[l]);
         }
     }
 };
@@ -565,7 +573,12 @@ __global__ void __launch_bounds__(BC_NT) lanes_hub_finalize(LanesParams p) {
                 __syncwarp();
                 if ((k.lane & (KK::GROUP - 1)) == 0) *ow = 0;
             }
-            k.commit_fwd(x, p.rp[x + 1] - p.rp[x], acc, aovf);
+            uint64_t um = 0;
+#pragma unroll
+            for (int j = 0; j < W; ++j)
+                if (j == k.my_word) um = p.active[j] & ~p.seen[(size_t)x * W + j];
+            const uint32_t ub = (uint32_t)((um >> k.my_off) & k.lm);
+            k.commit_fwd(x, p.rp[x + 1] - p.rp[x], ub, acc, aovf);
         }
     }
     k.epilogue();
@@ -583,12 +596,10 @@ __global__ void __launch_bounds__(BC_NT) lanes_init_kernel(LanesParams p, const 
     const int s = src[l];
     const int word = l >> 6;
     const uint64_t bit = 1ull << (l & 63);
-    SigT *S = reinterpret_cast<SigT *>(p.S);
     const int rs = p.rp[s], re = p.rp[s + 1];
     if (threadIdx.x == 0) {
         atomicOr((unsigned long long *)(mask0 + (size_t)s * W + word), (unsigned long long)bit);
         atomicOr((unsigned long long *)(p.seen + (size_t)s * W + word), (unsigned long long)bit);
-        S[(size_t)s * K + l] = SigT(1);
     }
     double cnt = 0.0;
     unsigned long long adj = 0;
@@ -596,7 +607,6 @@ __global__ void __launch_bounds__(BC_NT) lanes_init_kernel(LanesParams p, const 
         const int w = p.col[e];
         atomicOr((unsigned long long *)(mask1 + (size_t)w * W + word), (unsigned long long)bit);
         atomicOr((unsigned long long *)(p.seen + (size_t)w * W + word), (unsigned long long)bit);
-        S[(size_t)w * K + l] = SigT(1);
         cnt += 1.0 + (p.omega ? (double)p.omega[w] : 0.0);
         adj += (unsigned long long)(p.rp[w + 1] - p.rp[w]);
     }
@@ -621,6 +631,43 @@ __global__ void __launch_bounds__(BC_NT) lanes_init_kernel(LanesParams p, const 
         atomicAdd(p.stats + 2, (unsigned long long)deg);
         atomicAdd(p.stats + 3, (unsigned long long)deg);
         if (deg > 0) *p.any_new = 1;
+    }
+}
+
+// Rows of levels 0 and 1: sigma = 1 in the lanes of the level mask, 0 elsewhere
+// (warp per vertex; vertices outside the level skip).
+template <int W, typename SigT>
+__global__ void lanes_materialize_kernel(int n, const uint64_t *mask, SigT *S) {
+    constexpr int K = 64 * W, LPT = 2 * W;
+    const int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (v >= n) return;
+    const int lane = lane_id();
+    uint64_t m[W];
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        m[j] = mask[(size_t)v * W + j];
+        any |= m[j] != 0;
+    }
+    if (!any) return;
+    const int word = (lane * LPT) >> 6, off = (lane * LPT) & 63;
+    uint64_t mw = 0;
+#pragma unroll
+    for (int j = 0; j < W; ++j)
+        if (j == word) mw = m[j];
+    SigT *row = S + (size_t)v * K + lane * LPT;
+#pragma unroll
+    for (int i = 0; i < LPT; ++i) row[i] = (mw >> (off + i) & 1ull) ? SigT(1) : SigT(0);
+}
+
+// verification: sigma of lane 0 for the vertices at level L
+template <typename SigT>
+__global__ void gather_level_lane0_kernel(int n, const uint64_t *mask, int W, const SigT *S, int K,
+                                          const uint64_t *ovf, unsigned long long *sig, uint8_t *ov) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n && (mask[(size_t)v * W] & 1ull)) {
+        sig[v] = (unsigned long long)S[(size_t)v * K];
+        if (ov) ov[v] = ovf ? (uint8_t)(ovf[(size_t)v * W] & 1ull) : 0;
     }
 }
 
