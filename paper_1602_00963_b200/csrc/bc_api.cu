@@ -14,6 +14,7 @@
 #include "util.cuh"
 #include "lanes.cuh"
 #include "graph_kernels.cuh"
+#include "slices.cuh"
 #include <cub/device/device_radix_sort.cuh>
 
 using namespace bcb;
@@ -139,6 +140,21 @@ constexpr int TILE_ITEMS = 8192; // non-hub adjacency items per level-kernel til
 
 }  // namespace
 
+struct SlicesWS {
+    int rows = 0;  // CTAs (private rows)
+    int *depth = nullptr, *queue = nullptr, *loff = nullptr;
+    double *sigma = nullptr, *cf = nullptr, *bcp = nullptr;
+    void release() {
+        dfree(depth);
+        dfree(queue);
+        dfree(loff);
+        dfree(sigma);
+        dfree(cf);
+        dfree(bcp);
+        rows = 0;
+    }
+};
+
 struct bc_graph {
     int device = 0;
     int64_t n = 0;
@@ -159,6 +175,7 @@ struct bc_graph {
     int num_sms = 148;
     cudaStream_t own_stream = nullptr;
     LaneWS ws, vws;  // compute workspace, verification workspace (W = 1)
+    SlicesWS sws;    // slices-mode workspace
     unsigned long long *d_stats = nullptr;  // [4]
     int *d_work_ctr = nullptr;              // [4]
     int *d_flags = nullptr;                 // [flag_cap]
@@ -598,6 +615,69 @@ bc_status run_batch_w(bc_graph *g, LaneWS &ws, int W, const BatchCtx &c, std::ve
     }
 }
 
+bc_status ensure_slices(bc_graph *g, int rows) {
+    if (g->sws.rows >= rows) return BC_OK;
+    g->sws.release();
+    const size_t n = (size_t)g->n;
+    SlicesWS &w = g->sws;
+    CK(dalloc(&w.depth, n * rows));
+    CK(dalloc(&w.queue, n * rows));
+    CK(dalloc(&w.loff, (n + 2) * rows));
+    CK(dalloc(&w.sigma, n * rows));
+    CK(dalloc(&w.cf, n * rows));
+    CK(dalloc(&w.bcp, n * rows));
+    const size_t cnt = n * rows;
+    fill_int_kernel<<<(unsigned)((cnt + 255) / 256), 256>>>(w.depth, cnt, -1);
+    CU(cudaMemset(w.sigma, 0, cnt * 8));
+    CU(cudaMemset(w.cf, 0, cnt * 8));
+    CU(cudaMemset(w.bcp, 0, cnt * 8));
+    CU(cudaDeviceSynchronize());
+    w.rows = rows;
+    return BC_OK;
+}
+
+// One CTA per source (persistent grid), for long-diameter graphs.
+bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStream_t st,
+                     std::vector<cudaEvent_t> *ev) {
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slices_kernel, BC_NT, 0);
+    const int rows = std::max(1, std::min(ns, g->num_sms * std::max(1, occ)));
+    CK(ensure_slices(g, rows));
+    SlicesParams p{};
+    p.n = (int)g->n;
+    p.rp = run.rp;
+    p.col = run.col;
+    p.omega = g->pruned ? run.omega : nullptr;
+    p.src = d_src;
+    p.nsrc = ns;
+    p.next_src = g->d_work_ctr + 1;
+    p.depth = g->sws.depth;
+    p.sigma = g->sws.sigma;
+    p.cf = g->sws.cf;
+    p.queue = g->sws.queue;
+    p.loff = g->sws.loff;
+    p.bcp = g->sws.bcp;
+    p.stats = g->d_stats;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ev) {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+    }
+    slices_kernel<<<rows, BC_NT, 0, st>>>(p);
+    if (ev) {
+        cudaEventRecord(e1, st);
+        ev->push_back(e0);
+        ev->push_back(e1);
+    }
+    slices_reduce_kernel<<<(unsigned)((g->n + 255) / 256), 256, 0, st>>>((int)g->n, rows, g->sws.bcp, g->d_bc);
+    CU(cudaGetLastError());
+    g->last.kernel_launches += 2;
+    g->last.batches += 1;
+    g->last.lanes = 1;
+    return BC_OK;
+}
+
 bool is_device_ptr(const void *p) {
     cudaPointerAttributes a{};
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -650,6 +730,7 @@ bc_status bc_destroy(bc_graph *g) {
         dfree(g->removed);
         g->ws.release();
         g->vws.release();
+        g->sws.release();
         dfree(g->d_stats);
         dfree(g->d_work_ctr);
         dfree(g->d_flags);
@@ -898,11 +979,15 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     g->last = bc_stats{};
     g->last.num_sources = (int64_t)trav.size();
     g->last.num_trivial = (int64_t)triv.size();
+    // batch mode: bit lanes (low diameter) or one source per CTA (long
+    // diameter); auto picks slices for large sparse graphs (mean degree < 6)
+    int mode = g->mode;
+    if (mode == 0) mode = (g->n > 65536 && (double)run.nnz / (double)g->n < 6.0) ? 2 : 1;
     int W = g->lane_words_opt;
     if (W == 0) W = trav.size() > 128 ? 4 : (trav.size() > 64 ? 2 : 1);
     const int K = 64 * W;
     g->last.lanes = K;
-    CK(ensure_ws(g, g->ws, W, false, std::max(run.nhub, g->orig.nhub)));
+    if (mode == 1) CK(ensure_ws(g, g->ws, W, false, std::max(run.nhub, g->orig.nhub)));
     const int64_t need = (int64_t)(trav.size() + triv.size());
     if (g->src_cap < need) {
         dfree(g->d_src);
@@ -917,14 +1002,15 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     }
     if (!trav.empty()) {
         CU(cudaMemcpyAsync(g->d_src, trav.data(), trav.size() * 4, cudaMemcpyHostToDevice, st));
-        if (g->src_order == 2 && trav.size() > (size_t)K) CK(cluster_sources(g, run, (int)trav.size(), st));
+        if (mode == 1 && g->src_order == 2 && trav.size() > (size_t)K) CK(cluster_sources(g, run, (int)trav.size(), st));
     }
     if (!triv.empty())
         CU(cudaMemcpyAsync(g->d_src + trav.size(), triv.data(), triv.size() * 4, cudaMemcpyHostToDevice, st));
     CU(cudaMemsetAsync(g->d_bc, 0, (size_t)n * 8, st));
     CU(cudaMemsetAsync(g->d_stats, 0, 8 * sizeof(unsigned long long), st));
     std::vector<cudaEvent_t> ef, eb;
-    for (size_t off = 0; off < trav.size(); off += K) {
+    if (mode == 2 && !trav.empty()) CK(run_slices(g, run, g->d_src, (int)trav.size(), st, g->profile ? &ef : nullptr));
+    for (size_t off = 0; mode == 1 && off < trav.size(); off += K) {
         BatchCtx c{};
         c.csr = &run;
         c.omega = g->pruned ? run.omega : nullptr;

@@ -66,6 +66,44 @@ def test_small_suite_all_sources(words, hub, relabel):
             assert_bc_close(G.compute(), oracle.bc(g))
 
 
+@pytest.mark.parametrize("prune", [False, True])
+def test_small_suite_slices_mode(prune):
+    """Batch mode 'slices' (one source per CTA) on the same suite."""
+    bcb = _bcb()
+    for g in SUITE:
+        with bcb.Graph.from_csr(g) as G:
+            G.set_option(bcb.OPT_MODE, 2)
+            if prune:
+                G.prune_degree1()
+            assert_bc_close(G.compute(), oracle.bc(g))
+
+
+def test_grid_slices_and_lanes_agree_with_oracle():
+    bcb = _bcb()
+    g = gg.grid(64, 80)
+    want = oracle.bc(g)
+    with bcb.Graph.from_csr(g) as G:
+        for mode in (1, 2):
+            G.set_option(bcb.OPT_MODE, mode)
+            assert_bc_close(G.compute(), want)
+
+
+def test_config2_grid512_sampled_launch_config():
+    """BASELINE config 2 (grid 512x512) in the bench's launch configuration
+    (auto mode -> slices), on sampled sources the oracle can finish."""
+    bcb = _bcb()
+    g = gg.grid(512, 512)
+    S = gg.sample_sources(g, 262144, seed=2)[:64]
+    want = oracle.bc(g, S)
+    with bcb.Graph.from_csr(g) as G:
+        got = G.compute(S)
+        st = G.stats()
+    assert st["lanes"] == 1  # slices mode was chosen
+    assert_bc_close(got, want)
+    inv = st["dist_sum"] - (st["reached"] - st["num_sources"])
+    assert abs(got.sum() - inv) <= 1e-9 * inv
+
+
 @pytest.mark.parametrize("hub", [32, 4096])
 def test_small_suite_pruned(hub):
     bcb = _bcb()
