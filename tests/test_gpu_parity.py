@@ -272,3 +272,20 @@ def test_device_output_on_torch_stream():
             G.compute(None, out=out)
         s.synchronize()
         assert_bc_close(out.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_device_stats_match_oracle_per_source_counts(mode):
+    """The kernels' A_s / D_s / n_s counters (used for the roofline's
+    algorithmic bytes) equal the oracle's exact per-source statistics."""
+    bcb = _bcb()
+    g = gg.rmat(12, 16, seed=1)
+    S = gg.sample_sources(g, 300, seed=5)
+    _, st_o = oracle.bc(g, S, stats=True)
+    with bcb.Graph.from_csr(g) as G:
+        G.set_option(bcb.OPT_MODE, mode)
+        G.compute(S)
+        st = G.stats()
+    assert st["reached"] == int(st_o[:, 0].sum())
+    assert st["adj_reached"] == int(st_o[:, 1].sum())
+    assert st["dag_edges"] == int(st_o[:, 2].sum())
