@@ -49,6 +49,24 @@ template <typename T> struct Vec2;
 template <> struct Vec2<double> { using t = double2; };
 template <> struct Vec2<unsigned long long> { using t = ulonglong2; };
 
+// 16-byte read-only load with an L2 cache policy
+__device__ __forceinline__ double2 ld_pol(const double2 *p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ ulonglong2 ld_pol(const ulonglong2 *p, uint64_t pol) {
+    ulonglong2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;" : "=l"(v.x), "=l"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 struct LanesParams {
     int n;
     const int *rp;               // residual CSR row_ptr (int32, n+1)
@@ -91,6 +109,7 @@ struct LanesSmem {
     SigT part[BC_NW * 2 * 64 * W];
     uint32_t povf[BC_NW * 2 * 32];
     double ns[64 * W];  // per-lane n_s partial sums of this CTA (pruned graphs)
+    alignas(16) double sgs[BC_NW * 64 * W];  // backward: per-warp prefetched sigma row of the current slot
     int scan[2 * BC_NW + 2];
     int unit;
 };
@@ -101,6 +120,12 @@ struct LanesSmem {
 #ifndef BC_R4
 #define BC_R4 2  // item steps in flight per warp at W = 4
 #endif
+#ifndef BC_FULLROW
+#define BC_FULLROW 0  // 1: gather whole row slices (no per-hit lane test; rows are zero off-level)
+#endif
+#ifndef BC_L2HOT
+#define BC_L2HOT 32768  // rows of the BC_L2HOT highest-degree vertices are gathered with L2 evict_last
+#endif
 
 template <int W, typename SigT, bool BWD>
 struct LanesKernel {
@@ -109,6 +134,7 @@ struct LanesKernel {
     static constexpr int R = (W == 1) ? 4 : (W == 2 ? 2 : BC_R4);  // item steps in flight per warp
     static constexpr int U = (W == 1) ? 4 : (W == 2 ? 2 : BC_U4);  // sigma rows in flight per warp
     static constexpr bool VERIFY = std::is_same<SigT, unsigned long long>::value;
+    static constexpr bool FULL = BC_FULLROW && !VERIFY;  // unpredicated row gathers
     static constexpr int GROUP = 32 / W;        // threads sharing one mask word
     using V = typename Vec2<SigT>::t;
     using Smem = LanesSmem<W, SigT>;
@@ -184,17 +210,19 @@ struct LanesKernel {
 
     // ---- backward commit: finalise x at level L in the lanes of mb; the
     // level-L row of x becomes its coef row (zeros outside level L)
-    __device__ void commit_bwd(int x, uint32_t mb, const SigT (&acc)[LPT]) {
+    __device__ void commit_bwd(int x, uint32_t mb, const SigT (&acc)[LPT], bool staged = false) {
         double contrib = 0.0;
         if constexpr (!VERIFY) {
             if (__any_sync(0xffffffffu, mb != 0)) {
                 const double om = p.omega ? (double)p.omega[x] : 0.0;
                 double *row = Scur() + (size_t)x * K + lane * LPT;
+                const double *sgsrc = staged ? (const double *)(sm.sgs + wid * K + lane * LPT) : (const double *)row;
+                if (staged) cp_async_wait_all();
                 double cf[LPT];
 #pragma unroll
                 for (int pr = 0; pr < W; ++pr) {
                     double2 sg = make_double2(0.0, 0.0);
-                    if ((mb >> (2 * pr)) & 3u) sg = reinterpret_cast<const double2 *>(row)[pr];
+                    if ((mb >> (2 * pr)) & 3u) sg = reinterpret_cast<const double2 *>(sgsrc)[pr];
                     const double sgv[2] = {sg.x, sg.y};
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
@@ -215,10 +243,24 @@ struct LanesKernel {
         if (lane == 0 && contrib != 0.0) p.bc[x] += contrib;
     }
 
-    __device__ void commit_slot(int s, const SigT (&acc)[LPT], uint32_t aovf) {
+    // backward: start fetching the level-L sigma row slice of slot s into the
+    // warp's staging buffer (consumed by the slot's commit)
+    __device__ __forceinline__ void prefetch_sigma(int s) {
+        if constexpr (BWD && !VERIFY) {
+            cp_async_wait_all();  // an unconsumed earlier prefetch must land before the buffer is reused
+            const uint32_t mb = (uint32_t)((sm.u[s * W + my_word] >> my_off) & lm);
+            const double *row = Scur() + (size_t)sm.vert[s] * K + lane * LPT;
+            double *dst = sm.sgs + wid * K + lane * LPT;
+#pragma unroll
+            for (int pr = 0; pr < W; ++pr)
+                if ((mb >> (2 * pr)) & 3u) cp_async16(dst + 2 * pr, row + 2 * pr);
+        }
+    }
+
+    __device__ void commit_slot(int s, const SigT (&acc)[LPT], uint32_t aovf, bool staged = false) {
         if (BWD) {
             uint32_t mb = (uint32_t)((sm.u[s * W + my_word] >> my_off) & lm);
-            commit_bwd(sm.vert[s], mb, acc);
+            commit_bwd(sm.vert[s], mb, acc, staged);
         } else {
             const uint32_t ub = (uint32_t)((sm.u[s * W + my_word] >> my_off) & lm);
             commit_fwd(sm.vert[s], sm.cd[s + 1] - sm.cd[s], ub, acc, aovf);
@@ -230,7 +272,7 @@ struct LanesKernel {
                           uint32_t aovf) {
         bool owned = !hub_mode && sm.cd[s] >= ws && sm.cd[s + 1] <= we;
         if (owned) {
-            commit_slot(s, acc, aovf);
+            commit_slot(s, acc, aovf, true);
         } else {
             int idx = (s == first) ? 0 : 1;
             SigT *dst = sm.part + (wid * 2 + idx) * K + lane * LPT;
@@ -246,11 +288,13 @@ struct LanesKernel {
         int cur = slot_of(sm.cd, nslots, ws);
         const int first = cur;
         const int last = slot_of(sm.cd, nslots, we - 1);
+        if (!hub_mode) prefetch_sigma(cur);
         SigT acc[LPT];
 #pragma unroll
         for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
         uint32_t aovf = 0;
         const uint64_t pol = policy_evict_first();
+        const uint64_t pol_last = policy_evict_last();
 
         st_items += (lane == 0) ? (unsigned long long)(we - ws) : 0ull;
         for (int e0 = ws; e0 < we; e0 += 32 * R) {
@@ -279,7 +323,10 @@ struct LanesKernel {
             for (int k = 0; k < R; ++k) {
                 bool h = false;
 #pragma unroll
-                for (int j = 0; j < W; ++j) h |= (cc[k][j] != 0);
+                for (int j = 0; j < W; ++j) {
+                    h |= (cc[k][j] != 0);
+                    if (FULL && !BWD) st_dag += __popcll(cc[k][j]);
+                }
                 unsigned hm = __ballot_sync(0xffffffffu, h);
                 while (hm) {
                     int src[U], hs[U], hv[U];
@@ -297,6 +344,10 @@ struct LanesKernel {
                         if (src[q] >= 0) {
                             hs[q] = __shfl_sync(0xffffffffu, sl[k], src[q]);
                             hv[q] = __shfl_sync(0xffffffffu, vv[k], src[q]);
+                            if (FULL) {
+                                mb[q] = lm;
+                                continue;
+                            }
                             uint64_t w = 0;
 #pragma unroll
                             for (int j = 0; j < W; ++j) {
@@ -309,6 +360,11 @@ struct LanesKernel {
                     V val[U][W];
                     uint32_t po[U];
                     const SigT *Sread = BWD ? Snxt() : Scur();
+                    // hub rows (lowest compute ids) are reused across the whole level:
+                    // keep them in L2, stream the rest through it
+                    uint64_t rpol[U];
+#pragma unroll
+                    for (int q = 0; q < U; ++q) rpol[q] = (hv[q] < BC_L2HOT) ? pol_last : pol;
 #pragma unroll
                     for (int q = 0; q < U; ++q) {
                         const V *rowv = reinterpret_cast<const V *>(Sread + (size_t)hv[q] * K + lane * LPT);
@@ -316,7 +372,11 @@ struct LanesKernel {
                         for (int pr = 0; pr < W; ++pr) {
                             val[q][pr].x = SigT(0);
                             val[q][pr].y = SigT(0);
-                            if ((mb[q] >> (2 * pr)) & 3u) val[q][pr] = __ldg(rowv + pr);
+                            if (FULL) {
+                                if (src[q] >= 0) val[q][pr] = ld_pol(rowv + pr, rpol[q]);
+                            } else if ((mb[q] >> (2 * pr)) & 3u) {
+                                val[q][pr] = ld_pol(rowv + pr, rpol[q]);
+                            }
                         }
                         po[q] = 0;
                         if (VERIFY && mb[q])
@@ -329,6 +389,7 @@ struct LanesKernel {
                             while (cur < hs[q]) {
                                 flush(cur, first, ws, we, hub_mode, acc, aovf);
                                 ++cur;
+                                if (!hub_mode) prefetch_sigma(cur);
 #pragma unroll
                                 for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
                                 aovf = 0;
@@ -346,7 +407,7 @@ struct LanesKernel {
                             if (VERIFY && acc[2 * pr + 1] < o) aovf |= 1u << (2 * pr + 1);
                         }
                         aovf |= po[q];
-                        if (!BWD) st_dag += __popc(mb[q]);
+                        if (!BWD && !FULL) st_dag += __popc(mb[q]);
                         st_hits += (lane == 0);
                     }
                 }
@@ -355,6 +416,7 @@ struct LanesKernel {
         while (cur <= last) {
             flush(cur, first, ws, we, hub_mode, acc, aovf);
             ++cur;
+            if (!hub_mode && cur <= last) prefetch_sigma(cur);
 #pragma unroll
             for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
             aovf = 0;
