@@ -119,7 +119,9 @@ struct LaneWS {
     int hub_cap = 0;
     double *lane_w1 = nullptr;
     double *lane_ns = nullptr;
+    void *part = nullptr;  // split-slot partial sums [max CTAs][BC_NW][2][K]
     void release() {
+        dfree(part);
         for (auto &q : slev) dfree(q);
         slev.clear();
         dfree(seen);
@@ -390,6 +392,7 @@ bc_status ensure_ws(bc_graph *g, LaneWS &ws, int W, bool verify, int nhub) {
         if (verify) CK(dalloc(&ws.ovf, n * W));
         CK(dalloc(&ws.lane_w1, K));
         CK(dalloc(&ws.lane_ns, K));
+        CK(dalloc((double **)&ws.part, (size_t)g->num_sms * 8 * BC_NW * 2 * K));
         ws.W = W;
         ws.verify = verify;
     }
@@ -487,6 +490,7 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
     p.seg_len = g->hub_deg;
     p.hub_acc = ws.hub_acc;
     p.hub_ovf = ws.hub_ovf;
+    p.part = ws.part;
     p.ntiles = c.csr->ntiles;
     p.tile_vs = c.csr->tile_vs;
     p.dbg_delta = nullptr;
@@ -984,7 +988,17 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     int mode = g->mode;
     if (mode == 0) mode = (g->n > 65536 && (double)run.nnz / (double)g->n < 6.0) ? 2 : 1;
     int W = g->lane_words_opt;
-    if (W == 0) W = trav.size() > 128 ? 4 : (trav.size() > 64 ? 2 : 1);
+    if (W == 0) {
+        W = trav.size() > 128 ? 4 : (trav.size() > 64 ? 2 : 1);
+        // level rows cost n*512*W bytes per BFS level: keep ~10 levels within
+        // half of the free HBM (S23 -> W = 2)
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+            free_b += (size_t)g->ws.slev.size() * (size_t)g->n * 512 * (size_t)g->ws.W;  // reusable
+            while (W > 1 && (double)10 * g->n * 512.0 * W > 0.5 * (double)free_b) W >>= 1;
+        }
+        (void)cudaGetLastError();
+    }
     const int K = 64 * W;
     g->last.lanes = K;
     if (mode == 1) CK(ensure_ws(g, g->ws, W, false, std::max(run.nhub, g->orig.nhub)));

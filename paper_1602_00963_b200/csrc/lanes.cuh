@@ -66,6 +66,13 @@ __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// 16-byte async copy with zero fill when !valid, L2 cache policy
+__device__ __forceinline__ void cp_async16z(void *smem_dst, const void *gsrc, bool valid, uint64_t pol) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(d), "l"(gsrc),
+                 "r"(valid ? 16 : 0), "l"(pol)
+                 : "memory");
+}
 
 struct LanesParams {
     int n;
@@ -98,20 +105,7 @@ struct LanesParams {
     int ntiles;
     const int *tile_vs;          // [ntiles+1] tile t = vertices [tile_vs[t], tile_vs[t+1]), <= TV of them
     double *dbg_delta;           // backward: delta of lane 0 (verification), nullable
-};
-
-template <int W, typename SigT>
-struct LanesSmem {
-    int vert[TV];
-    int cd[TV + 1];
-    int rs[TV];
-    uint64_t u[TV * W];
-    SigT part[BC_NW * 2 * 64 * W];
-    uint32_t povf[BC_NW * 2 * 32];
-    double ns[64 * W];  // per-lane n_s partial sums of this CTA (pruned graphs)
-    alignas(16) double sgs[BC_NW * 64 * W];  // backward: per-warp prefetched sigma row of the current slot
-    int scan[2 * BC_NW + 2];
-    int unit;
+    void *part;                  // [gridDim][BC_NW][2][K] SigT: partial sums of slots split across warps
 };
 
 #ifndef BC_U4
@@ -120,12 +114,26 @@ struct LanesSmem {
 #ifndef BC_R4
 #define BC_R4 2  // item steps in flight per warp at W = 4
 #endif
-#ifndef BC_FULLROW
-#define BC_FULLROW 0  // 1: gather whole row slices (no per-hit lane test; rows are zero off-level)
+#ifndef BC_P
+#define BC_P 0  // >0: gather rows via cp.async into shared staging (measured slower: LDGSTS issue-bound)
 #endif
 #ifndef BC_L2HOT
 #define BC_L2HOT 32768  // rows of the BC_L2HOT highest-degree vertices are gathered with L2 evict_last
 #endif
+
+template <int W, typename SigT>
+struct LanesSmem {
+    int vert[TV];
+    int cd[TV + 1];
+    int rs[TV];
+    uint64_t u[TV * W];
+    alignas(16) SigT stg[BC_P > 0 ? BC_NW * BC_P * 64 * W : 2];  // per warp: cp.async staging (BC_P > 0)
+    uint32_t povf[BC_NW * 2 * 32];
+    double ns[64 * W];  // per-lane n_s partial sums of this CTA (pruned graphs)
+    alignas(16) double sgs[BC_NW * 64 * W];  // backward: per-warp prefetched sigma row of the current slot
+    int scan[2 * BC_NW + 2];
+    int unit;
+};
 
 template <int W, typename SigT, bool BWD>
 struct LanesKernel {
@@ -134,7 +142,7 @@ struct LanesKernel {
     static constexpr int R = (W == 1) ? 4 : (W == 2 ? 2 : BC_R4);  // item steps in flight per warp
     static constexpr int U = (W == 1) ? 4 : (W == 2 ? 2 : BC_U4);  // sigma rows in flight per warp
     static constexpr bool VERIFY = std::is_same<SigT, unsigned long long>::value;
-    static constexpr bool FULL = BC_FULLROW && !VERIFY;  // unpredicated row gathers
+    static constexpr bool STAGED = !VERIFY && BC_P > 0;  // cp.async row gathers via shared staging
     static constexpr int GROUP = 32 / W;        // threads sharing one mask word
     using V = typename Vec2<SigT>::t;
     using Smem = LanesSmem<W, SigT>;
@@ -156,6 +164,9 @@ struct LanesKernel {
     }
 
     __device__ __forceinline__ SigT *Scur() const { return reinterpret_cast<SigT *>(p.S_cur); }
+    __device__ __forceinline__ SigT *part_row(int w, int idx) const {
+        return reinterpret_cast<SigT *>(p.part) + ((size_t)(blockIdx.x * BC_NW + w) * 2 + idx) * K;
+    }
     __device__ __forceinline__ SigT *Snxt() const { return reinterpret_cast<SigT *>(p.S_nxt); }
 
     // write this thread's LPT-lane slice of a row: v[i] where bit i of keep, else 0
@@ -275,7 +286,7 @@ struct LanesKernel {
             commit_slot(s, acc, aovf, true);
         } else {
             int idx = (s == first) ? 0 : 1;
-            SigT *dst = sm.part + (wid * 2 + idx) * K + lane * LPT;
+            SigT *dst = part_row(wid, idx) + lane * LPT;
 #pragma unroll
             for (int i = 0; i < LPT; ++i) dst[i] = acc[i];
             if (VERIFY) sm.povf[(wid * 2 + idx) * 32 + lane] = aovf;
@@ -323,31 +334,25 @@ struct LanesKernel {
             for (int k = 0; k < R; ++k) {
                 bool h = false;
 #pragma unroll
-                for (int j = 0; j < W; ++j) {
-                    h |= (cc[k][j] != 0);
-                    if (FULL && !BWD) st_dag += __popcll(cc[k][j]);
-                }
+                for (int j = 0; j < W; ++j) h |= (cc[k][j] != 0);
                 unsigned hm = __ballot_sync(0xffffffffu, h);
                 while (hm) {
-                    int src[U], hs[U], hv[U];
-                    uint32_t mb[U];
+                    constexpr int Q = STAGED ? BC_P : U;
+                    int src[Q], hs[Q], hv[Q];
+                    uint32_t mb[Q];
 #pragma unroll
-                    for (int q = 0; q < U; ++q) {
+                    for (int q = 0; q < Q; ++q) {
                         src[q] = hm ? (__ffs(hm) - 1) : -1;
                         if (hm) hm &= hm - 1;
                     }
 #pragma unroll
-                    for (int q = 0; q < U; ++q) {
+                    for (int q = 0; q < Q; ++q) {
                         hs[q] = -1;
                         hv[q] = 0;
                         mb[q] = 0;
                         if (src[q] >= 0) {
                             hs[q] = __shfl_sync(0xffffffffu, sl[k], src[q]);
                             hv[q] = __shfl_sync(0xffffffffu, vv[k], src[q]);
-                            if (FULL) {
-                                mb[q] = lm;
-                                continue;
-                            }
                             uint64_t w = 0;
 #pragma unroll
                             for (int j = 0; j < W; ++j) {
@@ -357,33 +362,64 @@ struct LanesKernel {
                             mb[q] = (uint32_t)((w >> my_off) & lm);
                         }
                     }
-                    V val[U][W];
-                    uint32_t po[U];
                     const SigT *Sread = BWD ? Snxt() : Scur();
-                    // hub rows (lowest compute ids) are reused across the whole level:
-                    // keep them in L2, stream the rest through it
-                    uint64_t rpol[U];
+                    if constexpr (STAGED) {
+                        // gather: Q row slices -> the warp's shared staging, zero-filled
+                        // where no lane of the pair contributes; Q rows in flight
+                        SigT *stg = sm.stg + (size_t)wid * (BC_P * K) + lane * LPT;
 #pragma unroll
-                    for (int q = 0; q < U; ++q) rpol[q] = (hv[q] < BC_L2HOT) ? pol_last : pol;
+                        for (int q = 0; q < Q; ++q) {
+                            if (src[q] < 0) continue;
+                            const SigT *row = Sread + (size_t)hv[q] * K + lane * LPT;
+                            const uint64_t rp = (hv[q] < BC_L2HOT) ? pol_last : pol;
 #pragma unroll
-                    for (int q = 0; q < U; ++q) {
+                            for (int pr = 0; pr < W; ++pr)
+                                cp_async16z(stg + q * K + 2 * pr, row + 2 * pr, (mb[q] >> (2 * pr)) & 3u, rp);
+                        }
+                        cp_async_wait_all();
+#pragma unroll
+                        for (int q = 0; q < Q; ++q) {
+                            if (src[q] < 0) continue;
+                            if (hs[q] != cur) {
+                                while (cur < hs[q]) {
+                                    flush(cur, first, ws, we, hub_mode, acc, aovf);
+                                    ++cur;
+                                    if (!hub_mode) prefetch_sigma(cur);
+#pragma unroll
+                                    for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
+                                    aovf = 0;
+                                }
+                            }
+                            const V *sv = reinterpret_cast<const V *>(stg + q * K);
+#pragma unroll
+                            for (int pr = 0; pr < W; ++pr) {
+                                const V t = sv[pr];
+                                acc[2 * pr] += t.x;
+                                acc[2 * pr + 1] += t.y;
+                            }
+                            if (!BWD) st_dag += __popc(mb[q]);
+                            st_hits += (lane == 0);
+                        }
+                        continue;
+                    }
+                    V val[Q][W];
+                    uint32_t po[Q];
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) {
                         const V *rowv = reinterpret_cast<const V *>(Sread + (size_t)hv[q] * K + lane * LPT);
+                        const uint64_t rp = (hv[q] < BC_L2HOT) ? pol_last : pol;
 #pragma unroll
                         for (int pr = 0; pr < W; ++pr) {
                             val[q][pr].x = SigT(0);
                             val[q][pr].y = SigT(0);
-                            if (FULL) {
-                                if (src[q] >= 0) val[q][pr] = ld_pol(rowv + pr, rpol[q]);
-                            } else if ((mb[q] >> (2 * pr)) & 3u) {
-                                val[q][pr] = ld_pol(rowv + pr, rpol[q]);
-                            }
+                            if ((mb[q] >> (2 * pr)) & 3u) val[q][pr] = ld_pol(rowv + pr, rp);
                         }
                         po[q] = 0;
                         if (VERIFY && mb[q])
                             po[q] = mb[q] & (uint32_t)((__ldg(p.ovf + (size_t)hv[q] * W + my_word) >> my_off) & lm);
                     }
 #pragma unroll
-                    for (int q = 0; q < U; ++q) {
+                    for (int q = 0; q < Q; ++q) {
                         if (src[q] < 0) continue;
                         if (hs[q] != cur) {
                             while (cur < hs[q]) {
@@ -407,7 +443,7 @@ struct LanesKernel {
                             if (VERIFY && acc[2 * pr + 1] < o) aovf |= 1u << (2 * pr + 1);
                         }
                         aovf |= po[q];
-                        if (!BWD && !FULL) st_dag += __popc(mb[q]);
+                        if (!BWD) st_dag += __popc(mb[q]);
                         st_hits += (lane == 0);
                     }
                 }
@@ -477,7 +513,7 @@ struct LanesKernel {
                         int a0 = bnd(w, nitems), a1 = bnd(w + 1, nitems);
                         if (a0 >= a1 || a1 <= sm.cd[s] || a0 >= sm.cd[s + 1]) continue;
                         int idx = (sm.cd[s] <= a0) ? 0 : 1;
-                        const SigT *src = sm.part + (w * 2 + idx) * K + lane * LPT;
+                        const SigT *src = part_row(w, idx) + lane * LPT;
 #pragma unroll
                         for (int i = 0; i < LPT; ++i) {
                             SigT o = acc[i];
@@ -541,7 +577,7 @@ struct LanesKernel {
             for (int w = 0; w < BC_NW; ++w) {
                 if (bnd(w, nitems) >= bnd(w + 1, nitems)) continue;
                 SigT o = sum;
-                sum = o + sm.part[(w * 2) * K + l];
+                sum = o + part_row(w, 0)[l];
                 if (VERIFY && sum < o) ovf = true;
                 if (VERIFY && (sm.povf[(w * 2) * 32 + tl] >> ti & 1u)) ovf = true;
             }
