@@ -236,6 +236,7 @@ def main():
         import graphgen as gg  # noqa: F401
         om, rm, _, _ = G.pruning()
         S = S[rm[S] == 0]
+        per_gpu = min(per_gpu, len(S))
     if args.lane_words:
         G.set_option(bcb.OPT_LANE_WORDS, args.lane_words)
     stream = torch.cuda.current_stream()
