@@ -59,7 +59,8 @@ def source_list(g, cfg):
 
     total = CONFIGS[cfg][2]
     if total is None:
-        return np.arange(g.n, dtype=np.int32)
+        # "all sources": isolated vertices contribute 0 and are not counted in TEPS (R15, R21)
+        return g.non_isolated()
     return gg.sample_sources(g, total, seed=2)
 
 
