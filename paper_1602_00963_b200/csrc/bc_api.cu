@@ -144,10 +144,11 @@ constexpr int TILE_ITEMS = 8192; // non-hub adjacency items per level-kernel til
 
 struct SlicesWS {
     int rows = 0;  // CTAs (private rows)
-    int *depth = nullptr, *queue = nullptr, *loff = nullptr;
+    int *queue = nullptr, *loff = nullptr;
+    unsigned *bm = nullptr;
     double *sigma = nullptr, *cf = nullptr, *bcp = nullptr;
     void release() {
-        dfree(depth);
+        dfree(bm);
         dfree(queue);
         dfree(loff);
         dfree(sigma);
@@ -624,14 +625,15 @@ bc_status ensure_slices(bc_graph *g, int rows) {
     g->sws.release();
     const size_t n = (size_t)g->n;
     SlicesWS &w = g->sws;
-    CK(dalloc(&w.depth, n * rows));
+    const size_t bmw = (n + 31) / 32;
+    CK(dalloc(&w.bm, 3 * bmw * rows));
     CK(dalloc(&w.queue, n * rows));
     CK(dalloc(&w.loff, (n + 2) * rows));
     CK(dalloc(&w.sigma, n * rows));
     CK(dalloc(&w.cf, n * rows));
     CK(dalloc(&w.bcp, n * rows));
     const size_t cnt = n * rows;
-    fill_int_kernel<<<(unsigned)((cnt + 255) / 256), 256>>>(w.depth, cnt, -1);
+    if (w.bm) CU(cudaMemset(w.bm, 0, 3 * bmw * rows * sizeof(unsigned)));
     CU(cudaMemset(w.sigma, 0, cnt * 8));
     CU(cudaMemset(w.cf, 0, cnt * 8));
     CU(cudaMemset(w.bcp, 0, cnt * 8));
@@ -643,8 +645,18 @@ bc_status ensure_slices(bc_graph *g, int rows) {
 // One CTA per source (persistent grid), for long-diameter graphs.
 bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStream_t st,
                      std::vector<cudaEvent_t> *ev) {
+#ifndef BC_SLICES_SMEM_BM
+#define BC_SLICES_SMEM_BM 0  // shared-memory bitmaps cost occupancy; global (L2-resident) ones measured faster
+#endif
+    const bool smem_bm = BC_SLICES_SMEM_BM && g->n <= (int64_t)SLICES_SMEM_BM_WORDS * 32;
+    const size_t dsm = smem_bm ? 2 * SLICES_SMEM_BM_WORDS * sizeof(unsigned) : 0;
+    int maxdeg = 0;
+    for (int d : run.h_deg) maxdeg = std::max(maxdeg, d);
+    const bool lowdeg = maxdeg <= BC_LOWDEG;  // vertex-per-thread pull variant, no fp atomics
+    auto kern = lowdeg ? slices_lowdeg_kernel : (smem_bm ? slices_kernel<true> : slices_kernel<false>);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slices_kernel, BC_NT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BC_NT, dsm);
     const int rows = std::max(1, std::min(ns, g->num_sms * std::max(1, occ)));
     CK(ensure_slices(g, rows));
     SlicesParams p{};
@@ -655,7 +667,8 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
     p.src = d_src;
     p.nsrc = ns;
     p.next_src = g->d_work_ctr + 1;
-    p.depth = g->sws.depth;
+    p.bm = g->sws.bm;
+    p.bm_words = (int)((g->n + 31) / 32);
     p.sigma = g->sws.sigma;
     p.cf = g->sws.cf;
     p.queue = g->sws.queue;
@@ -668,7 +681,7 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
     }
-    slices_kernel<<<rows, BC_NT, 0, st>>>(p);
+    kern<<<rows, BC_NT, dsm, st>>>(p);
     if (ev) {
         cudaEventRecord(e1, st);
         ev->push_back(e0);
