@@ -656,7 +656,8 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
     auto kern = lowdeg ? slices_lowdeg_kernel : (smem_bm ? slices_kernel<true> : slices_kernel<false>);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BC_NT, dsm);
+    const int nt = lowdeg ? BC_SL_NT : BC_NT;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, dsm);
     const int rows = std::max(1, std::min(ns, g->num_sms * std::max(1, occ)));
     CK(ensure_slices(g, rows));
     SlicesParams p{};
@@ -681,7 +682,7 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
     }
-    kern<<<rows, BC_NT, dsm, st>>>(p);
+    kern<<<rows, nt, dsm, st>>>(p);
     if (ev) {
         cudaEventRecord(e1, st);
         ev->push_back(e0);

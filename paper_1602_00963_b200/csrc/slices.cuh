@@ -59,7 +59,7 @@ struct SlicesSmem {
     int scan[2 * BC_NW + 2];
     int tail;
     int src;
-    double red[BC_NW];
+    double red[32];
 };
 
 // Process the items of frontier chunk Q[c0, c1) (<= BC_NT vertices); calls
@@ -259,8 +259,11 @@ __global__ void __launch_bounds__(BC_NT) slices_kernel(SlicesParams p) {
 // from the child's side), and the backward step pulls coef from the level-(L+1)
 // neighbours.  Level membership is two bitmaps (levels L and L+1).
 constexpr int BC_LOWDEG = 64;
+#ifndef BC_SL_NT
+#define BC_SL_NT 256  // threads per CTA of the degree-bounded slices kernel (more sources in flight)
+#endif
 
-__global__ void __launch_bounds__(BC_NT) slices_lowdeg_kernel(SlicesParams p) {
+__global__ void __launch_bounds__(BC_SL_NT, 1) slices_lowdeg_kernel(SlicesParams p) {
     __shared__ SlicesSmem sm;
     const size_t n = (size_t)p.n;
     double *sigma = p.sigma + blockIdx.x * n;
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(BC_NT) slices_lowdeg_kernel(SlicesParams p) {
         unsigned *lcur = lb0, *lnxt = lb1;
         while (qs < qe) {
             // (1) discovery: frontier vertices push visited bits
-            for (int i = qs + threadIdx.x; i < qe; i += BC_NT) {
+            for (int i = qs + threadIdx.x; i < qe; i += BC_SL_NT) {
                 const int v = Q[i];
                 const int a = p.rp[v], b = p.rp[v + 1];
                 for (int e = a; e < b; ++e) {
@@ -314,7 +317,7 @@ __global__ void __launch_bounds__(BC_NT) slices_lowdeg_kernel(SlicesParams p) {
             __syncthreads();
             const int ne = sm.tail;
             // (2) sigma pull: each new vertex sums sigma of its level-L neighbours
-            for (int i = qe + threadIdx.x; i < ne; i += BC_NT) {
+            for (int i = qe + threadIdx.x; i < ne; i += BC_SL_NT) {
                 const int w = Q[i];
                 const int a = p.rp[w], b = p.rp[w + 1];
                 double sg = 0.0;
@@ -329,7 +332,7 @@ __global__ void __launch_bounds__(BC_NT) slices_lowdeg_kernel(SlicesParams p) {
             }
             __syncthreads();
             // (3) retire level L's bits
-            for (int i = qs + threadIdx.x; i < qe; i += BC_NT) {
+            for (int i = qs + threadIdx.x; i < qe; i += BC_SL_NT) {
                 const int v = Q[i];
                 atomicAnd(&lcur[v >> 5], ~(1u << (v & 31)));
             }
@@ -350,12 +353,12 @@ __global__ void __launch_bounds__(BC_NT) slices_lowdeg_kernel(SlicesParams p) {
         for (L = Lmax; L >= 1; --L) {
             const int a = loff[L], b = loff[L + 1];
             const int a1 = loff[L + 1], b1 = loff[L + 2];
-            for (int i = a1 + threadIdx.x; i < b1; i += BC_NT) {
+            for (int i = a1 + threadIdx.x; i < b1; i += BC_SL_NT) {
                 const int v = Q[i];
                 atomicOr(&lb0[v >> 5], 1u << (v & 31));
             }
             __syncthreads();
-            for (int i = a + threadIdx.x; i < b; i += BC_NT) {
+            for (int i = a + threadIdx.x; i < b; i += BC_SL_NT) {
                 const int w = Q[i];
                 double acc = 0.0;
                 const int ea = p.rp[w], eb = p.rp[w + 1];
@@ -372,13 +375,13 @@ __global__ void __launch_bounds__(BC_NT) slices_lowdeg_kernel(SlicesParams p) {
                 st_dsum += (unsigned long long)L;
             }
             __syncthreads();
-            for (int i = a1 + threadIdx.x; i < b1; i += BC_NT) {
+            for (int i = a1 + threadIdx.x; i < b1; i += BC_SL_NT) {
                 const int v = Q[i];
                 atomicAnd(&lb0[v >> 5], ~(1u << (v & 31)));
             }
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < reached; i += BC_NT) {
+        for (int i = threadIdx.x; i < reached; i += BC_SL_NT) {
             const int w = Q[i];
             ns_loc += 1.0 + (p.omega ? (double)p.omega[w] : 0.0);
             st_adj += (unsigned long long)(p.rp[w + 1] - p.rp[w]);
@@ -389,11 +392,11 @@ __global__ void __launch_bounds__(BC_NT) slices_lowdeg_kernel(SlicesParams p) {
         __syncthreads();
         if (threadIdx.x == 0 && p.omega) {
             double ns = 0.0;
-            for (int w = 0; w < BC_NW; ++w) ns += sm.red[w];
+            for (int w = 0; w < BC_SL_NT / 32; ++w) ns += sm.red[w];
             const double om = (double)p.omega[s];
             if (om != 0.0) bcp[s] += om * (ns - 2.0);
         }
-        for (int i = threadIdx.x; i < reached; i += BC_NT) {
+        for (int i = threadIdx.x; i < reached; i += BC_SL_NT) {
             const int w = Q[i];
             vis[w >> 5] = 0u;
             sigma[w] = 0.0;
