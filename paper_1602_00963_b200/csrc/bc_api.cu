@@ -15,6 +15,7 @@
 #include "lanes.cuh"
 #include "graph_kernels.cuh"
 #include "slices.cuh"
+#include "bwd_push.cuh"
 #include <cub/device/device_radix_sort.cuh>
 
 using namespace bcb;
@@ -120,8 +121,10 @@ struct LaneWS {
     double *lane_w1 = nullptr;
     double *lane_ns = nullptr;
     void *part = nullptr;  // split-slot partial sums [max CTAs][BC_NW][2][K]
+    double *A = nullptr;   // push-backward accumulators [n][K], zero between batches
     void release() {
         dfree(part);
+        dfree(A);
         for (auto &q : slev) dfree(q);
         slev.clear();
         dfree(seen);
@@ -353,13 +356,14 @@ bc_status build_run(bc_graph *g) {
 
 // Reorder d_src[0..ns) (compute ids, degree order) by anchor key, stably.
 bc_status cluster_sources(bc_graph *g, DevCSR &run, int ns, cudaStream_t st) {
-    unsigned *kin = nullptr, *kout = nullptr;
+    unsigned long long *kin = nullptr, *kout = nullptr;
     int *vout = nullptr;
     CK(dalloc(&kin, ns));
     CK(dalloc(&kout, ns));
     CK(dalloc(&vout, ns));
-    anchor_key_kernel<<<(unsigned)(((int64_t)ns * 32 + 255) / 256), 256, 0, st>>>(g->d_src, ns, run.rp, run.col, kin);
-    const int end_bit = std::max(1, 32 - __builtin_clz((unsigned)std::max<int64_t>(1, g->n)));
+    anchor_key_kernel<<<(unsigned)(((int64_t)ns * 32 + 255) / 256), 256, 0, st>>>(g->d_src, ns, run.rp, run.col, kin,
+                                                                                 g->src_order == 3 ? 1 : 0);
+    const int end_bit = 64;
     size_t tmp_bytes = 0;
     CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kin, kout, g->d_src, vout, ns, 0, end_bit, st));
     void *tmp = nullptr;
@@ -394,6 +398,10 @@ bc_status ensure_ws(bc_graph *g, LaneWS &ws, int W, bool verify, int nhub) {
         CK(dalloc(&ws.lane_w1, K));
         CK(dalloc(&ws.lane_ns, K));
         CK(dalloc((double **)&ws.part, (size_t)g->num_sms * 8 * BC_NW * 2 * K));
+        if (!verify) {
+            CK(dalloc(&ws.A, n * K));
+            CU(cudaMemset(ws.A, 0, n * K * sizeof(double)));
+        }
         ws.W = W;
         ws.verify = verify;
     }
@@ -570,6 +578,43 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
     }
     if constexpr (std::is_same<SigT, double>::value) {
         if (c.run_backward) {
+#ifndef BC_BWD_PULL
+            // push-form backward (bwd_push.cuh): finalize level L, then push its
+            // coef rows into the parents' accumulators
+            auto kpush = lanes_bwd_push_kernel<W>;
+            cudaFuncSetAttribute(kpush, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            int occp = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occp, kpush, BC_NT, 0);
+            const int gridp = std::max(1, std::min(g->num_sms * std::max(1, occp), units));
+            const unsigned fin_blocks = (unsigned)std::min<int64_t>(((int64_t)n * 32 + BC_NT - 1) / BC_NT,
+                                                                    (int64_t)g->num_sms * 8);
+            p.dbg_delta = c.dbg_delta;
+            for (int l = Lmax; l >= 1; --l) {
+                p.level = l;
+                p.S_cur = ws.slev[l];
+                p.S_nxt = nullptr;
+                p.mask_cur = level_ptr(g, ws, l);
+                p.mask_nxt_ro = level_ptr(g, ws, l - 1);  // parents
+                p.mask_nxt = nullptr;
+                p.any_new = g->d_flags;  // unused
+                cudaEvent_t e0 = nullptr, e1 = nullptr;
+                if (ev_b) {
+                    cudaEventCreate(&e0);
+                    cudaEventCreate(&e1);
+                    cudaEventRecord(e0, st);
+                }
+                lanes_bwd_finalize_kernel<W><<<fin_blocks, BC_NT, 0, st>>>(p, ws.A);
+                if (l >= 2) kpush<<<gridp, BC_NT, 0, st>>>(p, ws.A);
+                if (ev_b) {
+                    cudaEventRecord(e1, st);
+                    ev_b->push_back(e0);
+                    ev_b->push_back(e1);
+                }
+                CU(cudaGetLastError());
+                g->last.bwd_launches += 1;
+                g->last.kernel_launches += 1 + (l >= 2);
+            }
+#else
             auto kb = lanes_level_kernel<W, SigT, true>;
             const int gridb = level_grid(g, kb, units, SMEM);
             p.dbg_delta = c.dbg_delta;
@@ -598,6 +643,7 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
                 g->last.bwd_launches += 1;
                 g->last.kernel_launches += 1 + (p.nhub > 0);
             }
+#endif
             if (c.endpoint && c.omega) {
                 lanes_endpoint_kernel<<<(c.nl + 255) / 256, 256, 0, st>>>(c.src, c.nl, c.omega, ws.lane_ns,
                                                                          g->d_bc);
@@ -902,7 +948,7 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
             return BC_OK;
         }
         case BC_OPT_SOURCE_ORDER:
-            if (value < 0 || value > 2) return fail(BC_ERR_INVALID, "source order must be 0, 1 or 2");
+            if (value < 0 || value > 3) return fail(BC_ERR_INVALID, "source order must be 0..3");
             g->src_order = (int)value;
             return BC_OK;
         case BC_OPT_RELABEL: {
@@ -1030,7 +1076,7 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     }
     if (!trav.empty()) {
         CU(cudaMemcpyAsync(g->d_src, trav.data(), trav.size() * 4, cudaMemcpyHostToDevice, st));
-        if (mode == 1 && g->src_order == 2 && trav.size() > (size_t)K) CK(cluster_sources(g, run, (int)trav.size(), st));
+        if (mode == 1 && g->src_order >= 2 && trav.size() > (size_t)K) CK(cluster_sources(g, run, (int)trav.size(), st));
     }
     if (!triv.empty())
         CU(cudaMemcpyAsync(g->d_src + trav.size(), triv.data(), triv.size() * 4, cudaMemcpyHostToDevice, st));

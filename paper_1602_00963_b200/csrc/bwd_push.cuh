@@ -1,0 +1,288 @@
+// bwd_push.cuh -- backward dependency sweep, push form, for the bit-lane
+// batches (lanes.cuh).
+//
+// The pull form (successor checking, Alg.5, reading R2)
+// makes every level-L vertex gather the coef rows of its level-(L+1)
+// children.  On R-MAT those children are mostly low-degree vertices whose
+// rows are read once per parent and miss L2 -- the pull backward moved ~2x
+// its algorithmic bytes from DRAM (profiles/ncu_traffic.json).  The same sum
+//     delta(x) = sigma(x) * sum_{children v of x} coef(v)
+// is formed here from the other side of each DAG edge: once coef(v) of a
+// level-L vertex is final, v *pushes* it into an accumulator row A[y] of every
+// parent y (level L-1, lanes c = lvl[L][v] & lvl[L-1][y]) with fp64
+// red.global.add -- fire-and-forget, so no gather latency is on the critical
+// path, each child row is read once, and the parents' accumulators (hubs,
+// mostly) stay L2-resident.  Per level L = Lmax .. 1:
+//   lanes_bwd_finalize_kernel(L): for x at level L, lanes in lvl[L][x]:
+//       acc = A[x] (complete: all children pushed at level L+1); A[x] := 0
+//       delta = sigma * acc; coef = (1 + omega(x) + delta) / sigma   (Eq.5)
+//       S_L[x] := coef (row stays zero outside level L)
+//       BC[x] += sum_lanes (1 + omega(s)) (delta + omega(x))          (R13)
+//   lanes_bwd_push_kernel(L), L >= 2: items (x, y) over the adjacency of the
+//       level-L vertices, mapped to threads by the tile CD scan + binary
+//       search; hubs are cut into segments.  Every cell
+//       of A is consumed (and re-zeroed) by exactly one finalize, so A is
+//       zero again after every batch.
+// Lane-to-thread mapping here is *strided* (lane l -> thread l % 32, group
+// l / 32) so one red instruction covers 32 consecutive doubles (256 B); the
+// microbenchmark tools/micro/red_bench.cu measured 560 G red/s for that
+// pattern on L2-resident rows vs 190 G/s for 8-lane thread slices.
+#pragma once
+#include "lanes.cuh"
+
+namespace bcb {
+
+__device__ __forceinline__ void red_add_f64(double *p, double v) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+template <int W>
+struct PushSmem {
+    int vert[TV];
+    int cd[TV + 1];
+    int rs[TV];
+    uint64_t u[TV * W];
+    int scan[2 * BC_NW + 2];
+    int unit;
+};
+
+// x at level L: finalise coef and BC (warp per vertex, strided lanes; all
+// loads of a vertex are issued before its stores)
+template <int W>
+__global__ void __launch_bounds__(BC_NT) lanes_bwd_finalize_kernel(LanesParams p, double *__restrict__ A) {
+    constexpr int K = 64 * W, NG = 2 * W;
+    const int lane = lane_id();
+    const int nwarps = (int)((gridDim.x * (size_t)BC_NT) >> 5);
+    double *__restrict__ S = reinterpret_cast<double *>(p.S_cur);
+    for (int x = (int)(((size_t)blockIdx.x * BC_NT + threadIdx.x) >> 5); x < p.n; x += nwarps) {
+        uint64_t m[W];
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            m[j] = __ldg(p.mask_cur + (size_t)x * W + j);
+            any |= m[j] != 0;
+        }
+        if (!any) continue;  // warp-uniform
+        uint32_t bits = 0;
+#pragma unroll
+        for (int j = 0; j < NG; ++j) bits |= (((uint32_t)(m[j >> 1] >> ((j & 1) * 32)) >> lane) & 1u) << j;
+        double *arow = A + (size_t)x * K + lane;
+        double *row = S + (size_t)x * K + lane;
+        double av[NG], sv[NG];
+#pragma unroll
+        for (int j = 0; j < NG; ++j) {
+            av[j] = 0.0;
+            sv[j] = 1.0;
+            if (bits >> j & 1u) {
+                av[j] = arow[32 * j];
+                sv[j] = row[32 * j];
+            }
+        }
+        const double om = p.omega ? (double)p.omega[x] : 0.0;
+        double contrib = 0.0;
+#pragma unroll
+        for (int j = 0; j < NG; ++j) {
+            if (bits >> j & 1u) {
+                const double delta = sv[j] * av[j];
+                arow[32 * j] = 0.0;
+                row[32 * j] = (1.0 + om + delta) / sv[j];
+                contrib += p.lane_w1[32 * j + lane] * (delta + om);
+                if (j == 0 && lane == 0 && p.dbg_delta) p.dbg_delta[x] = delta;
+            }
+        }
+        contrib = warp_sum(contrib);
+        if (lane == 0 && contrib != 0.0) p.bc[x] += contrib;
+    }
+}
+
+template <int W>
+struct PushKernel {
+    static constexpr int K = 64 * W, NG = 2 * W;
+    static constexpr int R = (W == 4) ? 2 : 4;
+    const LanesParams &p;
+    double *A;
+    PushSmem<W> &sm;
+    const int lane, wid;
+    unsigned long long st_items = 0, st_hits = 0;
+
+    __device__ PushKernel(const LanesParams &pp, double *a, PushSmem<W> &s)
+        : p(pp), A(a), sm(s), lane(lane_id()), wid(warp_id()) {}
+
+    // one warp: items [ws, we) of the slots in sm; u[slot] = lvl[L][x]
+    __device__ void warp_push(int nslots, int ws, int we) {
+        const uint64_t *mpar = p.mask_nxt_ro;  // lvl[L-1] (parents)
+        const double *S = reinterpret_cast<const double *>(p.S_cur);
+        const uint64_t pol = policy_evict_first();
+        int cur = -1;
+        double cf[NG];
+#pragma unroll
+        for (int j = 0; j < NG; ++j) cf[j] = 0.0;
+        st_items += (lane == 0) ? (unsigned long long)(we - ws) : 0ull;
+        for (int e0 = ws; e0 < we; e0 += 32 * R) {
+            int sl[R], vv[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                const int e = e0 + k * 32 + lane;
+                sl[k] = -1;
+                vv[k] = 0;
+                if (e < we) {
+                    const int s = slot_of(sm.cd, nslots, e);
+                    sl[k] = s;
+                    vv[k] = ld_stream(p.col + sm.rs[s] + (e - sm.cd[s]), pol);
+                }
+            }
+            uint64_t cc[R][W];
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+#pragma unroll
+                for (int j = 0; j < W; ++j) {
+                    cc[k][j] = 0;
+                    if (sl[k] >= 0) cc[k][j] = sm.u[sl[k] * W + j] & __ldg(mpar + (size_t)vv[k] * W + j);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                uint32_t gmk = 0;
+#pragma unroll
+                for (int j = 0; j < NG; ++j)
+                    if ((uint32_t)(cc[k][j >> 1] >> ((j & 1) * 32))) gmk |= 1u << j;
+                unsigned hm = __ballot_sync(0xffffffffu, gmk != 0);
+                st_hits += (lane == 0) ? __popc(hm) : 0;
+                while (hm) {
+                    const int src = __ffs(hm) - 1;
+                    hm &= hm - 1;
+                    const int hs = __shfl_sync(0xffffffffu, sl[k], src);
+                    const int y = __shfl_sync(0xffffffffu, vv[k], src);
+                    const uint32_t gm = __shfl_sync(0xffffffffu, gmk, src);
+                    if (hs != cur) {  // warp-uniform: coef row of the new slot
+                        cur = hs;
+                        const double *row = S + (size_t)sm.vert[hs] * K + lane;
+#pragma unroll
+                        for (int j = 0; j < NG; ++j) cf[j] = row[32 * j];
+                    }
+                    double *arow = A + (size_t)y * K + lane;
+#pragma unroll
+                    for (int j = 0; j < NG; ++j) {
+                        if (gm >> j & 1u) {  // uniform
+                            const uint32_t cw =
+                                __shfl_sync(0xffffffffu, (uint32_t)(cc[k][j >> 1] >> ((j & 1) * 32)), src);
+                            if (cw >> lane & 1u) red_add_f64(arow + 32 * j, cf[j]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+
+    __device__ __forceinline__ static int bnd(int j, int nitems) {
+        return (int)(((long long)j * nitems) / BC_NW);
+    }
+
+    __device__ void tile(int t) {
+        const int v0 = p.tile_vs[t], v1 = p.tile_vs[t + 1];
+        const int x = v0 + threadIdx.x;
+        int deg = 0, act = 0, rs = 0;
+        uint64_t u[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) u[j] = 0;
+        if (x < v1) {
+            rs = p.rp[x];
+            deg = p.rp[x + 1] - rs;
+            if (deg > 0 && deg <= p.hub_deg) {
+#pragma unroll
+                for (int j = 0; j < W; ++j) {
+                    u[j] = p.mask_cur[(size_t)x * W + j];
+                    act |= (u[j] != 0);
+                }
+            }
+        }
+        int slot, cd, nslots, nitems;
+        block_excl_scan2(act, act ? deg : 0, slot, cd, nslots, nitems, sm.scan);
+        if (act) {
+            sm.vert[slot] = x;
+            sm.cd[slot] = cd;
+            sm.rs[slot] = rs;
+#pragma unroll
+            for (int j = 0; j < W; ++j) sm.u[slot * W + j] = u[j];
+        }
+        if (threadIdx.x == 0) sm.cd[nslots] = nitems;
+        __syncthreads();
+        if (nslots > 0) {
+            const int ws = bnd(wid, nitems), we = bnd(wid + 1, nitems);
+            if (ws < we) warp_push(nslots, ws, we);
+        }
+        __syncthreads();
+    }
+
+    __device__ void hub_segment(int unit) {
+        if (threadIdx.x == 0) {
+            int lo = 0, hi = p.nhub - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (p.hub_seg_off[mid] <= unit) lo = mid;
+                else hi = mid - 1;
+            }
+            sm.scan[0] = lo;
+        }
+        __syncthreads();
+        const int h = sm.scan[0];
+        __syncthreads();
+        const int x = p.hub_ids[h];
+        const int seg = unit - p.hub_seg_off[h];
+        const int a = p.rp[x] + seg * p.seg_len;
+        const int b = min(p.rp[x + 1], a + p.seg_len);
+        uint64_t u[W];
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            u[j] = p.mask_cur[(size_t)x * W + j];
+            any |= (u[j] != 0);
+        }
+        if (any) {
+            if (threadIdx.x == 0) {
+                sm.vert[0] = x;
+                sm.cd[0] = 0;
+                sm.cd[1] = b - a;
+                sm.rs[0] = a;
+#pragma unroll
+                for (int j = 0; j < W; ++j) sm.u[j] = u[j];
+            }
+            __syncthreads();
+            const int nitems = b - a;
+            const int ws = bnd(wid, nitems), we = bnd(wid + 1, nitems);
+            if (ws < we) warp_push(1, ws, we);
+        }
+        __syncthreads();
+    }
+
+    __device__ void epilogue() {
+        const unsigned long long it = warp_sum_u64(st_items), ht = warp_sum_u64(st_hits);
+        if (lane == 0) {
+            if (it) atomicAdd(p.stats + 6, it);
+            if (ht) atomicAdd(p.stats + 7, ht);
+        }
+    }
+};
+
+template <int W>
+__global__ void __launch_bounds__(BC_NT, BC_MINB) lanes_bwd_push_kernel(LanesParams p, double *A) {
+    __shared__ PushSmem<W> sm;
+    PushKernel<W> k(p, A, sm);
+    const int total = p.nseg + p.ntiles;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const int t = atomicAdd(p.work_ctr, 1);
+            if (t == total + (int)gridDim.x - 1) *p.work_ctr = 0;  // last fetch resets
+            sm.unit = t;
+        }
+        __syncthreads();
+        const int unit = sm.unit;
+        __syncthreads();
+        if (unit >= total) break;
+        if (unit < p.nseg) k.hub_segment(unit);
+        else k.tile(unit - p.nseg);
+    }
+    k.epilogue();
+}
+
+}  // namespace bcb

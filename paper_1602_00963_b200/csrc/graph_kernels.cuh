@@ -199,14 +199,25 @@ __global__ void map_ids_kernel(long long cnt, const int *inv, const int *in, int
 // its highest-degree closed neighbour.  Sources sharing that anchor are at
 // distance <= 2, so their BFS depth profiles differ by <= 2 everywhere and a
 // batch of them keeps its lanes in step (dense level masks, few levels).
-__global__ void anchor_key_kernel(const int *src, int ns, const int *rp, const int *col, unsigned *key) {
+__global__ void anchor_key_kernel(const int *src, int ns, const int *rp, const int *col, unsigned long long *key,
+                                  int two_level) {
     const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (i >= ns) return;
     const int s = src[i];
     int m = s;
     for (int e = rp[s] + lane_id(); e < rp[s + 1]; e += 32) m = min(m, col[e]);
     m = __reduce_min_sync(0xffffffffu, m);
-    if (lane_id() == 0) key[i] = (unsigned)m;
+    // second anchor: the next highest-degree closed neighbour (sub-clusters)
+    int m2 = 0x7fffffff;
+    if (two_level) {
+        if (s != m) m2 = s;
+        for (int e = rp[s] + lane_id(); e < rp[s + 1]; e += 32) {
+            const int c = col[e];
+            if (c != m) m2 = min(m2, c);
+        }
+        m2 = __reduce_min_sync(0xffffffffu, m2);
+    }
+    if (lane_id() == 0) key[i] = ((unsigned long long)(unsigned)m << 32) | (unsigned)(two_level ? m2 : 0);
 }
 
 // out[v] (original label) = bc_new[inv[v]]
