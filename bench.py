@@ -188,13 +188,15 @@ def run_reference(args, cfg):
 
 
 def algorithmic_bytes(st, K):
-    """SURVEY §8(d-iii) model, split per kernel:
-    forward  = A(4/K + 1/8) + 8 D + 8 n_s     (col ids shared by K lanes, 1-bit level test per lane,
-                                                sigma read per DAG edge, sigma written per reached vertex)
-    backward = A(4/K + 1/8) + 8 D + 16 n_s    (coef read per DAG edge, sigma read + coef write per vertex)"""
+    """SURVEY §8(d-iii) model split per kernel.  A = sum of
+    reached adjacency, D = DAG lane-edges, N = reached lane-vertices:
+      fwd  level kernel (pull)  A(4/K + 1/8) + 8 D + 8 N   col ids shared by K lanes,
+                                 1 mask bit per lane, sigma per DAG edge, sigma row write
+      bwd  push kernel           A(4/K + 1/8) + 8 D          coef value per DAG edge (red)
+      bwd  finalize kernel       32 N                        acc, sigma read; coef, acc write"""
     A, D, N = st["adj_reached"], st["dag_edges"], st["reached"]
-    common = A * (4.0 / K + 1.0 / 8.0) + 8.0 * D
-    return common + 8.0 * N, common + 16.0 * N
+    scan = A * (4.0 / K + 1.0 / 8.0)
+    return {"fwd": scan + 8.0 * D + 8.0 * N, "bwd_push": scan + 8.0 * D, "bwd_fin": 32.0 * N}
 
 
 def main():
@@ -264,9 +266,10 @@ def main():
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    agg = {"fwd_ms": 0.0, "bwd_ms": 0.0, "fwd_launches": 0, "bwd_launches": 0, "kernel_launches": 0,
-           "reached": 0, "adj_reached": 0, "dag_edges": 0, "num_sources": 0, "levels_total": 0, "batches": 0}
-    fwd_bytes = bwd_bytes = 0.0
+    agg = {"fwd_ms": 0.0, "bwd_ms": 0.0, "bwd_push_ms": 0.0, "bwd_fin_ms": 0.0, "fwd_launches": 0,
+           "bwd_launches": 0, "kernel_launches": 0, "reached": 0, "adj_reached": 0, "dag_edges": 0,
+           "num_sources": 0, "levels_total": 0, "batches": 0}
+    kbytes = {"fwd": 0.0, "bwd_push": 0.0, "bwd_fin": 0.0}
     lanes = 0
     e0.record(stream)
     for i in range(args.steps):
@@ -275,9 +278,8 @@ def main():
         lanes = st["lanes"]
         for k in agg:
             agg[k] += st[k]
-        fb, bb = algorithmic_bytes(st, st["lanes"])
-        fwd_bytes += fb
-        bwd_bytes += bb
+        for kk, vb in algorithmic_bytes(st, st["lanes"]).items():
+            kbytes[kk] += vb
     e1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -317,10 +319,12 @@ def main():
 
     if rank == 0:
         pk, pk_kind = peaks()
-        dom = "bwd" if agg["bwd_ms"] >= agg["fwd_ms"] else "fwd"
-        dom_bytes = bwd_bytes if dom == "bwd" else fwd_bytes
-        dom_ms = agg[f"{dom}_ms"]
-        achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
+        kms = {"fwd": agg["fwd_ms"], "bwd_push": agg["bwd_push_ms"], "bwd_fin": agg["bwd_fin_ms"]}
+        names = {"fwd": "lanes_level_kernel<fwd> (pull)", "bwd_push": "lanes_push_kernel<bwd>",
+                 "bwd_fin": "lanes_bwd_finalize_kernel"}
+        dom = max(kms, key=lambda k: kms[k])
+        dom_ms = kms[dom]
+        achieved = kbytes[dom] / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
         traffic = None
         try:
             tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
@@ -328,13 +332,10 @@ def main():
         except Exception:
             pass
         roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "kernel": f"lanes_level_kernel<{dom}>",
-                "peak_kind": pk_kind,
-                "kernel_share_of_step": dom_ms / (ms / 1.0) if ms > 0 else None,
-                "fwd": {"ms": agg["fwd_ms"], "alg_gb": fwd_bytes / 1e9,
-                        "gbs": fwd_bytes / (agg["fwd_ms"] / 1e3) / 1e9 if agg["fwd_ms"] else 0},
-                "bwd": {"ms": agg["bwd_ms"], "alg_gb": bwd_bytes / 1e9,
-                        "gbs": bwd_bytes / (agg["bwd_ms"] / 1e3) / 1e9 if agg["bwd_ms"] else 0}}
+                "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "kernel": names[dom],
+                "peak_kind": pk_kind, "kernel_share_of_step": dom_ms / ms if ms > 0 else None,
+                "kernels": {k: {"ms": kms[k], "alg_gb": kbytes[k] / 1e9,
+                                "gbs": kbytes[k] / (kms[k] / 1e3) / 1e9 if kms[k] else 0.0} for k in kms}}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(g, S)

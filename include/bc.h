@@ -135,7 +135,8 @@ typedef enum {
     BC_OPT_PROFILE = 3,    /* 1 = record CUDA events around the level kernels (bc_get_stats) */
     BC_OPT_MODE = 4,       /* 0 = auto, 1 = lanes (bit-lane batches), 2 = slices (CTA per source) */
     BC_OPT_RELABEL = 5,    /* 1 (default) = traverse a degree-descending relabelled copy of the graph */
-    BC_OPT_SOURCE_ORDER = 6 /* batch schedule: 0 = given order, 1 = degree, 2 (default) = anchor clusters */
+    BC_OPT_SOURCE_ORDER = 6, /* batch schedule: 0 = given order, 1 = degree, 2 (default) = anchor clusters */
+    BC_OPT_FWD_PUSH = 7     /* forward levels L <= value expand in push form (default 0), later ones pull */
 } bc_option;
 
 bc_status bc_set_option(bc_graph *g, int option, int64_t value);
@@ -161,6 +162,8 @@ typedef struct {
     int64_t fwd_hits;        /* items with >= 1 contributing lane, forward      */
     int64_t bwd_items;       /* adjacency items scanned by backward level kernels */
     int64_t bwd_hits;        /* items with >= 1 contributing lane, backward     */
+    double bwd_fin_ms;       /* backward finalize kernels (BC_OPT_PROFILE)       */
+    double bwd_push_ms;      /* backward push kernels (BC_OPT_PROFILE)           */
 } bc_stats;
 
 bc_status bc_get_stats(const bc_graph *g, bc_stats *out);

@@ -60,7 +60,7 @@ class bc_stats(ctypes.Structure):
         ("dag_edges", ctypes.c_int64), ("fwd_ms", ctypes.c_double), ("bwd_ms", ctypes.c_double),
         ("total_ms", ctypes.c_double), ("kernel_launches", ctypes.c_int64), ("dist_sum", ctypes.c_int64),
         ("fwd_items", ctypes.c_int64), ("fwd_hits", ctypes.c_int64), ("bwd_items", ctypes.c_int64),
-        ("bwd_hits", ctypes.c_int64),
+        ("bwd_hits", ctypes.c_int64), ("bwd_fin_ms", ctypes.c_double), ("bwd_push_ms", ctypes.c_double),
     ]
 
     def as_dict(self):

@@ -168,6 +168,7 @@ struct bc_graph {
     DevCSR run;        // the CSR the level kernels traverse: cur() relabelled by degree
     bool run_valid = false;
     int relabel = 1;
+    int fwd_push_levels = 0;  // forward levels L <= this use the push form (measured: pull is as fast at L=1)
     int src_order = 2;  // 0 given, 1 degree, 2 anchor clusters
     bool pruned = false;
     uint32_t *omega = nullptr;
@@ -194,6 +195,7 @@ struct bc_graph {
     int *d_tmp = nullptr;  // scan scratch
     int64_t tmp_cap = 0;
     bc_stats last{};
+    std::vector<cudaEvent_t> ev_push;  // profile: push-kernel intervals of the last compute
     DevCSR &cur() { return pruned ? res : orig; }
 };
 
@@ -554,8 +556,25 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
             cudaEventCreate(&e1);
             cudaEventRecord(e0, st);
         }
-        kf<<<grid, BC_NT, SMEM, st>>>(p);
-        if (p.nhub > 0) lanes_hub_finalize<W, SigT, false><<<hub_grid, BC_NT, SMEM, st>>>(p);
+        bool pushed = false;
+        if constexpr (std::is_same<SigT, double>::value) {
+            if (L <= g->fwd_push_levels) {
+                // small frontier: push sigma into the accumulators, then commit
+                auto kpf = lanes_push_kernel<W, true>;
+                int occp = 1;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occp, kpf, BC_NT, 0);
+                const int gridp = std::max(1, std::min(g->num_sms * std::max(1, occp), units));
+                kpf<<<gridp, BC_NT, 0, st>>>(p, ws.A);
+                const unsigned cb = (unsigned)std::min<int64_t>(((int64_t)n * 32 + BC_NT - 1) / BC_NT,
+                                                                (int64_t)g->num_sms * 8);
+                lanes_fwd_commit_kernel<W><<<cb, BC_NT, 0, st>>>(p, ws.A);
+                pushed = true;
+            }
+        }
+        if (!pushed) {
+            kf<<<grid, BC_NT, SMEM, st>>>(p);
+            if (p.nhub > 0) lanes_hub_finalize<W, SigT, false><<<hub_grid, BC_NT, SMEM, st>>>(p);
+        }
         if (ev_f) {
             cudaEventRecord(e1, st);
             ev_f->push_back(e0);
@@ -581,7 +600,7 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
 #ifndef BC_BWD_PULL
             // push-form backward (bwd_push.cuh): finalize level L, then push its
             // coef rows into the parents' accumulators
-            auto kpush = lanes_bwd_push_kernel<W>;
+            auto kpush = lanes_push_kernel<W, false>;
             cudaFuncSetAttribute(kpush, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
             int occp = 1;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occp, kpush, BC_NT, 0);
@@ -597,18 +616,26 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
                 p.mask_nxt_ro = level_ptr(g, ws, l - 1);  // parents
                 p.mask_nxt = nullptr;
                 p.any_new = g->d_flags;  // unused
-                cudaEvent_t e0 = nullptr, e1 = nullptr;
+                cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
                 if (ev_b) {
                     cudaEventCreate(&e0);
                     cudaEventCreate(&e1);
+                    cudaEventCreate(&e2);
+                    cudaEventCreate(&e3);
                     cudaEventRecord(e0, st);
                 }
                 lanes_bwd_finalize_kernel<W><<<fin_blocks, BC_NT, 0, st>>>(p, ws.A);
-                if (l >= 2) kpush<<<gridp, BC_NT, 0, st>>>(p, ws.A);
                 if (ev_b) {
                     cudaEventRecord(e1, st);
+                    cudaEventRecord(e2, st);
+                }
+                if (l >= 2) kpush<<<gridp, BC_NT, 0, st>>>(p, ws.A);
+                if (ev_b) {
+                    cudaEventRecord(e3, st);
                     ev_b->push_back(e0);
                     ev_b->push_back(e1);
+                    g->ev_push.push_back(e2);
+                    g->ev_push.push_back(e3);
                 }
                 CU(cudaGetLastError());
                 g->last.bwd_launches += 1;
@@ -947,6 +974,10 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
             CK(build_run(g));
             return BC_OK;
         }
+        case BC_OPT_FWD_PUSH:
+            if (value < 0 || value > 1000) return fail(BC_ERR_INVALID, "fwd push levels out of range");
+            g->fwd_push_levels = (int)value;
+            return BC_OK;
         case BC_OPT_SOURCE_ORDER:
             if (value < 0 || value > 3) return fail(BC_ERR_INVALID, "source order must be 0..3");
             g->src_order = (int)value;
@@ -1124,7 +1155,9 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     g->last.bwd_hits = (int64_t)hst[7];
     if (g->profile) {
         g->last.fwd_ms = sum_events(ef);
-        g->last.bwd_ms = sum_events(eb);
+        g->last.bwd_fin_ms = sum_events(eb);
+        g->last.bwd_push_ms = sum_events(g->ev_push);
+        g->last.bwd_ms = g->last.bwd_fin_ms + g->last.bwd_push_ms;
         float ms = 0;
         cudaEventElapsedTime(&ms, t0, t1);
         g->last.total_ms = ms;

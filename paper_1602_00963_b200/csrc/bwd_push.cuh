@@ -95,7 +95,12 @@ __global__ void __launch_bounds__(BC_NT) lanes_bwd_finalize_kernel(LanesParams p
     }
 }
 
-template <int W>
+// FWD = true: forward push for a small frontier (level L -> L+1): every
+// frontier vertex x pushes sigma_L(x) into A[y] of each neighbour y in the
+// lanes c = lvl[L][x] & active & ~seen[y] and ORs c into lvl[L+1][y];
+// lanes_fwd_commit_kernel then turns A into the level-(L+1) sigma rows.
+// FWD = false: the backward push described above.
+template <int W, bool FWD>
 struct PushKernel {
     static constexpr int K = 64 * W, NG = 2 * W;
     static constexpr int R = (W == 4) ? 2 : 4;
@@ -103,14 +108,14 @@ struct PushKernel {
     double *A;
     PushSmem<W> &sm;
     const int lane, wid;
-    unsigned long long st_items = 0, st_hits = 0;
+    unsigned long long st_items = 0, st_hits = 0, st_dag = 0;
 
     __device__ PushKernel(const LanesParams &pp, double *a, PushSmem<W> &s)
         : p(pp), A(a), sm(s), lane(lane_id()), wid(warp_id()) {}
 
     // one warp: items [ws, we) of the slots in sm; u[slot] = lvl[L][x]
     __device__ void warp_push(int nslots, int ws, int we) {
-        const uint64_t *mpar = p.mask_nxt_ro;  // lvl[L-1] (parents)
+        const uint64_t *mpar = FWD ? p.seen : p.mask_nxt_ro;  // fwd: seen[y]; bwd: lvl[L-1] (parents)
         const double *S = reinterpret_cast<const double *>(p.S_cur);
         const uint64_t pol = policy_evict_first();
         int cur = -1;
@@ -137,7 +142,11 @@ struct PushKernel {
 #pragma unroll
                 for (int j = 0; j < W; ++j) {
                     cc[k][j] = 0;
-                    if (sl[k] >= 0) cc[k][j] = sm.u[sl[k] * W + j] & __ldg(mpar + (size_t)vv[k] * W + j);
+                    if (sl[k] >= 0) {
+                        uint64_t mv = __ldg(mpar + (size_t)vv[k] * W + j);
+                        if (FWD) mv = p.active[j] & ~mv;
+                        cc[k][j] = sm.u[sl[k] * W + j] & mv;
+                    }
                 }
             }
 #pragma unroll
@@ -161,14 +170,21 @@ struct PushKernel {
                         for (int j = 0; j < NG; ++j) cf[j] = row[32 * j];
                     }
                     double *arow = A + (size_t)y * K + lane;
+                    uint64_t myword = 0;  // fwd: thread j < W ORs word j of c into lvl[L+1][y]
 #pragma unroll
                     for (int j = 0; j < NG; ++j) {
                         if (gm >> j & 1u) {  // uniform
                             const uint32_t cw =
                                 __shfl_sync(0xffffffffu, (uint32_t)(cc[k][j >> 1] >> ((j & 1) * 32)), src);
-                            if (cw >> lane & 1u) red_add_f64(arow + 32 * j, cf[j]);
+                            if (cw >> lane & 1u) {
+                                red_add_f64(arow + 32 * j, cf[j]);
+                                if (FWD) ++st_dag;
+                            }
+                            if (FWD && lane == (j >> 1)) myword |= (uint64_t)cw << ((j & 1) * 32);
                         }
                     }
+                    if (FWD && myword) atomicOr((unsigned long long *)(p.mask_nxt + (size_t)y * W + lane),
+                                                (unsigned long long)myword);
                 }
             }
         }
@@ -256,18 +272,20 @@ struct PushKernel {
     }
 
     __device__ void epilogue() {
-        const unsigned long long it = warp_sum_u64(st_items), ht = warp_sum_u64(st_hits);
+        const unsigned long long it = warp_sum_u64(st_items), ht = warp_sum_u64(st_hits),
+                                 dg = warp_sum_u64(st_dag);
         if (lane == 0) {
-            if (it) atomicAdd(p.stats + 6, it);
-            if (ht) atomicAdd(p.stats + 7, ht);
+            if (it) atomicAdd(p.stats + (FWD ? 4 : 6), it);
+            if (ht) atomicAdd(p.stats + (FWD ? 5 : 7), ht);
+            if (dg) atomicAdd(p.stats + 2, dg);
         }
     }
 };
 
-template <int W>
-__global__ void __launch_bounds__(BC_NT, BC_MINB) lanes_bwd_push_kernel(LanesParams p, double *A) {
+template <int W, bool FWD>
+__global__ void __launch_bounds__(BC_NT, BC_MINB) lanes_push_kernel(LanesParams p, double *A) {
     __shared__ PushSmem<W> sm;
-    PushKernel<W> k(p, A, sm);
+    PushKernel<W, FWD> k(p, A, sm);
     const int total = p.nseg + p.ntiles;
     for (;;) {
         if (threadIdx.x == 0) {
@@ -283,6 +301,71 @@ __global__ void __launch_bounds__(BC_NT, BC_MINB) lanes_bwd_push_kernel(LanesPar
         else k.tile(unit - p.nseg);
     }
     k.epilogue();
+}
+
+// Forward commit after a push level: x with lvl[L+1][x] != 0 gets its
+// level-(L+1) sigma row from A (zeros outside the new lanes), A is re-zeroed,
+// seen is updated (warp per vertex, strided lanes).
+template <int W>
+__global__ void __launch_bounds__(BC_NT) lanes_fwd_commit_kernel(LanesParams p, double *__restrict__ A) {
+    constexpr int K = 64 * W, NG = 2 * W;
+    __shared__ double ns_sm[K];
+    const int lane = lane_id();
+    if (p.lane_ns) {
+        for (int l = threadIdx.x; l < K; l += BC_NT) ns_sm[l] = 0.0;
+        __syncthreads();
+    }
+    const int nwarps = (int)((gridDim.x * (size_t)BC_NT) >> 5);
+    double *__restrict__ S = reinterpret_cast<double *>(p.S_nxt);
+    unsigned long long st_reach = 0, st_adj = 0, st_dsum = 0;
+    int any_new = 0;
+    for (int x = (int)(((size_t)blockIdx.x * BC_NT + threadIdx.x) >> 5); x < p.n; x += nwarps) {
+        uint64_t m[W];
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            m[j] = p.mask_nxt[(size_t)x * W + j];
+            any |= m[j] != 0;
+        }
+        if (!any) continue;  // warp-uniform
+        double *arow = A + (size_t)x * K + lane;
+        double *row = S + (size_t)x * K + lane;
+        double av[NG];
+        uint32_t bits = 0;
+#pragma unroll
+        for (int j = 0; j < NG; ++j) {
+            bits |= (((uint32_t)(m[j >> 1] >> ((j & 1) * 32)) >> lane) & 1u) << j;
+            av[j] = (bits >> j & 1u) ? arow[32 * j] : 0.0;
+        }
+        const double wx = 1.0 + (p.omega ? (double)p.omega[x] : 0.0);
+#pragma unroll
+        for (int j = 0; j < NG; ++j) {
+            row[32 * j] = av[j];
+            if (bits >> j & 1u) {
+                arow[32 * j] = 0.0;
+                if (p.lane_ns) atomicAdd(&ns_sm[32 * j + lane], wx);
+            }
+        }
+        if (lane < W) p.seen[(size_t)x * W + lane] |= m[lane];
+        const int pc = __popc(bits);
+        const int deg = p.rp[x + 1] - p.rp[x];
+        st_reach += pc;
+        st_adj += (unsigned long long)pc * deg;
+        st_dsum += (unsigned long long)pc * (unsigned)(p.level + 1);
+        any_new = 1;
+    }
+    const unsigned long long a = warp_sum_u64(st_reach), b = warp_sum_u64(st_adj), d = warp_sum_u64(st_dsum);
+    if (lane == 0) {
+        if (a) atomicAdd(p.stats + 0, a);
+        if (b) atomicAdd(p.stats + 1, b);
+        if (d) atomicAdd(p.stats + 3, d);
+    }
+    if (__any_sync(0xffffffffu, any_new) && lane == 0) *p.any_new = 1;
+    if (p.lane_ns) {
+        __syncthreads();
+        for (int l = threadIdx.x; l < K; l += BC_NT)
+            if (ns_sm[l] != 0.0) atomicAdd(p.lane_ns + l, ns_sm[l]);
+    }
 }
 
 }  // namespace bcb

@@ -289,3 +289,19 @@ def test_device_stats_match_oracle_per_source_counts(mode):
     assert st["reached"] == int(st_o[:, 0].sum())
     assert st["adj_reached"] == int(st_o[:, 1].sum())
     assert st["dag_edges"] == int(st_o[:, 2].sum())
+
+
+def test_profiling_counters_do_not_disturb_results():
+    """BC_OPT_PROFILE records CUDA events around every level kernel (bench's
+    roofline timing); the results and the library state must be unaffected."""
+    bcb = _bcb()
+    g = gg.rmat(11, 16, seed=2)
+    S = g.non_isolated()[:700]
+    want = oracle.bc(g, S)
+    with bcb.Graph.from_csr(g) as G:
+        G.set_option(bcb.OPT_PROFILE, 1)
+        for _ in range(2):
+            assert_bc_close(G.compute(S), want)
+            st = G.stats()
+            assert st["fwd_ms"] > 0 and st["bwd_ms"] > 0
+            assert abs(st["bwd_ms"] - st["bwd_fin_ms"] - st["bwd_push_ms"]) < 1e-9
