@@ -240,6 +240,11 @@ def main():
         om, rm, _, _ = G.pruning()
         S = S[rm[S] == 0]
         per_gpu = min(per_gpu, len(S))
+        # a pruned source s stands for s and its omega(s) removed children (R13):
+        # count |S+| = sum (1 + omega(s)) sources of the equivalent unpruned job
+        splus_factor = float((1 + om[S].astype(np.float64)).sum()) / len(S)
+    else:
+        splus_factor = 1.0
     if args.lane_words:
         G.set_option(bcb.OPT_LANE_WORDS, args.lane_words)
     stream = torch.cuda.current_stream()
@@ -291,7 +296,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    sources_all = per_gpu * world * args.steps
+    sources_all = per_gpu * world * args.steps * splus_factor
     value = sources_all * g.m / (ms_max / 1e3)
 
     # ---- end to end through the C ABI with HOST buffers (sources H2D, BC D2H inside the region)
@@ -345,6 +350,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(cfg), "n": g.n, "m": g.m, "sources_total": len(S),
                        "sources_per_gpu_per_step": per_gpu, "lanes_per_batch": lanes, "pruning": prune,
+                       "teps_sources": "|S+| (pruned: each source counts 1 + omega(s))" if prune else "|S|",
                        "parallelism": f"source-sharded x{world} + NCCL BC all-reduce" if world > 1 else "1 GPU",
                        "l2": "inputs exceed L2 (per step: CSR 4*2m B streamed + sigma/coef rows 8*K*n B); no flush"},
             "teps_paper_convention": 2 * value,
