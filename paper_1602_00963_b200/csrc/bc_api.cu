@@ -196,6 +196,11 @@ struct bc_graph {
     int64_t tmp_cap = 0;
     bc_stats last{};
     std::vector<cudaEvent_t> ev_push;  // profile: push-kernel intervals of the last compute
+    unsigned long long *cl_kin = nullptr, *cl_kout = nullptr;  // source clustering scratch
+    int *cl_vout = nullptr;
+    int64_t cl_cap = 0;
+    void *cl_tmp = nullptr;
+    size_t cl_tmp_bytes = 0;
     DevCSR &cur() { return pruned ? res : orig; }
 };
 
@@ -358,25 +363,31 @@ bc_status build_run(bc_graph *g) {
 
 // Reorder d_src[0..ns) (compute ids, degree order) by anchor key, stably.
 bc_status cluster_sources(bc_graph *g, DevCSR &run, int ns, cudaStream_t st) {
-    unsigned long long *kin = nullptr, *kout = nullptr;
-    int *vout = nullptr;
-    CK(dalloc(&kin, ns));
-    CK(dalloc(&kout, ns));
-    CK(dalloc(&vout, ns));
+    // grow-only scratch (no per-call cudaMalloc/cudaFree on the timed path)
+    if (g->cl_cap < ns) {
+        dfree(g->cl_kin);
+        dfree(g->cl_kout);
+        dfree(g->cl_vout);
+        CK(dalloc(&g->cl_kin, ns));
+        CK(dalloc(&g->cl_kout, ns));
+        CK(dalloc(&g->cl_vout, ns));
+        g->cl_cap = ns;
+    }
+    unsigned long long *kin = g->cl_kin, *kout = g->cl_kout;
+    int *vout = g->cl_vout;
     anchor_key_kernel<<<(unsigned)(((int64_t)ns * 32 + 255) / 256), 256, 0, st>>>(g->d_src, ns, run.rp, run.col, kin,
                                                                                  g->src_order == 3 ? 1 : 0);
     const int end_bit = 64;
     size_t tmp_bytes = 0;
     CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kin, kout, g->d_src, vout, ns, 0, end_bit, st));
-    void *tmp = nullptr;
-    CU(cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 16)));
-    CU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, g->d_src, vout, ns, 0, end_bit, st));
+    if (g->cl_tmp_bytes < tmp_bytes) {
+        if (g->cl_tmp) cudaFree(g->cl_tmp);
+        g->cl_tmp = nullptr;
+        CU(cudaMalloc(&g->cl_tmp, std::max<size_t>(tmp_bytes, 16)));
+        g->cl_tmp_bytes = tmp_bytes;
+    }
+    CU(cub::DeviceRadixSort::SortPairs(g->cl_tmp, tmp_bytes, kin, kout, g->d_src, vout, ns, 0, end_bit, st));
     CU(cudaMemcpyAsync(g->d_src, vout, (size_t)ns * 4, cudaMemcpyDeviceToDevice, st));
-    CU(cudaStreamSynchronize(st));
-    cudaFree(tmp);
-    dfree(kin);
-    dfree(kout);
-    dfree(vout);
     return BC_OK;
 }
 
@@ -828,6 +839,10 @@ bc_status bc_destroy(bc_graph *g) {
         dfree(g->d_src);
         dfree(g->d_bc);
         dfree(g->d_bc2);
+        dfree(g->cl_kin);
+        dfree(g->cl_kout);
+        dfree(g->cl_vout);
+        if (g->cl_tmp) cudaFree(g->cl_tmp);
         dfree(g->d_tmp);
         if (g->h_flag) cudaFreeHost(g->h_flag);
         if (g->own_stream) cudaStreamDestroy(g->own_stream);

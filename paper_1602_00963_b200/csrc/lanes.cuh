@@ -114,9 +114,6 @@ struct LanesParams {
 #ifndef BC_R4
 #define BC_R4 2  // item steps in flight per warp at W = 4
 #endif
-#ifndef BC_P
-#define BC_P 0  // >0: gather rows via cp.async into shared staging (measured slower: LDGSTS issue-bound)
-#endif
 #ifndef BC_L2HOT
 #define BC_L2HOT 32768  // rows of the BC_L2HOT highest-degree vertices are gathered with L2 evict_last
 #endif
@@ -127,7 +124,8 @@ struct LanesSmem {
     int cd[TV + 1];
     int rs[TV];
     uint64_t u[TV * W];
-    alignas(16) SigT stg[BC_P > 0 ? BC_NW * BC_P * 64 * W : 2];  // per warp: cp.async staging (BC_P > 0)
+    alignas(16) uint64_t hc[BC_NW * 32 * W];  // per warp: contributing-lane words c of the step's items
+    int2 hsv[BC_NW * 32];                     // per warp: (slot, v) of the step's items
     uint32_t povf[BC_NW * 2 * 32];
     double ns[64 * W];  // per-lane n_s partial sums of this CTA (pruned graphs)
     alignas(16) double sgs[BC_NW * 64 * W];  // backward: per-warp prefetched sigma row of the current slot
@@ -142,7 +140,7 @@ struct LanesKernel {
     static constexpr int R = (W == 1) ? 4 : (W == 2 ? 2 : BC_R4);  // item steps in flight per warp
     static constexpr int U = (W == 1) ? 4 : (W == 2 ? 2 : BC_U4);  // sigma rows in flight per warp
     static constexpr bool VERIFY = std::is_same<SigT, unsigned long long>::value;
-    static constexpr bool STAGED = !VERIFY && BC_P > 0;  // cp.async row gathers via shared staging
+    static constexpr int Q = U;
     static constexpr int GROUP = 32 / W;        // threads sharing one mask word
     using V = typename Vec2<SigT>::t;
     using Smem = LanesSmem<W, SigT>;
@@ -336,8 +334,18 @@ struct LanesKernel {
 #pragma unroll
                 for (int j = 0; j < W; ++j) h |= (cc[k][j] != 0);
                 unsigned hm = __ballot_sync(0xffffffffu, h);
+                if (hm == 0) continue;
+                // publish (slot, v, c) of every item of this step in shared memory:
+                // a hit then costs two shared loads instead of 2 + 2W shuffles
+                {
+                    int2 *hsv = sm.hsv + wid * 32;
+                    uint64_t *hc = sm.hc + wid * 32 * W;
+                    hsv[lane] = make_int2(sl[k], vv[k]);
+#pragma unroll
+                    for (int j = 0; j < W; ++j) hc[lane * W + j] = cc[k][j];
+                    __syncwarp();
+                }
                 while (hm) {
-                    constexpr int Q = STAGED ? BC_P : U;
                     int src[Q], hs[Q], hv[Q];
                     uint32_t mb[Q];
 #pragma unroll
@@ -351,57 +359,14 @@ struct LanesKernel {
                         hv[q] = 0;
                         mb[q] = 0;
                         if (src[q] >= 0) {
-                            hs[q] = __shfl_sync(0xffffffffu, sl[k], src[q]);
-                            hv[q] = __shfl_sync(0xffffffffu, vv[k], src[q]);
-                            uint64_t w = 0;
-#pragma unroll
-                            for (int j = 0; j < W; ++j) {
-                                uint64_t cw = __shfl_sync(0xffffffffu, cc[k][j], src[q]);
-                                if (j == my_word) w = cw;
-                            }
-                            mb[q] = (uint32_t)((w >> my_off) & lm);
+                            const int2 sv = sm.hsv[wid * 32 + src[q]];
+                            hs[q] = sv.x;
+                            hv[q] = sv.y;
+                            const uint32_t *cw = reinterpret_cast<const uint32_t *>(sm.hc + (wid * 32 + src[q]) * W);
+                            mb[q] = (cw[(lane * LPT) >> 5] >> ((lane * LPT) & 31)) & (uint32_t)lm;
                         }
                     }
                     const SigT *Sread = BWD ? Snxt() : Scur();
-                    if constexpr (STAGED) {
-                        // gather: Q row slices -> the warp's shared staging, zero-filled
-                        // where no lane of the pair contributes; Q rows in flight
-                        SigT *stg = sm.stg + (size_t)wid * (BC_P * K) + lane * LPT;
-#pragma unroll
-                        for (int q = 0; q < Q; ++q) {
-                            if (src[q] < 0) continue;
-                            const SigT *row = Sread + (size_t)hv[q] * K + lane * LPT;
-                            const uint64_t rp = (hv[q] < BC_L2HOT) ? pol_last : pol;
-#pragma unroll
-                            for (int pr = 0; pr < W; ++pr)
-                                cp_async16z(stg + q * K + 2 * pr, row + 2 * pr, (mb[q] >> (2 * pr)) & 3u, rp);
-                        }
-                        cp_async_wait_all();
-#pragma unroll
-                        for (int q = 0; q < Q; ++q) {
-                            if (src[q] < 0) continue;
-                            if (hs[q] != cur) {
-                                while (cur < hs[q]) {
-                                    flush(cur, first, ws, we, hub_mode, acc, aovf);
-                                    ++cur;
-                                    if (!hub_mode) prefetch_sigma(cur);
-#pragma unroll
-                                    for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
-                                    aovf = 0;
-                                }
-                            }
-                            const V *sv = reinterpret_cast<const V *>(stg + q * K);
-#pragma unroll
-                            for (int pr = 0; pr < W; ++pr) {
-                                const V t = sv[pr];
-                                acc[2 * pr] += t.x;
-                                acc[2 * pr + 1] += t.y;
-                            }
-                            if (!BWD) st_dag += __popc(mb[q]);
-                            st_hits += (lane == 0);
-                        }
-                        continue;
-                    }
                     V val[Q][W];
                     uint32_t po[Q];
 #pragma unroll
@@ -447,6 +412,7 @@ struct LanesKernel {
                         st_hits += (lane == 0);
                     }
                 }
+                __syncwarp();  // the step's shared hit records are reused by the next step
             }
         }
         while (cur <= last) {
