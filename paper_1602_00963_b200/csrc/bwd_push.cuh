@@ -36,12 +36,18 @@ __device__ __forceinline__ void red_add_f64(double *p, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
+#ifndef BC_PUSH_MINB
+#define BC_PUSH_MINB 4  // push kernels need fewer registers: 4 CTAs (32 warps) per SM
+#endif
+
 template <int W>
 struct PushSmem {
     int vert[TV];
     int cd[TV + 1];
     int rs[TV];
     uint64_t u[TV * W];
+    uint64_t hc[BC_NW * 32 * W];  // per warp: contributing-lane words of the step's items
+    int4 hsv[BC_NW * 32];         // per warp: (slot, y, group mask, -) of the step's items
     int scan[2 * BC_NW + 2];
     int unit;
 };
@@ -157,12 +163,19 @@ struct PushKernel {
                     if ((uint32_t)(cc[k][j >> 1] >> ((j & 1) * 32))) gmk |= 1u << j;
                 unsigned hm = __ballot_sync(0xffffffffu, gmk != 0);
                 st_hits += (lane == 0) ? __popc(hm) : 0;
+                if (hm == 0) continue;
+                int4 *hsv = sm.hsv + wid * 32;
+                const uint32_t *hc32 = reinterpret_cast<const uint32_t *>(sm.hc + wid * 32 * W);
+                hsv[lane] = make_int4(sl[k], vv[k], (int)gmk, 0);
+#pragma unroll
+                for (int j = 0; j < W; ++j) sm.hc[(wid * 32 + lane) * W + j] = cc[k][j];
+                __syncwarp();
                 while (hm) {
                     const int src = __ffs(hm) - 1;
                     hm &= hm - 1;
-                    const int hs = __shfl_sync(0xffffffffu, sl[k], src);
-                    const int y = __shfl_sync(0xffffffffu, vv[k], src);
-                    const uint32_t gm = __shfl_sync(0xffffffffu, gmk, src);
+                    const int4 rec = hsv[src];
+                    const int hs = rec.x, y = rec.y;
+                    const uint32_t gm = (uint32_t)rec.z;
                     if (hs != cur) {  // warp-uniform: coef row of the new slot
                         cur = hs;
                         const double *row = S + (size_t)sm.vert[hs] * K + lane;
@@ -174,8 +187,7 @@ struct PushKernel {
 #pragma unroll
                     for (int j = 0; j < NG; ++j) {
                         if (gm >> j & 1u) {  // uniform
-                            const uint32_t cw =
-                                __shfl_sync(0xffffffffu, (uint32_t)(cc[k][j >> 1] >> ((j & 1) * 32)), src);
+                            const uint32_t cw = hc32[src * 2 * W + j];
                             if (cw >> lane & 1u) {
                                 red_add_f64(arow + 32 * j, cf[j]);
                                 if (FWD) ++st_dag;
@@ -186,6 +198,7 @@ struct PushKernel {
                     if (FWD && myword) atomicOr((unsigned long long *)(p.mask_nxt + (size_t)y * W + lane),
                                                 (unsigned long long)myword);
                 }
+                __syncwarp();
             }
         }
     }
@@ -283,7 +296,7 @@ struct PushKernel {
 };
 
 template <int W, bool FWD>
-__global__ void __launch_bounds__(BC_NT, BC_MINB) lanes_push_kernel(LanesParams p, double *A) {
+__global__ void __launch_bounds__(BC_NT, BC_PUSH_MINB) lanes_push_kernel(LanesParams p, double *A) {
     __shared__ PushSmem<W> sm;
     PushKernel<W, FWD> k(p, A, sm);
     const int total = p.nseg + p.ntiles;
