@@ -109,7 +109,7 @@ struct LanesParams {
 };
 
 #ifndef BC_U4
-#define BC_U4 2  // sigma rows in flight per warp at W = 4
+#define BC_U4 1  // sigma rows in flight per warp at W = 4 (more resident warps beat deeper per-warp MLP)
 #endif
 #ifndef BC_R4
 #define BC_R4 2  // item steps in flight per warp at W = 4
@@ -586,7 +586,7 @@ struct LanesKernel {
 #endif
 
 template <int W, typename SigT, bool BWD>
-__global__ void __launch_bounds__(BC_NT, BC_MINB) lanes_level_kernel(LanesParams p) {
+__global__ void __launch_bounds__(BC_NT, (W == 4 ? BC_MINB + 1 : BC_MINB)) lanes_level_kernel(LanesParams p) {
     extern __shared__ __align__(16) unsigned char smraw[];
     LanesSmem<W, SigT> &sm = *reinterpret_cast<LanesSmem<W, SigT> *>(smraw);
     LanesKernel<W, SigT, BWD> k(p, sm);
