@@ -46,7 +46,7 @@ struct PushSmem {
     int cd[TV + 1];
     int rs[TV];
     uint64_t u[TV * W];
-    uint64_t hc[BC_NW * 32 * W];  // per warp: contributing-lane words of the step's items
+    alignas(16) uint64_t hc[BC_NW * 32 * W];  // per warp: contributing-lane words of the step's items
     int4 hsv[BC_NW * 32];         // per warp: (slot, y, group mask, -) of the step's items
     int scan[2 * BC_NW + 2];
     int unit;
@@ -146,12 +146,13 @@ struct PushKernel {
 #pragma unroll
             for (int k = 0; k < R; ++k) {
 #pragma unroll
-                for (int j = 0; j < W; ++j) {
-                    cc[k][j] = 0;
-                    if (sl[k] >= 0) {
-                        uint64_t mv = __ldg(mpar + (size_t)vv[k] * W + j);
-                        if (FWD) mv = p.active[j] & ~mv;
-                        cc[k][j] = sm.u[sl[k] * W + j] & mv;
+                for (int j = 0; j < W; ++j) cc[k][j] = 0;
+                if (sl[k] >= 0) {
+                    load_mask<W>(mpar + (size_t)vv[k] * W, cc[k]);
+#pragma unroll
+                    for (int j = 0; j < W; ++j) {
+                        if (FWD) cc[k][j] = p.active[j] & ~cc[k][j];
+                        cc[k][j] &= sm.u[sl[k] * W + j];
                     }
                 }
             }
@@ -165,7 +166,6 @@ struct PushKernel {
                 st_hits += (lane == 0) ? __popc(hm) : 0;
                 if (hm == 0) continue;
                 int4 *hsv = sm.hsv + wid * 32;
-                const uint32_t *hc32 = reinterpret_cast<const uint32_t *>(sm.hc + wid * 32 * W);
                 hsv[lane] = make_int4(sl[k], vv[k], (int)gmk, 0);
 #pragma unroll
                 for (int j = 0; j < W; ++j) sm.hc[(wid * 32 + lane) * W + j] = cc[k][j];
@@ -184,10 +184,21 @@ struct PushKernel {
                     }
                     double *arow = A + (size_t)y * K + lane;
                     uint64_t myword = 0;  // fwd: thread j < W ORs word j of c into lvl[L+1][y]
+                    uint64_t cwords[W];
+#pragma unroll
+                    for (int j = 0; j < W; j += (W >= 2 ? 2 : 1)) {
+                        if constexpr (W >= 2) {
+                            const ulonglong2 t = reinterpret_cast<const ulonglong2 *>(sm.hc + (wid * 32 + src) * W)[j / 2];
+                            cwords[j] = t.x;
+                            cwords[j + 1] = t.y;
+                        } else {
+                            cwords[0] = sm.hc[wid * 32 + src];
+                        }
+                    }
 #pragma unroll
                     for (int j = 0; j < NG; ++j) {
                         if (gm >> j & 1u) {  // uniform
-                            const uint32_t cw = hc32[src * 2 * W + j];
+                            const uint32_t cw = (uint32_t)(cwords[j >> 1] >> ((j & 1) * 32));
                             if (cw >> lane & 1u) {
                                 red_add_f64(arow + 32 * j, cf[j]);
                                 if (FWD) ++st_dag;

@@ -74,6 +74,22 @@ __device__ __forceinline__ void cp_async16z(void *smem_dst, const void *gsrc, bo
                  : "memory");
 }
 
+// the W mask words of one vertex with as few L1 wavefronts as possible
+// (one 16-byte load per two words; all words share one 32-byte sector)
+template <int W>
+__device__ __forceinline__ void load_mask(const uint64_t *p, uint64_t (&m)[W]) {
+    if constexpr (W >= 2) {
+#pragma unroll
+        for (int j = 0; j < W; j += 2) {
+            const ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2 *>(p + j));
+            m[j] = t.x;
+            m[j + 1] = t.y;
+        }
+    } else {
+        m[0] = __ldg(p);
+    }
+}
+
 struct LanesParams {
     int n;
     const int *rp;               // residual CSR row_ptr (int32, n+1)
@@ -323,9 +339,11 @@ struct LanesKernel {
 #pragma unroll
             for (int k = 0; k < R; ++k) {
 #pragma unroll
-                for (int j = 0; j < W; ++j) {
-                    cc[k][j] = 0;
-                    if (sl[k] >= 0) cc[k][j] = sm.u[sl[k] * W + j] & __ldg(mread + (size_t)vv[k] * W + j);
+                for (int j = 0; j < W; ++j) cc[k][j] = 0;
+                if (sl[k] >= 0) {
+                    load_mask<W>(mread + (size_t)vv[k] * W, cc[k]);
+#pragma unroll
+                    for (int j = 0; j < W; ++j) cc[k][j] &= sm.u[sl[k] * W + j];
                 }
             }
 #pragma unroll
