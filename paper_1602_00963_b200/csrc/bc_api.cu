@@ -534,17 +534,13 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
     CU(cudaGetLastError());
     g->last.kernel_launches += 4;
 
-    auto kf = lanes_level_kernel<W, SigT, false>;
+    auto kf = lanes_level_kernel<W, SigT>;
     const int units = p.nseg + p.ntiles;
     constexpr size_t SMEM = sizeof(LanesSmem<W, SigT>);
     const int grid = level_grid(g, kf, units, SMEM);
     {
-        auto kh = lanes_hub_finalize<W, SigT, false>;
+        auto kh = lanes_hub_finalize<W, SigT>;
         cudaFuncSetAttribute(kh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-        auto kb = lanes_level_kernel<W, SigT, true>;
-        cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-        auto khb = lanes_hub_finalize<W, SigT, true>;
-        cudaFuncSetAttribute(khb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
     }
     const int hub_grid = (c.csr->nhub * 32 + BC_NT - 1) / BC_NT;
 
@@ -584,7 +580,7 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
         }
         if (!pushed) {
             kf<<<grid, BC_NT, SMEM, st>>>(p);
-            if (p.nhub > 0) lanes_hub_finalize<W, SigT, false><<<hub_grid, BC_NT, SMEM, st>>>(p);
+            if (p.nhub > 0) lanes_hub_finalize<W, SigT><<<hub_grid, BC_NT, SMEM, st>>>(p);
         }
         if (ev_f) {
             cudaEventRecord(e1, st);
@@ -608,7 +604,6 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
     }
     if constexpr (std::is_same<SigT, double>::value) {
         if (c.run_backward) {
-#ifndef BC_BWD_PULL
             // push-form backward (bwd_push.cuh): finalize level L, then push its
             // coef rows into the parents' accumulators
             auto kpush = lanes_push_kernel<W, false>;
@@ -652,36 +647,6 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
                 g->last.bwd_launches += 1;
                 g->last.kernel_launches += 1 + (l >= 2);
             }
-#else
-            auto kb = lanes_level_kernel<W, SigT, true>;
-            const int gridb = level_grid(g, kb, units, SMEM);
-            p.dbg_delta = c.dbg_delta;
-            for (int l = Lmax; l >= 1; --l) {
-                p.level = l;
-                p.S_cur = ws.slev[l];
-                p.S_nxt = ws.slev[l + 1];
-                p.mask_cur = level_ptr(g, ws, l);
-                p.mask_nxt_ro = level_ptr(g, ws, l + 1);  // zero for l == Lmax
-                p.mask_nxt = nullptr;
-                p.any_new = g->d_flags;  // unused
-                cudaEvent_t e0 = nullptr, e1 = nullptr;
-                if (ev_b) {
-                    cudaEventCreate(&e0);
-                    cudaEventCreate(&e1);
-                    cudaEventRecord(e0, st);
-                }
-                kb<<<gridb, BC_NT, SMEM, st>>>(p);
-                if (p.nhub > 0) lanes_hub_finalize<W, SigT, true><<<hub_grid, BC_NT, SMEM, st>>>(p);
-                if (ev_b) {
-                    cudaEventRecord(e1, st);
-                    ev_b->push_back(e0);
-                    ev_b->push_back(e1);
-                }
-                CU(cudaGetLastError());
-                g->last.bwd_launches += 1;
-                g->last.kernel_launches += 1 + (p.nhub > 0);
-            }
-#endif
             if (c.endpoint && c.omega) {
                 lanes_endpoint_kernel<<<(c.nl + 255) / 256, 256, 0, st>>>(c.src, c.nl, c.omega, ws.lane_ns,
                                                                          g->d_bc);

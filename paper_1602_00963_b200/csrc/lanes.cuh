@@ -90,6 +90,21 @@ __device__ __forceinline__ void load_mask(const uint64_t *p, uint64_t (&m)[W]) {
     }
 }
 
+// the W words of one hit record in shared memory (broadcast reads)
+template <int W>
+__device__ __forceinline__ void load_mask_smem(const uint64_t *p, uint64_t (&m)[W]) {
+    if constexpr (W >= 2) {
+#pragma unroll
+        for (int j = 0; j < W; j += 2) {
+            const ulonglong2 t = *reinterpret_cast<const ulonglong2 *>(p + j);
+            m[j] = t.x;
+            m[j + 1] = t.y;
+        }
+    } else {
+        m[0] = *p;
+    }
+}
+
 struct LanesParams {
     int n;
     const int *rp;               // residual CSR row_ptr (int32, n+1)
@@ -144,12 +159,52 @@ struct LanesSmem {
     int2 hsv[BC_NW * 32];                     // per warp: (slot, v) of the step's items
     uint32_t povf[BC_NW * 2 * 32];
     double ns[64 * W];  // per-lane n_s partial sums of this CTA (pruned graphs)
-    alignas(16) double sgs[BC_NW * 64 * W];  // backward: per-warp prefetched sigma row of the current slot
     int scan[2 * BC_NW + 2];
     int unit;
 };
 
-template <int W, typename SigT, bool BWD>
+// Lane -> thread mapping of the level kernel ("pair-strided"): thread t of
+// a warp owns the LPT = 2W lanes lane_of(i) = 64*(i/2) + 2t + (i%2), i.e.
+// bits 2t, 2t+1 of every mask word.  A row gather is then W 16-byte loads
+// per thread whose warp footprint is W contiguous 512-byte spans (4 L1
+// wavefronts each), and the thread's bits of any mask are pick2(words).
+template <int W>
+__device__ __forceinline__ uint32_t pick2(const uint64_t (&w)[W], int t2) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int j = 0; j < W; ++j) r |= (uint32_t)((w[j] >> t2) & 3ull) << (2 * j);
+    return r;
+}
+// bit t of a, b -> bits 2t, 2t+1 of the result
+__device__ __forceinline__ uint64_t interleave2(uint32_t a, uint32_t b) {
+    uint64_t x = a, y = b;
+    x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
+    y = (y | (y << 16)) & 0x0000FFFF0000FFFFull;
+    x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
+    y = (y | (y << 8)) & 0x00FF00FF00FF00FFull;
+    x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
+    y = (y | (y << 4)) & 0x0F0F0F0F0F0F0F0Full;
+    x = (x | (x << 2)) & 0x3333333333333333ull;
+    y = (y | (y << 2)) & 0x3333333333333333ull;
+    x = (x | (x << 1)) & 0x5555555555555555ull;
+    y = (y | (y << 1)) & 0x5555555555555555ull;
+    return x | (y << 1);
+}
+// warp-collective: the W mask words whose thread-t bits are bits of `bits`;
+// word j is returned to lane j (other lanes: 0)
+template <int W>
+__device__ __forceinline__ uint64_t gather_words(uint32_t bits, int lane) {
+    uint64_t mine = 0;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        const uint32_t b0 = __ballot_sync(0xffffffffu, (bits >> (2 * j)) & 1u);
+        const uint32_t b1 = __ballot_sync(0xffffffffu, (bits >> (2 * j + 1)) & 1u);
+        if (lane == j) mine = interleave2(b0, b1);
+    }
+    return mine;
+}
+
+template <int W, typename SigT>
 struct LanesKernel {
     static constexpr int K = 64 * W;
     static constexpr int LPT = 2 * W;           // lanes per thread
@@ -157,25 +212,25 @@ struct LanesKernel {
     static constexpr int U = (W == 1) ? 4 : (W == 2 ? 2 : BC_U4);  // sigma rows in flight per warp
     static constexpr bool VERIFY = std::is_same<SigT, unsigned long long>::value;
     static constexpr int Q = U;
-    static constexpr int GROUP = 32 / W;        // threads sharing one mask word
     using V = typename Vec2<SigT>::t;
     using Smem = LanesSmem<W, SigT>;
 
     const LanesParams &p;
     Smem &sm;
-    const int lane, wid, my_word, my_off;
-    const uint64_t lm;
+    const int lane, wid, t2;
     unsigned long long st_reach = 0, st_adj = 0, st_dag = 0, st_dsum = 0, st_items = 0, st_hits = 0;
     int any_new_loc = 0;
 
     __device__ LanesKernel(const LanesParams &pp, Smem &s)
-        : p(pp), sm(s), lane(lane_id()), wid(warp_id()), my_word((lane_id() * LPT) >> 6),
-          my_off((lane_id() * LPT) & 63), lm((1ull << LPT) - 1ull) {
-        if (!BWD && p.lane_ns) {
+        : p(pp), sm(s), lane(lane_id()), wid(warp_id()), t2(2 * lane_id()) {
+        if (p.lane_ns) {
             for (int l = threadIdx.x; l < K; l += BC_NT) sm.ns[l] = 0.0;
             __syncthreads();
         }
     }
+
+    // lane index of this thread's i-th accumulator
+    __device__ __forceinline__ int lane_of(int i) const { return 64 * (i >> 1) + t2 + (i & 1); }
 
     __device__ __forceinline__ SigT *Scur() const { return reinterpret_cast<SigT *>(p.S_cur); }
     __device__ __forceinline__ SigT *part_row(int w, int idx) const {
@@ -183,14 +238,22 @@ struct LanesKernel {
     }
     __device__ __forceinline__ SigT *Snxt() const { return reinterpret_cast<SigT *>(p.S_nxt); }
 
-    // write this thread's LPT-lane slice of a row: v[i] where bit i of keep, else 0
+    // this thread's bits of the W words at w (shared or global, generic load)
+    __device__ __forceinline__ uint32_t bits_of(const uint64_t *w) const {
+        uint64_t m[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) m[j] = w[j];
+        return pick2<W>(m, t2);
+    }
+
+    // write this thread's lanes of a row: v[i] where bit i of keep, else 0
     __device__ __forceinline__ void store_slice(SigT *row, uint32_t keep, const SigT (&v)[LPT]) {
 #pragma unroll
         for (int pr = 0; pr < W; ++pr) {
             V t;
             t.x = (keep >> (2 * pr) & 1u) ? v[2 * pr] : SigT(0);
             t.y = (keep >> (2 * pr + 1) & 1u) ? v[2 * pr + 1] : SigT(0);
-            reinterpret_cast<V *>(row)[pr] = t;
+            *reinterpret_cast<V *>(row + 64 * pr + t2) = t;
         }
     }
 
@@ -204,7 +267,8 @@ struct LanesKernel {
         nb &= ub;
         aovf &= ub;
         const bool any = __any_sync(0xffffffffu, nb != 0);
-        if (any) store_slice(Snxt() + (size_t)x * K + lane * LPT, nb, acc);
+        if (!any) return;  // warp-uniform
+        store_slice(Snxt() + (size_t)x * K, nb, acc);
         if (nb) {
             any_new_loc = 1;
             int pc = __popc(nb);
@@ -215,81 +279,23 @@ struct LanesKernel {
                 double wx = 1.0 + (p.omega ? (double)p.omega[x] : 0.0);
 #pragma unroll
                 for (int i = 0; i < LPT; ++i)
-                    if (nb >> i & 1u) atomicAdd(&sm.ns[lane * LPT + i], wx);
+                    if (nb >> i & 1u) atomicAdd(&sm.ns[lane_of(i)], wx);
             }
         }
-        uint64_t wv = (uint64_t)nb << my_off;
-        uint64_t ov = (uint64_t)aovf << my_off;
-#pragma unroll
-        for (int o = 1; o < GROUP; o <<= 1) {
-            wv |= __shfl_xor_sync(0xffffffffu, wv, o);
-            if (VERIFY) ov |= __shfl_xor_sync(0xffffffffu, ov, o);
-        }
-        if ((lane & (GROUP - 1)) == 0 && wv) {
-            size_t wi = (size_t)x * W + my_word;
+        const uint64_t wv = gather_words<W>(nb, lane);
+        uint64_t ov = 0;
+        if (VERIFY) ov = gather_words<W>(aovf, lane);
+        if (lane < W && wv) {
+            size_t wi = (size_t)x * W + lane;
             p.mask_nxt[wi] = wv;
             p.seen[wi] |= wv;
             if (VERIFY && ov) p.ovf[wi] |= ov;
         }
     }
 
-    // ---- backward commit: finalise x at level L in the lanes of mb; the
-    // level-L row of x becomes its coef row (zeros outside level L)
-    __device__ void commit_bwd(int x, uint32_t mb, const SigT (&acc)[LPT], bool staged = false) {
-        double contrib = 0.0;
-        if constexpr (!VERIFY) {
-            if (__any_sync(0xffffffffu, mb != 0)) {
-                const double om = p.omega ? (double)p.omega[x] : 0.0;
-                double *row = Scur() + (size_t)x * K + lane * LPT;
-                const double *sgsrc = staged ? (const double *)(sm.sgs + wid * K + lane * LPT) : (const double *)row;
-                if (staged) cp_async_wait_all();
-                double cf[LPT];
-#pragma unroll
-                for (int pr = 0; pr < W; ++pr) {
-                    double2 sg = make_double2(0.0, 0.0);
-                    if ((mb >> (2 * pr)) & 3u) sg = reinterpret_cast<const double2 *>(sgsrc)[pr];
-                    const double sgv[2] = {sg.x, sg.y};
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int i = 2 * pr + h;
-                        cf[i] = 0.0;
-                        if (mb >> i & 1u) {
-                            const double delta = sgv[h] * acc[i];
-                            cf[i] = (1.0 + om + delta) / sgv[h];
-                            contrib += p.lane_w1[lane * LPT + i] * (delta + om);
-                            if (i == 0 && lane == 0 && p.dbg_delta) p.dbg_delta[x] = delta;
-                        }
-                    }
-                }
-                store_slice(row, mb, cf);
-            }
-        }
-        contrib = warp_sum(contrib);
-        if (lane == 0 && contrib != 0.0) p.bc[x] += contrib;
-    }
-
-    // backward: start fetching the level-L sigma row slice of slot s into the
-    // warp's staging buffer (consumed by the slot's commit)
-    __device__ __forceinline__ void prefetch_sigma(int s) {
-        if constexpr (BWD && !VERIFY) {
-            cp_async_wait_all();  // an unconsumed earlier prefetch must land before the buffer is reused
-            const uint32_t mb = (uint32_t)((sm.u[s * W + my_word] >> my_off) & lm);
-            const double *row = Scur() + (size_t)sm.vert[s] * K + lane * LPT;
-            double *dst = sm.sgs + wid * K + lane * LPT;
-#pragma unroll
-            for (int pr = 0; pr < W; ++pr)
-                if ((mb >> (2 * pr)) & 3u) cp_async16(dst + 2 * pr, row + 2 * pr);
-        }
-    }
-
-    __device__ void commit_slot(int s, const SigT (&acc)[LPT], uint32_t aovf, bool staged = false) {
-        if (BWD) {
-            uint32_t mb = (uint32_t)((sm.u[s * W + my_word] >> my_off) & lm);
-            commit_bwd(sm.vert[s], mb, acc, staged);
-        } else {
-            const uint32_t ub = (uint32_t)((sm.u[s * W + my_word] >> my_off) & lm);
-            commit_fwd(sm.vert[s], sm.cd[s + 1] - sm.cd[s], ub, acc, aovf);
-        }
+    __device__ __forceinline__ void commit_slot(int s, const SigT (&acc)[LPT], uint32_t aovf) {
+        const uint32_t ub = bits_of(sm.u + s * W);
+        commit_fwd(sm.vert[s], sm.cd[s + 1] - sm.cd[s], ub, acc, aovf);
     }
 
     // flush the running accumulator of slot s (warp-uniform)
@@ -297,23 +303,27 @@ struct LanesKernel {
                           uint32_t aovf) {
         bool owned = !hub_mode && sm.cd[s] >= ws && sm.cd[s + 1] <= we;
         if (owned) {
-            commit_slot(s, acc, aovf, true);
+            commit_slot(s, acc, aovf);
         } else {
             int idx = (s == first) ? 0 : 1;
-            SigT *dst = part_row(wid, idx) + lane * LPT;
+            SigT *dst = part_row(wid, idx);
 #pragma unroll
-            for (int i = 0; i < LPT; ++i) dst[i] = acc[i];
+            for (int pr = 0; pr < W; ++pr) {
+                V t;
+                t.x = acc[2 * pr];
+                t.y = acc[2 * pr + 1];
+                *reinterpret_cast<V *>(dst + 64 * pr + t2) = t;
+            }
             if (VERIFY) sm.povf[(wid * 2 + idx) * 32 + lane] = aovf;
         }
     }
 
     // One warp walks items [ws, we) of the current tile (slots in sm).
     __device__ void warp_walk(int nslots, int ws, int we, bool hub_mode) {
-        const uint64_t *mread = BWD ? p.mask_nxt_ro : p.mask_cur;
+        const uint64_t *mread = p.mask_cur;
         int cur = slot_of(sm.cd, nslots, ws);
         const int first = cur;
         const int last = slot_of(sm.cd, nslots, we - 1);
-        if (!hub_mode) prefetch_sigma(cur);
         SigT acc[LPT];
 #pragma unroll
         for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
@@ -354,7 +364,7 @@ struct LanesKernel {
                 unsigned hm = __ballot_sync(0xffffffffu, h);
                 if (hm == 0) continue;
                 // publish (slot, v, c) of every item of this step in shared memory:
-                // a hit then costs two shared loads instead of 2 + 2W shuffles
+                // a hit then costs shared broadcasts instead of 2 + 2W shuffles
                 {
                     int2 *hsv = sm.hsv + wid * 32;
                     uint64_t *hc = sm.hc + wid * 32 * W;
@@ -380,26 +390,30 @@ struct LanesKernel {
                             const int2 sv = sm.hsv[wid * 32 + src[q]];
                             hs[q] = sv.x;
                             hv[q] = sv.y;
-                            const uint32_t *cw = reinterpret_cast<const uint32_t *>(sm.hc + (wid * 32 + src[q]) * W);
-                            mb[q] = (cw[(lane * LPT) >> 5] >> ((lane * LPT) & 31)) & (uint32_t)lm;
+                            uint64_t cw[W];
+                            load_mask_smem<W>(sm.hc + (wid * 32 + src[q]) * W, cw);
+                            mb[q] = pick2<W>(cw, t2);
                         }
                     }
-                    const SigT *Sread = BWD ? Snxt() : Scur();
+                    const SigT *Sread = Scur();
                     V val[Q][W];
                     uint32_t po[Q];
 #pragma unroll
                     for (int q = 0; q < Q; ++q) {
-                        const V *rowv = reinterpret_cast<const V *>(Sread + (size_t)hv[q] * K + lane * LPT);
+                        const V *rowv = reinterpret_cast<const V *>(Sread + (size_t)hv[q] * K + t2);
                         const uint64_t rp = (hv[q] < BC_L2HOT) ? pol_last : pol;
 #pragma unroll
                         for (int pr = 0; pr < W; ++pr) {
                             val[q][pr].x = SigT(0);
                             val[q][pr].y = SigT(0);
-                            if ((mb[q] >> (2 * pr)) & 3u) val[q][pr] = ld_pol(rowv + pr, rp);
+                            if ((mb[q] >> (2 * pr)) & 3u) val[q][pr] = ld_pol(rowv + 32 * pr, rp);
                         }
                         po[q] = 0;
-                        if (VERIFY && mb[q])
-                            po[q] = mb[q] & (uint32_t)((__ldg(p.ovf + (size_t)hv[q] * W + my_word) >> my_off) & lm);
+                        if (VERIFY && mb[q]) {
+                            uint64_t ow[W];
+                            load_mask<W>(p.ovf + (size_t)hv[q] * W, ow);
+                            po[q] = mb[q] & pick2<W>(ow, t2);
+                        }
                     }
 #pragma unroll
                     for (int q = 0; q < Q; ++q) {
@@ -408,7 +422,6 @@ struct LanesKernel {
                             while (cur < hs[q]) {
                                 flush(cur, first, ws, we, hub_mode, acc, aovf);
                                 ++cur;
-                                if (!hub_mode) prefetch_sigma(cur);
 #pragma unroll
                                 for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
                                 aovf = 0;
@@ -426,7 +439,7 @@ struct LanesKernel {
                             if (VERIFY && acc[2 * pr + 1] < o) aovf |= 1u << (2 * pr + 1);
                         }
                         aovf |= po[q];
-                        if (!BWD) st_dag += __popc(mb[q]);
+                        st_dag += __popc(mb[q]);
                         st_hits += (lane == 0);
                     }
                 }
@@ -436,7 +449,6 @@ struct LanesKernel {
         while (cur <= last) {
             flush(cur, first, ws, we, hub_mode, acc, aovf);
             ++cur;
-            if (!hub_mode && cur <= last) prefetch_sigma(cur);
 #pragma unroll
             for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
             aovf = 0;
@@ -462,8 +474,7 @@ struct LanesKernel {
             if (deg > 0 && deg <= p.hub_deg) {
 #pragma unroll
                 for (int j = 0; j < W; ++j) {
-                    if (BWD) u[j] = p.mask_cur[(size_t)x * W + j];
-                    else u[j] = p.active[j] & ~p.seen[(size_t)x * W + j];
+                    u[j] = p.active[j] & ~p.seen[(size_t)x * W + j];
                     act |= (u[j] != 0);
                 }
             }
@@ -497,11 +508,11 @@ struct LanesKernel {
                         int a0 = bnd(w, nitems), a1 = bnd(w + 1, nitems);
                         if (a0 >= a1 || a1 <= sm.cd[s] || a0 >= sm.cd[s + 1]) continue;
                         int idx = (sm.cd[s] <= a0) ? 0 : 1;
-                        const SigT *src = part_row(w, idx) + lane * LPT;
+                        const SigT *src = part_row(w, idx);
 #pragma unroll
                         for (int i = 0; i < LPT; ++i) {
                             SigT o = acc[i];
-                            acc[i] = o + src[i];
+                            acc[i] = o + src[lane_of(i)];
                             if (VERIFY && acc[i] < o) aovf |= 1u << i;
                         }
                         if (VERIFY) aovf |= sm.povf[(w * 2 + idx) * 32 + lane];
@@ -535,8 +546,7 @@ struct LanesKernel {
         bool any = false;
 #pragma unroll
         for (int j = 0; j < W; ++j) {
-            if (BWD) u[j] = p.mask_cur[(size_t)x * W + j];
-            else u[j] = p.active[j] & ~p.seen[(size_t)x * W + j];
+            u[j] = p.active[j] & ~p.seen[(size_t)x * W + j];
             any |= (u[j] != 0);
         }
         if (!any) return;  // uniform
@@ -557,7 +567,7 @@ struct LanesKernel {
         for (int l = threadIdx.x; l < K; l += BC_NT) {
             SigT sum = SigT(0);
             bool ovf = false;
-            const int tl = l / LPT, ti = l % LPT;
+            const int tl = (l & 63) >> 1, ti = 2 * (l >> 6) + (l & 1);  // owner thread / acc index of lane l
             for (int w = 0; w < BC_NW; ++w) {
                 if (bnd(w, nitems) >= bnd(w + 1, nitems)) continue;
                 SigT o = sum;
@@ -586,12 +596,12 @@ struct LanesKernel {
         }
         const unsigned long long it = warp_sum_u64(st_items), ht = warp_sum_u64(st_hits);
         if (lane == 0) {
-            if (it) atomicAdd(p.stats + (BWD ? 6 : 4), it);
-            if (ht) atomicAdd(p.stats + (BWD ? 7 : 5), ht);
+            if (it) atomicAdd(p.stats + 4, it);
+            if (ht) atomicAdd(p.stats + 5, ht);
         }
         int anyw = __any_sync(0xffffffffu, any_new_loc);
         if (lane == 0 && anyw) *p.any_new = 1;
-        if (!BWD && p.lane_ns) {
+        if (p.lane_ns) {
             __syncthreads();
             for (int l = threadIdx.x; l < K; l += BC_NT)
                 if (sm.ns[l] != 0.0) atomicAdd(p.lane_ns + l, sm.ns[l]);
@@ -603,11 +613,11 @@ struct LanesKernel {
 #define BC_MINB 2  // min resident CTAs per SM for the level kernels (register cap)
 #endif
 
-template <int W, typename SigT, bool BWD>
+template <int W, typename SigT>
 __global__ void __launch_bounds__(BC_NT, (W == 4 ? BC_MINB + 1 : BC_MINB)) lanes_level_kernel(LanesParams p) {
     extern __shared__ __align__(16) unsigned char smraw[];
     LanesSmem<W, SigT> &sm = *reinterpret_cast<LanesSmem<W, SigT> *>(smraw);
-    LanesKernel<W, SigT, BWD> k(p, sm);
+    LanesKernel<W, SigT> k(p, sm);
     const int total = p.nseg + p.ntiles;
     for (;;) {
         if (threadIdx.x == 0) {
@@ -625,11 +635,11 @@ __global__ void __launch_bounds__(BC_NT, (W == 4 ? BC_MINB + 1 : BC_MINB)) lanes
     k.epilogue();
 }
 
-// One warp per hub: commit the hub's summed row (forward) or finalise it
-// (backward).  Resets the scratch row for the next level.
-template <int W, typename SigT, bool BWD>
+// One warp per hub: commit the hub's summed row.  Resets the scratch row for
+// the next level.
+template <int W, typename SigT>
 __global__ void __launch_bounds__(BC_NT) lanes_hub_finalize(LanesParams p) {
-    using KK = LanesKernel<W, SigT, BWD>;
+    using KK = LanesKernel<W, SigT>;
     constexpr int K = KK::K, LPT = KK::LPT;
     extern __shared__ __align__(16) unsigned char smraw[];
     LanesSmem<W, SigT> &sm = *reinterpret_cast<LanesSmem<W, SigT> *>(smraw);
@@ -637,31 +647,25 @@ __global__ void __launch_bounds__(BC_NT) lanes_hub_finalize(LanesParams p) {
     const int h = (blockIdx.x * BC_NT + threadIdx.x) >> 5;
     if (h < p.nhub) {
         const int x = p.hub_ids[h];
-        SigT *row = reinterpret_cast<SigT *>(p.hub_acc) + (size_t)h * K + k.lane * LPT;
+        SigT *row = reinterpret_cast<SigT *>(p.hub_acc) + (size_t)h * K;
         SigT acc[LPT];
 #pragma unroll
         for (int i = 0; i < LPT; ++i) {
-            acc[i] = row[i];
-            if (acc[i] != SigT(0)) row[i] = SigT(0);
+            acc[i] = row[k.lane_of(i)];
+            if (acc[i] != SigT(0)) row[k.lane_of(i)] = SigT(0);
         }
-        if (BWD) {
-            uint32_t mb = (uint32_t)((p.mask_cur[(size_t)x * W + k.my_word] >> k.my_off) & k.lm);
-            k.commit_bwd(x, mb, acc);
-        } else {
-            uint32_t aovf = 0;
-            if (KK::VERIFY) {
-                uint64_t *ow = p.hub_ovf + (size_t)h * W + k.my_word;
-                aovf = (uint32_t)((*ow >> k.my_off) & k.lm);
-                __syncwarp();
-                if ((k.lane & (KK::GROUP - 1)) == 0) *ow = 0;
-            }
-            uint64_t um = 0;
+        uint32_t aovf = 0;
+        if (KK::VERIFY) {
+            uint64_t *ow = p.hub_ovf + (size_t)h * W;
+            aovf = k.bits_of(ow);
+            __syncwarp();
+            if (k.lane < W) ow[k.lane] = 0;
+        }
+        uint64_t um[W];
 #pragma unroll
-            for (int j = 0; j < W; ++j)
-                if (j == k.my_word) um = p.active[j] & ~p.seen[(size_t)x * W + j];
-            const uint32_t ub = (uint32_t)((um >> k.my_off) & k.lm);
-            k.commit_fwd(x, p.rp[x + 1] - p.rp[x], ub, acc, aovf);
-        }
+        for (int j = 0; j < W; ++j) um[j] = p.active[j] & ~p.seen[(size_t)x * W + j];
+        const uint32_t ub = pick2<W>(um, k.t2);
+        k.commit_fwd(x, p.rp[x + 1] - p.rp[x], ub, acc, aovf);
     }
     k.epilogue();
 }
