@@ -105,6 +105,26 @@ __device__ __forceinline__ void load_mask_smem(const uint64_t *p, uint64_t (&m)[
     }
 }
 
+// W 32-bit halves to / from shared memory with vector accesses
+template <int W>
+__device__ __forceinline__ void store_halves(uint32_t *d, const uint32_t (&h)[W]) {
+    if constexpr (W == 4) *reinterpret_cast<uint4 *>(d) = make_uint4(h[0], h[1], h[2], h[3]);
+    else if constexpr (W == 2) *reinterpret_cast<uint2 *>(d) = make_uint2(h[0], h[1]);
+    else d[0] = h[0];
+}
+template <int W>
+__device__ __forceinline__ void load_halves(const uint32_t *d, uint32_t (&h)[W]) {
+    if constexpr (W == 4) {
+        const uint4 t = *reinterpret_cast<const uint4 *>(d);
+        h[0] = t.x; h[1] = t.y; h[2] = t.z; h[3] = t.w;
+    } else if constexpr (W == 2) {
+        const uint2 t = *reinterpret_cast<const uint2 *>(d);
+        h[0] = t.x; h[1] = t.y;
+    } else {
+        h[0] = d[0];
+    }
+}
+
 struct LanesParams {
     int n;
     const int *rp;               // residual CSR row_ptr (int32, n+1)
@@ -139,14 +159,8 @@ struct LanesParams {
     void *part;                  // [gridDim][BC_NW][2][K] SigT: partial sums of slots split across warps
 };
 
-#ifndef BC_U4
-#define BC_U4 1  // sigma rows in flight per warp at W = 4 (more resident warps beat deeper per-warp MLP)
-#endif
 #ifndef BC_R4
 #define BC_R4 2  // item steps in flight per warp at W = 4
-#endif
-#ifndef BC_L2HOT
-#define BC_L2HOT 32768  // rows of the BC_L2HOT highest-degree vertices are gathered with L2 evict_last
 #endif
 
 template <int W, typename SigT>
@@ -155,10 +169,14 @@ struct LanesSmem {
     int cd[TV + 1];
     int rs[TV];
     uint64_t u[TV * W];
-    alignas(16) uint64_t hc[BC_NW * 32 * W];  // per warp: contributing-lane words c of the step's items
+    // per warp, per item of the step: the contributing-lane words c as 32-bit
+    // halves [lo_0..lo_{W-1}, hi_0..hi_{W-1}] (thread t reads the W halves
+    // holding its bits 2t, 2t+1 with one vector load)
+    alignas(16) uint32_t hc[BC_NW * 32 * 2 * W];
     int2 hsv[BC_NW * 32];                     // per warp: (slot, v) of the step's items
     uint32_t povf[BC_NW * 2 * 32];
     double ns[64 * W];  // per-lane n_s partial sums of this CTA (pruned graphs)
+    unsigned long long st[6];  // CTA statistics (flushed from 32-bit thread counters per work unit)
     int scan[2 * BC_NW + 2];
     int unit;
 };
@@ -209,24 +227,34 @@ struct LanesKernel {
     static constexpr int K = 64 * W;
     static constexpr int LPT = 2 * W;           // lanes per thread
     static constexpr int R = (W == 1) ? 4 : (W == 2 ? 2 : BC_R4);  // item steps in flight per warp
-    static constexpr int U = (W == 1) ? 4 : (W == 2 ? 2 : BC_U4);  // sigma rows in flight per warp
     static constexpr bool VERIFY = std::is_same<SigT, unsigned long long>::value;
-    static constexpr int Q = U;
     using V = typename Vec2<SigT>::t;
     using Smem = LanesSmem<W, SigT>;
 
     const LanesParams &p;
     Smem &sm;
     const int lane, wid, t2;
-    unsigned long long st_reach = 0, st_adj = 0, st_dag = 0, st_dsum = 0, st_items = 0, st_hits = 0;
+    // per-thread statistics of the current work unit (bounded by its items, so
+    // 32 bits suffice except the adjacency sum); flushed by flush_stats()
+    unsigned st_reach = 0, st_dag = 0, st_dsum = 0, st_items = 0, st_hits = 0;
+    unsigned long long st_adj = 0;
     int any_new_loc = 0;
 
     __device__ LanesKernel(const LanesParams &pp, Smem &s)
         : p(pp), sm(s), lane(lane_id()), wid(warp_id()), t2(2 * lane_id()) {
-        if (p.lane_ns) {
+        if (p.lane_ns)
             for (int l = threadIdx.x; l < K; l += BC_NT) sm.ns[l] = 0.0;
-            __syncthreads();
-        }
+        if (threadIdx.x < 6) sm.st[threadIdx.x] = 0;
+        __syncthreads();
+    }
+
+    __device__ void flush_stats() {
+        const unsigned long long v[6] = {st_reach, st_adj, st_dag, st_dsum, st_items, st_hits};
+#pragma unroll
+        for (int i = 0; i < 6; ++i)
+            if (v[i]) atomicAdd(&sm.st[i], v[i]);
+        st_reach = st_dag = st_dsum = st_items = st_hits = 0;
+        st_adj = 0;
     }
 
     // lane index of this thread's i-th accumulator
@@ -274,7 +302,7 @@ struct LanesKernel {
             int pc = __popc(nb);
             st_reach += pc;
             st_adj += (unsigned long long)pc * deg;
-            st_dsum += (unsigned long long)pc * (unsigned)(p.level + 1);
+            st_dsum += (unsigned)pc * (unsigned)(p.level + 1);
             if (p.lane_ns) {
                 double wx = 1.0 + (p.omega ? (double)p.omega[x] : 0.0);
 #pragma unroll
@@ -329,9 +357,8 @@ struct LanesKernel {
         for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
         uint32_t aovf = 0;
         const uint64_t pol = policy_evict_first();
-        const uint64_t pol_last = policy_evict_last();
 
-        st_items += (lane == 0) ? (unsigned long long)(we - ws) : 0ull;
+        st_items += (lane == 0) ? (unsigned)(we - ws) : 0u;
         for (int e0 = ws; e0 < we; e0 += 32 * R) {
             int sl[R], vv[R];
 #pragma unroll
@@ -360,87 +387,82 @@ struct LanesKernel {
             for (int k = 0; k < R; ++k) {
                 bool h = false;
 #pragma unroll
-                for (int j = 0; j < W; ++j) h |= (cc[k][j] != 0);
+                for (int j = 0; j < W; ++j) {
+                    h |= (cc[k][j] != 0);
+                    st_dag += (unsigned)__popcll(cc[k][j]);
+                }
                 unsigned hm = __ballot_sync(0xffffffffu, h);
                 if (hm == 0) continue;
+                st_hits += (lane == 0) ? __popc(hm) : 0;
                 // publish (slot, v, c) of every item of this step in shared memory:
-                // a hit then costs shared broadcasts instead of 2 + 2W shuffles
+                // a hit then costs two shared broadcasts instead of 2 + 2W shuffles
                 {
-                    int2 *hsv = sm.hsv + wid * 32;
-                    uint64_t *hc = sm.hc + wid * 32 * W;
-                    hsv[lane] = make_int2(sl[k], vv[k]);
+                    sm.hsv[wid * 32 + lane] = make_int2(sl[k], vv[k]);
+                    uint32_t *hc = sm.hc + (wid * 32 + lane) * 2 * W;
+                    uint32_t lo[W], hi[W];
 #pragma unroll
-                    for (int j = 0; j < W; ++j) hc[lane * W + j] = cc[k][j];
+                    for (int j = 0; j < W; ++j) {
+                        lo[j] = (uint32_t)cc[k][j];
+                        hi[j] = (uint32_t)(cc[k][j] >> 32);
+                    }
+                    store_halves<W>(hc, lo);
+                    store_halves<W>(hc + W, hi);
                     __syncwarp();
                 }
+                const uint32_t *hcw = sm.hc + wid * 32 * 2 * W + (lane >> 4) * W;
+                const int sh = t2 & 31;
                 while (hm) {
-                    int src[Q], hs[Q], hv[Q];
-                    uint32_t mb[Q];
+                    const int src = __ffs(hm) - 1;
+                    hm &= hm - 1;
+                    const int2 sv = sm.hsv[wid * 32 + src];
+                    uint32_t cw[W];
+                    load_halves<W>(hcw + src * 2 * W, cw);
+                    if (sv.x != cur) {
+                        while (cur < sv.x) {
+                            flush(cur, first, ws, we, hub_mode, acc, aovf);
+                            ++cur;
 #pragma unroll
-                    for (int q = 0; q < Q; ++q) {
-                        src[q] = hm ? (__ffs(hm) - 1) : -1;
-                        if (hm) hm &= hm - 1;
-                    }
-#pragma unroll
-                    for (int q = 0; q < Q; ++q) {
-                        hs[q] = -1;
-                        hv[q] = 0;
-                        mb[q] = 0;
-                        if (src[q] >= 0) {
-                            const int2 sv = sm.hsv[wid * 32 + src[q]];
-                            hs[q] = sv.x;
-                            hv[q] = sv.y;
-                            uint64_t cw[W];
-                            load_mask_smem<W>(sm.hc + (wid * 32 + src[q]) * W, cw);
-                            mb[q] = pick2<W>(cw, t2);
+                            for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
+                            aovf = 0;
                         }
                     }
-                    const SigT *Sread = Scur();
-                    V val[Q][W];
-                    uint32_t po[Q];
-#pragma unroll
-                    for (int q = 0; q < Q; ++q) {
-                        const V *rowv = reinterpret_cast<const V *>(Sread + (size_t)hv[q] * K + t2);
-                        const uint64_t rp = (hv[q] < BC_L2HOT) ? pol_last : pol;
+                    // rows are zero outside their level: add whole pairs
+                    // (lanes outside c only collect values the commit discards)
+                    const V *rowv = reinterpret_cast<const V *>(Scur() + (size_t)sv.y * K + t2);
+                    if constexpr (!VERIFY) {
 #pragma unroll
                         for (int pr = 0; pr < W; ++pr) {
-                            val[q][pr].x = SigT(0);
-                            val[q][pr].y = SigT(0);
-                            if ((mb[q] >> (2 * pr)) & 3u) val[q][pr] = ld_pol(rowv + 32 * pr, rp);
-                        }
-                        po[q] = 0;
-                        if (VERIFY && mb[q]) {
-                            uint64_t ow[W];
-                            load_mask<W>(p.ovf + (size_t)hv[q] * W, ow);
-                            po[q] = mb[q] & pick2<W>(ow, t2);
-                        }
-                    }
-#pragma unroll
-                    for (int q = 0; q < Q; ++q) {
-                        if (src[q] < 0) continue;
-                        if (hs[q] != cur) {
-                            while (cur < hs[q]) {
-                                flush(cur, first, ws, we, hub_mode, acc, aovf);
-                                ++cur;
-#pragma unroll
-                                for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
-                                aovf = 0;
+                            if (cw[pr] & (3u << sh)) {
+                                const V t = __ldg(rowv + 32 * pr);
+                                acc[2 * pr] += t.x;
+                                acc[2 * pr + 1] += t.y;
                             }
                         }
-                        // rows are zero outside their level: add whole pairs unmasked
-                        // (lanes outside c only collect values the commit discards)
+                    } else {
+                        uint32_t mb = 0;
+#pragma unroll
+                        for (int pr = 0; pr < W; ++pr) mb |= ((cw[pr] >> sh) & 3u) << (2 * pr);
+                        V val[W];
+#pragma unroll
+                        for (int pr = 0; pr < W; ++pr) {
+                            val[pr].x = SigT(0);
+                            val[pr].y = SigT(0);
+                            if ((mb >> (2 * pr)) & 3u) val[pr] = __ldg(rowv + 32 * pr);
+                        }
+                        if (mb) {
+                            uint64_t ow[W];
+                            load_mask<W>(p.ovf + (size_t)sv.y * W, ow);
+                            aovf |= mb & pick2<W>(ow, t2);
+                        }
 #pragma unroll
                         for (int pr = 0; pr < W; ++pr) {
                             SigT o = acc[2 * pr];
-                            acc[2 * pr] = o + val[q][pr].x;
-                            if (VERIFY && acc[2 * pr] < o) aovf |= 1u << (2 * pr);
+                            acc[2 * pr] = o + val[pr].x;
+                            if (acc[2 * pr] < o) aovf |= 1u << (2 * pr);
                             o = acc[2 * pr + 1];
-                            acc[2 * pr + 1] = o + val[q][pr].y;
-                            if (VERIFY && acc[2 * pr + 1] < o) aovf |= 1u << (2 * pr + 1);
+                            acc[2 * pr + 1] = o + val[pr].y;
+                            if (acc[2 * pr + 1] < o) aovf |= 1u << (2 * pr + 1);
                         }
-                        aovf |= po[q];
-                        st_dag += __popc(mb[q]);
-                        st_hits += (lane == 0);
                     }
                 }
                 __syncwarp();  // the step's shared hit records are reused by the next step
@@ -521,6 +543,7 @@ struct LanesKernel {
                 }
             }
         }
+        flush_stats();
         __syncthreads();
     }
 
@@ -582,23 +605,14 @@ struct LanesKernel {
             }
             if (VERIFY && ovf) atomicOr((unsigned long long *)(p.hub_ovf + (size_t)h * W + (l >> 6)), 1ull << (l & 63));
         }
+        flush_stats();
         __syncthreads();
     }
 
     __device__ void epilogue() {
-        unsigned long long a = warp_sum_u64(st_reach), b = warp_sum_u64(st_adj), c = warp_sum_u64(st_dag),
-                           d = warp_sum_u64(st_dsum);
-        if (lane == 0) {
-            if (a) atomicAdd(p.stats + 0, a);
-            if (b) atomicAdd(p.stats + 1, b);
-            if (c) atomicAdd(p.stats + 2, c);
-            if (d) atomicAdd(p.stats + 3, d);
-        }
-        const unsigned long long it = warp_sum_u64(st_items), ht = warp_sum_u64(st_hits);
-        if (lane == 0) {
-            if (it) atomicAdd(p.stats + 4, it);
-            if (ht) atomicAdd(p.stats + 5, ht);
-        }
+        flush_stats();
+        __syncthreads();
+        if (threadIdx.x < 6 && sm.st[threadIdx.x]) atomicAdd(p.stats + threadIdx.x, sm.st[threadIdx.x]);
         int anyw = __any_sync(0xffffffffu, any_new_loc);
         if (lane == 0 && anyw) *p.any_new = 1;
         if (p.lane_ns) {
