@@ -160,7 +160,7 @@ struct LanesParams {
 };
 
 #ifndef BC_R4
-#define BC_R4 2  // item steps in flight per warp at W = 4
+#define BC_R4 1  // item steps in flight per warp at W = 4 (occupancy beats per-warp MLP)
 #endif
 
 template <int W, typename SigT>
@@ -624,11 +624,14 @@ struct LanesKernel {
 };
 
 #ifndef BC_MINB
-#define BC_MINB 2  // min resident CTAs per SM for the level kernels (register cap)
+#define BC_MINB 2  // min resident CTAs per SM for the level kernels at W < 4 (register cap)
+#endif
+#ifndef BC_MINB4
+#define BC_MINB4 4  // ... and at W = 4: 32 resident warps (64 registers, no spills)
 #endif
 
 template <int W, typename SigT>
-__global__ void __launch_bounds__(BC_NT, (W == 4 ? BC_MINB + 1 : BC_MINB)) lanes_level_kernel(LanesParams p) {
+__global__ void __launch_bounds__(BC_NT, (W == 4 ? BC_MINB4 : BC_MINB)) lanes_level_kernel(LanesParams p) {
     extern __shared__ __align__(16) unsigned char smraw[];
     LanesSmem<W, SigT> &sm = *reinterpret_cast<LanesSmem<W, SigT> *>(smraw);
     LanesKernel<W, SigT> k(p, sm);
