@@ -136,7 +136,8 @@ typedef enum {
     BC_OPT_MODE = 4,       /* 0 = auto, 1 = lanes (bit-lane batches), 2 = slices (CTA per source) */
     BC_OPT_RELABEL = 5,    /* 1 (default) = traverse a degree-descending relabelled copy of the graph */
     BC_OPT_SOURCE_ORDER = 6, /* batch schedule: 0 = given order, 1 = degree, 2 (default) = anchor clusters */
-    BC_OPT_FWD_PUSH = 7     /* forward levels L <= value expand in push form (default 0), later ones pull */
+    BC_OPT_FWD_PUSH = 7,    /* forward levels L <= value expand in push form (default 0), later ones pull */
+    BC_OPT_BWD_MODE = 8     /* backward sweep: 0 = default, 1 = push form, 2 = pull form (successor checking) */
 } bc_option;
 
 bc_status bc_set_option(bc_graph *g, int option, int64_t value);

@@ -20,10 +20,12 @@ import numpy as np
 from . import _lib as _L
 
 __all__ = ["Graph", "BCError", "build", "BC_CREATE_VALIDATE", "OPT_LANE_WORDS", "OPT_HUB_DEGREE",
-           "OPT_PROFILE", "OPT_MODE", "OPT_RELABEL", "OPT_SOURCE_ORDER", "OPT_FWD_PUSH"]
+           "OPT_PROFILE", "OPT_MODE", "OPT_RELABEL", "OPT_SOURCE_ORDER", "OPT_FWD_PUSH",
+           "OPT_BWD_MODE"]
 
 BC_CREATE_VALIDATE = 0x1
 OPT_LANE_WORDS, OPT_HUB_DEGREE, OPT_PROFILE, OPT_MODE, OPT_RELABEL, OPT_SOURCE_ORDER, OPT_FWD_PUSH = 1, 2, 3, 4, 5, 6, 7
+OPT_BWD_MODE = 8
 build = _L.build
 
 

@@ -168,6 +168,7 @@ struct bc_graph {
     DevCSR run;        // the CSR the level kernels traverse: cur() relabelled by degree
     bool run_valid = false;
     int relabel = 1;
+    int bwd_mode = 0;         // 0 = default, 1 = push form (bwd_push.cuh), 2 = pull form (lanes.cuh, BWD)
     int fwd_push_levels = 0;  // forward levels L <= this use the push form (measured: pull is as fast at L=1)
     int src_order = 2;  // 0 given, 1 degree, 2 anchor clusters
     bool pruned = false;
@@ -603,7 +604,40 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
         for (int l = 0; l <= Lmax; ++l) c.lvl_out->push_back(level_ptr(g, ws, l));
     }
     if constexpr (std::is_same<SigT, double>::value) {
-        if (c.run_backward) {
+        if (c.run_backward && g->bwd_mode == 2) {
+            // pull-form backward (successor checking, Alg.5): level-L vertices
+            // gather the coef rows of their level-(L+1) children
+            auto kb = lanes_level_kernel<W, SigT, true>;
+            const int gridb = level_grid(g, kb, units, SMEM);
+            auto khb = lanes_hub_finalize<W, SigT, true>;
+            cudaFuncSetAttribute(khb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+            p.dbg_delta = c.dbg_delta;
+            for (int l = Lmax; l >= 1; --l) {
+                p.level = l;
+                p.S_cur = ws.slev[l];
+                p.S_nxt = ws.slev[l + 1];
+                p.mask_cur = level_ptr(g, ws, l);
+                p.mask_nxt_ro = level_ptr(g, ws, l + 1);  // all zero for l == Lmax
+                p.mask_nxt = nullptr;
+                p.any_new = g->d_flags;  // unused
+                cudaEvent_t e0 = nullptr, e1 = nullptr;
+                if (ev_b) {
+                    cudaEventCreate(&e0);
+                    cudaEventCreate(&e1);
+                    cudaEventRecord(e0, st);
+                }
+                kb<<<gridb, BC_NT, SMEM, st>>>(p);
+                if (p.nhub > 0) khb<<<hub_grid, BC_NT, SMEM, st>>>(p);
+                if (ev_b) {
+                    cudaEventRecord(e1, st);
+                    ev_b->push_back(e0);
+                    ev_b->push_back(e1);
+                }
+                CU(cudaGetLastError());
+                g->last.bwd_launches += 1;
+                g->last.kernel_launches += 1 + (p.nhub > 0);
+            }
+        } else if (c.run_backward) {
             // push-form backward (bwd_push.cuh): finalize level L, then push its
             // coef rows into the parents' accumulators
             auto kpush = lanes_push_kernel<W, false>;
@@ -647,11 +681,10 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
                 g->last.bwd_launches += 1;
                 g->last.kernel_launches += 1 + (l >= 2);
             }
-            if (c.endpoint && c.omega) {
-                lanes_endpoint_kernel<<<(c.nl + 255) / 256, 256, 0, st>>>(c.src, c.nl, c.omega, ws.lane_ns,
-                                                                         g->d_bc);
-                g->last.kernel_launches += 1;
-            }
+        }
+        if (c.run_backward && c.endpoint && c.omega) {
+            lanes_endpoint_kernel<<<(c.nl + 255) / 256, 256, 0, st>>>(c.src, c.nl, c.omega, ws.lane_ns, g->d_bc);
+            g->last.kernel_launches += 1;
         }
     }
     CU(cudaGetLastError());
@@ -957,6 +990,10 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
         case BC_OPT_FWD_PUSH:
             if (value < 0 || value > 1000) return fail(BC_ERR_INVALID, "fwd push levels out of range");
             g->fwd_push_levels = (int)value;
+            return BC_OK;
+        case BC_OPT_BWD_MODE:
+            if (value < 0 || value > 2) return fail(BC_ERR_INVALID, "backward mode must be 0, 1 or 2");
+            g->bwd_mode = (int)value;
             return BC_OK;
         case BC_OPT_SOURCE_ORDER:
             if (value < 0 || value > 3) return fail(BC_ERR_INVALID, "source order must be 0..3");

@@ -55,49 +55,63 @@ struct PushSmem {
 // x at level L: finalise coef and BC (warp per vertex, strided lanes; all
 // loads of a vertex are issued before its stores)
 template <int W>
-__global__ void __launch_bounds__(BC_NT) lanes_bwd_finalize_kernel(LanesParams p, double *__restrict__ A) {
+__device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double *__restrict__ A,
+                                                    double *__restrict__ S, int x, int lane) {
     constexpr int K = 64 * W, NG = 2 * W;
+    uint64_t m[W];
+    load_mask<W>(p.mask_cur + (size_t)x * W, m);
+    uint32_t bits = 0;
+#pragma unroll
+    for (int j = 0; j < NG; ++j) bits |= (((uint32_t)(m[j >> 1] >> ((j & 1) * 32)) >> lane) & 1u) << j;
+    double *arow = A + (size_t)x * K + lane;
+    double *row = S + (size_t)x * K + lane;
+    double av[NG], sv[NG];
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+        av[j] = 0.0;
+        sv[j] = 1.0;
+        if (bits >> j & 1u) {
+            av[j] = arow[32 * j];
+            sv[j] = row[32 * j];
+        }
+    }
+    const double om = p.omega ? (double)p.omega[x] : 0.0;
+    double contrib = 0.0;
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+        if (bits >> j & 1u) {
+            const double delta = sv[j] * av[j];
+            arow[32 * j] = 0.0;
+            row[32 * j] = (1.0 + om + delta) / sv[j];
+            contrib += p.lane_w1[32 * j + lane] * (delta + om);
+            if (j == 0 && lane == 0 && p.dbg_delta) p.dbg_delta[x] = delta;
+        }
+    }
+    contrib = warp_sum(contrib);
+    if (lane == 0 && contrib != 0.0) p.bc[x] += contrib;
+}
+
+// 32 vertices per warp step: lane i tests vertex base + i, then the warp
+// finalises the ones at level L (most vertices are not at any given level)
+template <int W>
+__global__ void __launch_bounds__(BC_NT) lanes_bwd_finalize_kernel(LanesParams p, double *__restrict__ A) {
     const int lane = lane_id();
     const int nwarps = (int)((gridDim.x * (size_t)BC_NT) >> 5);
     double *__restrict__ S = reinterpret_cast<double *>(p.S_cur);
-    for (int x = (int)(((size_t)blockIdx.x * BC_NT + threadIdx.x) >> 5); x < p.n; x += nwarps) {
-        uint64_t m[W];
-        bool any = false;
+    for (int base = (int)(((size_t)blockIdx.x * BC_NT + threadIdx.x) >> 5) * 32; base < p.n; base += nwarps * 32) {
+        bool mine = false;
+        if (base + lane < p.n) {
+            uint64_t mm[W];
+            load_mask<W>(p.mask_cur + (size_t)(base + lane) * W, mm);
 #pragma unroll
-        for (int j = 0; j < W; ++j) {
-            m[j] = __ldg(p.mask_cur + (size_t)x * W + j);
-            any |= m[j] != 0;
+            for (int j = 0; j < W; ++j) mine |= mm[j] != 0;
         }
-        if (!any) continue;  // warp-uniform
-        uint32_t bits = 0;
-#pragma unroll
-        for (int j = 0; j < NG; ++j) bits |= (((uint32_t)(m[j >> 1] >> ((j & 1) * 32)) >> lane) & 1u) << j;
-        double *arow = A + (size_t)x * K + lane;
-        double *row = S + (size_t)x * K + lane;
-        double av[NG], sv[NG];
-#pragma unroll
-        for (int j = 0; j < NG; ++j) {
-            av[j] = 0.0;
-            sv[j] = 1.0;
-            if (bits >> j & 1u) {
-                av[j] = arow[32 * j];
-                sv[j] = row[32 * j];
-            }
+        unsigned todo = __ballot_sync(0xffffffffu, mine);
+        while (todo) {
+            const int x = base + __ffs(todo) - 1;
+            todo &= todo - 1;
+            bwd_finalize_vertex<W>(p, A, S, x, lane);
         }
-        const double om = p.omega ? (double)p.omega[x] : 0.0;
-        double contrib = 0.0;
-#pragma unroll
-        for (int j = 0; j < NG; ++j) {
-            if (bits >> j & 1u) {
-                const double delta = sv[j] * av[j];
-                arow[32 * j] = 0.0;
-                row[32 * j] = (1.0 + om + delta) / sv[j];
-                contrib += p.lane_w1[32 * j + lane] * (delta + om);
-                if (j == 0 && lane == 0 && p.dbg_delta) p.dbg_delta[x] = delta;
-            }
-        }
-        contrib = warp_sum(contrib);
-        if (lane == 0 && contrib != 0.0) p.bc[x] += contrib;
     }
 }
 

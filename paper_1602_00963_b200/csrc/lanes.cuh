@@ -222,7 +222,7 @@ __device__ __forceinline__ uint64_t gather_words(uint32_t bits, int lane) {
     return mine;
 }
 
-template <int W, typename SigT>
+template <int W, typename SigT, bool BWD = false>
 struct LanesKernel {
     static constexpr int K = 64 * W;
     static constexpr int LPT = 2 * W;           // lanes per thread
@@ -242,7 +242,7 @@ struct LanesKernel {
 
     __device__ LanesKernel(const LanesParams &pp, Smem &s)
         : p(pp), sm(s), lane(lane_id()), wid(warp_id()), t2(2 * lane_id()) {
-        if (p.lane_ns)
+        if (!BWD && p.lane_ns)
             for (int l = threadIdx.x; l < K; l += BC_NT) sm.ns[l] = 0.0;
         if (threadIdx.x < 6) sm.st[threadIdx.x] = 0;
         __syncthreads();
@@ -321,9 +321,52 @@ struct LanesKernel {
         }
     }
 
+    // ---- backward commit (pull form): x is at level L in the lanes of mb and
+    // acc = sum of coef(v) over its children v (level L+1); then
+    //   delta = sigma * acc, coef = (1 + omega(x) + delta) / sigma      (Eq.5)
+    //   BC[x] += sum_lanes (1 + omega(s)) * (delta + omega(x))          (R13)
+    // and the level-L row of x becomes its coef row (zeros stay zeros).
+    __device__ void commit_bwd(int x, uint32_t mb, const SigT (&acc)[LPT]) {
+        if constexpr (BWD && !VERIFY) {
+            if (!__any_sync(0xffffffffu, mb != 0)) return;  // warp-uniform
+            double *row = Scur() + (size_t)x * K;
+            const double om = p.omega ? (double)p.omega[x] : 0.0;
+            double contrib = 0.0;
+            // pair by pair (few live registers); pairs without level-L lanes
+            // stay zero, the other lane of a half-used pair is zero as well
+#pragma unroll
+            for (int pr = 0; pr < W; ++pr) {
+                const uint32_t b2 = (mb >> (2 * pr)) & 3u;
+                if (b2) {
+                    double2 *cell = reinterpret_cast<double2 *>(row + 64 * pr + t2);
+                    const double2 sg = *cell;
+                    double2 cf = make_double2(0.0, 0.0);
+                    if (b2 & 1u) {
+                        const double delta = sg.x * acc[2 * pr];
+                        cf.x = (1.0 + om + delta) / sg.x;
+                        contrib += p.lane_w1[64 * pr + t2] * (delta + om);
+                        if (pr == 0 && lane == 0 && p.dbg_delta) p.dbg_delta[x] = delta;
+                    }
+                    if (b2 & 2u) {
+                        const double delta = sg.y * acc[2 * pr + 1];
+                        cf.y = (1.0 + om + delta) / sg.y;
+                        contrib += p.lane_w1[64 * pr + t2 + 1] * (delta + om);
+                    }
+                    *cell = cf;
+                }
+            }
+            contrib = warp_sum(contrib);
+            if (lane == 0 && contrib != 0.0) p.bc[x] += contrib;
+        }
+    }
+
     __device__ __forceinline__ void commit_slot(int s, const SigT (&acc)[LPT], uint32_t aovf) {
-        const uint32_t ub = bits_of(sm.u + s * W);
-        commit_fwd(sm.vert[s], sm.cd[s + 1] - sm.cd[s], ub, acc, aovf);
+        if constexpr (BWD) {
+            commit_bwd(sm.vert[s], bits_of(sm.u + s * W), acc);
+        } else {
+            const uint32_t ub = bits_of(sm.u + s * W);
+            commit_fwd(sm.vert[s], sm.cd[s + 1] - sm.cd[s], ub, acc, aovf);
+        }
     }
 
     // flush the running accumulator of slot s (warp-uniform)
@@ -348,7 +391,7 @@ struct LanesKernel {
 
     // One warp walks items [ws, we) of the current tile (slots in sm).
     __device__ void warp_walk(int nslots, int ws, int we, bool hub_mode) {
-        const uint64_t *mread = p.mask_cur;
+        const uint64_t *mread = BWD ? p.mask_nxt_ro : p.mask_cur;  // bwd: children at L+1
         int cur = slot_of(sm.cd, nslots, ws);
         const int first = cur;
         const int last = slot_of(sm.cd, nslots, we - 1);
@@ -389,7 +432,7 @@ struct LanesKernel {
 #pragma unroll
                 for (int j = 0; j < W; ++j) {
                     h |= (cc[k][j] != 0);
-                    st_dag += (unsigned)__popcll(cc[k][j]);
+                    if (!BWD) st_dag += (unsigned)__popcll(cc[k][j]);
                 }
                 unsigned hm = __ballot_sync(0xffffffffu, h);
                 if (hm == 0) continue;
@@ -428,7 +471,7 @@ struct LanesKernel {
                     }
                     // rows are zero outside their level: add whole pairs
                     // (lanes outside c only collect values the commit discards)
-                    const V *rowv = reinterpret_cast<const V *>(Scur() + (size_t)sv.y * K + t2);
+                    const V *rowv = reinterpret_cast<const V *>((BWD ? Snxt() : Scur()) + (size_t)sv.y * K + t2);
                     if constexpr (!VERIFY) {
 #pragma unroll
                         for (int pr = 0; pr < W; ++pr) {
@@ -496,7 +539,7 @@ struct LanesKernel {
             if (deg > 0 && deg <= p.hub_deg) {
 #pragma unroll
                 for (int j = 0; j < W; ++j) {
-                    u[j] = p.active[j] & ~p.seen[(size_t)x * W + j];
+                    u[j] = BWD ? p.mask_cur[(size_t)x * W + j] : p.active[j] & ~p.seen[(size_t)x * W + j];
                     act |= (u[j] != 0);
                 }
             }
@@ -569,7 +612,7 @@ struct LanesKernel {
         bool any = false;
 #pragma unroll
         for (int j = 0; j < W; ++j) {
-            u[j] = p.active[j] & ~p.seen[(size_t)x * W + j];
+            u[j] = BWD ? p.mask_cur[(size_t)x * W + j] : p.active[j] & ~p.seen[(size_t)x * W + j];
             any |= (u[j] != 0);
         }
         if (!any) return;  // uniform
@@ -612,10 +655,13 @@ struct LanesKernel {
     __device__ void epilogue() {
         flush_stats();
         __syncthreads();
-        if (threadIdx.x < 6 && sm.st[threadIdx.x]) atomicAdd(p.stats + threadIdx.x, sm.st[threadIdx.x]);
+        if (threadIdx.x < 6 && sm.st[threadIdx.x]) {
+            const int slot = BWD ? (threadIdx.x >= 4 ? threadIdx.x + 2 : -1) : (int)threadIdx.x;  // bwd: items, hits
+            if (slot >= 0) atomicAdd(p.stats + slot, sm.st[threadIdx.x]);
+        }
         int anyw = __any_sync(0xffffffffu, any_new_loc);
         if (lane == 0 && anyw) *p.any_new = 1;
-        if (p.lane_ns) {
+        if (!BWD && p.lane_ns) {
             __syncthreads();
             for (int l = threadIdx.x; l < K; l += BC_NT)
                 if (sm.ns[l] != 0.0) atomicAdd(p.lane_ns + l, sm.ns[l]);
@@ -630,11 +676,11 @@ struct LanesKernel {
 #define BC_MINB4 4  // ... and at W = 4: 32 resident warps (64 registers, no spills)
 #endif
 
-template <int W, typename SigT>
+template <int W, typename SigT, bool BWD = false>
 __global__ void __launch_bounds__(BC_NT, (W == 4 ? BC_MINB4 : BC_MINB)) lanes_level_kernel(LanesParams p) {
     extern __shared__ __align__(16) unsigned char smraw[];
     LanesSmem<W, SigT> &sm = *reinterpret_cast<LanesSmem<W, SigT> *>(smraw);
-    LanesKernel<W, SigT> k(p, sm);
+    LanesKernel<W, SigT, BWD> k(p, sm);
     const int total = p.nseg + p.ntiles;
     for (;;) {
         if (threadIdx.x == 0) {
@@ -654,9 +700,9 @@ __global__ void __launch_bounds__(BC_NT, (W == 4 ? BC_MINB4 : BC_MINB)) lanes_le
 
 // One warp per hub: commit the hub's summed row.  Resets the scratch row for
 // the next level.
-template <int W, typename SigT>
+template <int W, typename SigT, bool BWD = false>
 __global__ void __launch_bounds__(BC_NT) lanes_hub_finalize(LanesParams p) {
-    using KK = LanesKernel<W, SigT>;
+    using KK = LanesKernel<W, SigT, BWD>;
     constexpr int K = KK::K, LPT = KK::LPT;
     extern __shared__ __align__(16) unsigned char smraw[];
     LanesSmem<W, SigT> &sm = *reinterpret_cast<LanesSmem<W, SigT> *>(smraw);
@@ -671,18 +717,22 @@ __global__ void __launch_bounds__(BC_NT) lanes_hub_finalize(LanesParams p) {
             acc[i] = row[k.lane_of(i)];
             if (acc[i] != SigT(0)) row[k.lane_of(i)] = SigT(0);
         }
-        uint32_t aovf = 0;
-        if (KK::VERIFY) {
-            uint64_t *ow = p.hub_ovf + (size_t)h * W;
-            aovf = k.bits_of(ow);
-            __syncwarp();
-            if (k.lane < W) ow[k.lane] = 0;
-        }
-        uint64_t um[W];
+        if constexpr (BWD) {
+            k.commit_bwd(x, k.bits_of(p.mask_cur + (size_t)x * W), acc);
+        } else {
+            uint32_t aovf = 0;
+            if (KK::VERIFY) {
+                uint64_t *ow = p.hub_ovf + (size_t)h * W;
+                aovf = k.bits_of(ow);
+                __syncwarp();
+                if (k.lane < W) ow[k.lane] = 0;
+            }
+            uint64_t um[W];
 #pragma unroll
-        for (int j = 0; j < W; ++j) um[j] = p.active[j] & ~p.seen[(size_t)x * W + j];
-        const uint32_t ub = pick2<W>(um, k.t2);
-        k.commit_fwd(x, p.rp[x + 1] - p.rp[x], ub, acc, aovf);
+            for (int j = 0; j < W; ++j) um[j] = p.active[j] & ~p.seen[(size_t)x * W + j];
+            const uint32_t ub = pick2<W>(um, k.t2);
+            k.commit_fwd(x, p.rp[x + 1] - p.rp[x], ub, acc, aovf);
+        }
     }
     k.epilogue();
 }

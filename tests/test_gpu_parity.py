@@ -66,6 +66,31 @@ def test_small_suite_all_sources(words, hub, relabel):
             assert_bc_close(G.compute(), oracle.bc(g))
 
 
+@pytest.mark.parametrize("bwd", [1, 2])
+@pytest.mark.parametrize("words", [1, 4])
+def test_backward_forms_push_and_pull(bwd, words):
+    """Both backward forms (push: bwd_push.cuh; pull / successor checking:
+    lanes.cuh BWD) on the small suite with split hubs, unpruned and pruned,
+    and on a multi-batch R-MAT sample."""
+    bcb = _bcb()
+    for g in SUITE:
+        for prune in (False, True):
+            with bcb.Graph.from_csr(g) as G:
+                G.set_option(bcb.OPT_BWD_MODE, bwd)
+                G.set_option(bcb.OPT_LANE_WORDS, words)
+                G.set_option(bcb.OPT_HUB_DEGREE, 32)
+                if prune:
+                    G.prune_degree1()
+                assert_bc_close(G.compute(), oracle.bc(g))
+    g = gg.rmat(13, 16, seed=5)
+    S = gg.sample_sources(g, 600, seed=6)
+    with bcb.Graph.from_csr(g) as G:
+        G.set_option(bcb.OPT_BWD_MODE, bwd)
+        G.set_option(bcb.OPT_LANE_WORDS, words)
+        G.set_option(bcb.OPT_HUB_DEGREE, 64)
+        assert_bc_close(G.compute(S), oracle.bc(g, S))
+
+
 @pytest.mark.parametrize("prune", [False, True])
 def test_small_suite_slices_mode(prune):
     """Batch mode 'slices' (one source per CTA) on the same suite."""

@@ -22,6 +22,7 @@ ap.add_argument("--prune", action="store_true")
 ap.add_argument("--relabel", type=int, default=1)
 ap.add_argument("--order", type=int, default=2)
 ap.add_argument("--fwd-push", type=int, default=0)
+ap.add_argument("--bwd", type=int, default=0)
 ap.add_argument("--sort", default="none", choices=["none", "deg", "degasc"])
 a = ap.parse_args()
 g = gg.grid(a.grid, a.grid) if a.grid else gg.rmat(a.scale, a.ef, seed=1)
@@ -35,6 +36,7 @@ G.set_option(bcb.OPT_LANE_WORDS, a.lane_words)
 G.set_option(bcb.OPT_RELABEL, a.relabel)
 G.set_option(bcb.OPT_SOURCE_ORDER, a.order)
 G.set_option(bcb.OPT_FWD_PUSH, a.fwd_push)
+G.set_option(bcb.OPT_BWD_MODE, a.bwd)
 if a.sort != "none":
     d = g.degrees[S]
     S = S[np.argsort(-d if a.sort == "deg" else d, kind="stable")]
