@@ -638,8 +638,10 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
                 g->last.kernel_launches += 1 + (p.nhub > 0);
             }
         } else if (c.run_backward) {
-            // push-form backward (bwd_push.cuh): finalize level L, then push its
-            // coef rows into the parents' accumulators
+            // push-form backward (bwd_push.cuh): for L >= 2 the push kernel forms
+            // coef of the level-L vertices from sigma and A (fused finalize) and
+            // pushes it into the parents' accumulators; hubs are finalised by a
+            // warp-per-hub kernel after it, level 1 by the finalize scan
             auto kpush = lanes_push_kernel<W, false>;
             cudaFuncSetAttribute(kpush, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
             int occp = 1;
@@ -664,22 +666,29 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
                     cudaEventCreate(&e3);
                     cudaEventRecord(e0, st);
                 }
-                lanes_bwd_finalize_kernel<W><<<fin_blocks, BC_NT, 0, st>>>(p, ws.A);
+                if (l >= 2) kpush<<<gridp, BC_NT, 0, st>>>(p, ws.A);
                 if (ev_b) {
                     cudaEventRecord(e1, st);
                     cudaEventRecord(e2, st);
                 }
-                if (l >= 2) kpush<<<gridp, BC_NT, 0, st>>>(p, ws.A);
+                int nk = (l >= 2);
+                if (l == 1) {
+                    lanes_bwd_finalize_kernel<W, false><<<fin_blocks, BC_NT, 0, st>>>(p, ws.A);
+                    ++nk;
+                } else if (p.nhub > 0) {
+                    lanes_bwd_hub_fin_kernel<W><<<(p.nhub * 32 + BC_NT - 1) / BC_NT, BC_NT, 0, st>>>(p, ws.A);
+                    ++nk;
+                }
                 if (ev_b) {
                     cudaEventRecord(e3, st);
-                    ev_b->push_back(e0);
-                    ev_b->push_back(e1);
-                    g->ev_push.push_back(e2);
-                    g->ev_push.push_back(e3);
+                    g->ev_push.push_back(e0);
+                    g->ev_push.push_back(e1);
+                    ev_b->push_back(e2);
+                    ev_b->push_back(e3);
                 }
                 CU(cudaGetLastError());
                 g->last.bwd_launches += 1;
-                g->last.kernel_launches += 1 + (l >= 2);
+                g->last.kernel_launches += nk;
             }
         }
         if (c.run_backward && c.endpoint && c.omega) {

@@ -36,6 +36,20 @@ __device__ __forceinline__ void red_add_f64(double *p, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
+// 1/x for x >= 1 (sigma): hardware approximation + two Newton steps, within
+// ~1 ulp, no division subroutine (which costs registers in the push loop)
+__device__ __forceinline__ double rcp_f64(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+
+#ifndef BC_PR4
+#define BC_PR4 1  // item steps in flight per warp at W = 4 (keeps 64 registers: occupancy wins)
+#endif
 #ifndef BC_PUSH_MINB
 #define BC_PUSH_MINB 4  // push kernels need fewer registers: 4 CTAs (32 warps) per SM
 #endif
@@ -54,7 +68,9 @@ struct PushSmem {
 
 // x at level L: finalise coef and BC (warp per vertex, strided lanes; all
 // loads of a vertex are issued before its stores)
-template <int W>
+// COEF = false: only BC and the re-zeroing of A (the fused push computes the
+// coef values itself and never reads the coef row)
+template <int W, bool COEF>
 __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double *__restrict__ A,
                                                     double *__restrict__ S, int x, int lane) {
     constexpr int K = 64 * W, NG = 2 * W;
@@ -82,7 +98,7 @@ __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double
         if (bits >> j & 1u) {
             const double delta = sv[j] * av[j];
             arow[32 * j] = 0.0;
-            row[32 * j] = (1.0 + om + delta) / sv[j];
+            if (COEF) row[32 * j] = (1.0 + om + delta) / sv[j];
             contrib += p.lane_w1[32 * j + lane] * (delta + om);
             if (j == 0 && lane == 0 && p.dbg_delta) p.dbg_delta[x] = delta;
         }
@@ -93,7 +109,7 @@ __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double
 
 // 32 vertices per warp step: lane i tests vertex base + i, then the warp
 // finalises the ones at level L (most vertices are not at any given level)
-template <int W>
+template <int W, bool COEF>
 __global__ void __launch_bounds__(BC_NT) lanes_bwd_finalize_kernel(LanesParams p, double *__restrict__ A) {
     const int lane = lane_id();
     const int nwarps = (int)((gridDim.x * (size_t)BC_NT) >> 5);
@@ -110,9 +126,24 @@ __global__ void __launch_bounds__(BC_NT) lanes_bwd_finalize_kernel(LanesParams p
         while (todo) {
             const int x = base + __ffs(todo) - 1;
             todo &= todo - 1;
-            bwd_finalize_vertex<W>(p, A, S, x, lane);
+            bwd_finalize_vertex<W, COEF>(p, A, S, x, lane);
         }
     }
+}
+
+// Hubs at level L after the fused push: BC and the re-zeroing of A (their
+// adjacency segments ran on several CTAs; warp per hub)
+template <int W>
+__global__ void __launch_bounds__(BC_NT) lanes_bwd_hub_fin_kernel(LanesParams p, double *__restrict__ A) {
+    const int h = (int)(((size_t)blockIdx.x * BC_NT + threadIdx.x) >> 5);
+    if (h >= p.nhub) return;
+    const int x = p.hub_ids[h];
+    uint64_t m[W];
+    load_mask<W>(p.mask_cur + (size_t)x * W, m);
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < W; ++j) any |= m[j] != 0;
+    if (any) bwd_finalize_vertex<W, false>(p, A, reinterpret_cast<double *>(p.S_cur), x, lane_id());
 }
 
 // FWD = true: forward push for a small frontier (level L -> L+1): every
@@ -123,7 +154,7 @@ __global__ void __launch_bounds__(BC_NT) lanes_bwd_finalize_kernel(LanesParams p
 template <int W, bool FWD>
 struct PushKernel {
     static constexpr int K = 64 * W, NG = 2 * W;
-    static constexpr int R = (W == 4) ? 2 : 4;
+    static constexpr int R = (W == 4) ? BC_PR4 : 4;  // item steps in flight per warp
     const LanesParams &p;
     double *A;
     PushSmem<W> &sm;
@@ -134,7 +165,56 @@ struct PushKernel {
         : p(pp), A(a), sm(s), lane(lane_id()), wid(warp_id()) {}
 
     // one warp: items [ws, we) of the slots in sm; u[slot] = lvl[L][x]
-    __device__ void warp_push(int nslots, int ws, int we) {
+    // backward, fused finalize: coef of slot hs (vertex x at level L) from
+    // sigma_L(x) and the accumulator A[x] (complete: all children pushed at
+    // L+1), coef = (1 + omega + delta) / sigma, delta = sigma * A   (Eq.5).
+    // A slot owned by this warp alone is finalised here (BC, A := 0); split
+    // slots after the tile, hubs by lanes_bwd_hub_fin_kernel.
+    __device__ __forceinline__ void slot_coef(int hs, bool owned, double (&cf)[NG]) {
+        const int x = sm.vert[hs];
+        uint32_t bits = 0;
+#pragma unroll
+        for (int j = 0; j < NG; ++j)
+            bits |= (((uint32_t)(sm.u[hs * W + (j >> 1)] >> ((j & 1) * 32)) >> lane) & 1u) << j;
+        const double *row = reinterpret_cast<const double *>(p.S_cur) + (size_t)x * K + lane;
+        double *arow = A + (size_t)x * K + lane;
+        const double om = p.omega ? (double)p.omega[x] : 0.0;
+        double contrib = 0.0;
+        // two halves of the groups (bounded live registers: cf stays live in the hit loop)
+#pragma unroll
+        for (int h = 0; h < NG; h += NG / 2) {
+            double sv[NG / 2], av[NG / 2];
+#pragma unroll
+            for (int q = 0; q < NG / 2; ++q) {
+                sv[q] = 1.0;
+                av[q] = 0.0;
+                if (bits >> (h + q) & 1u) {
+                    sv[q] = row[32 * (h + q)];
+                    av[q] = arow[32 * (h + q)];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < NG / 2; ++q) {
+                const int j = h + q;
+                cf[j] = 0.0;
+                if (bits >> j & 1u) {
+                    const double delta = sv[q] * av[q];
+                    cf[j] = (1.0 + om + delta) * rcp_f64(sv[q]);
+                    if (owned) {
+                        arow[32 * j] = 0.0;
+                        contrib += p.lane_w1[32 * j + lane] * (delta + om);
+                        if (j == 0 && lane == 0 && p.dbg_delta) p.dbg_delta[x] = delta;
+                    }
+                }
+            }
+        }
+        if (owned) {  // warp-uniform
+            contrib = warp_sum(contrib);
+            if (lane == 0 && contrib != 0.0) p.bc[x] += contrib;
+        }
+    }
+
+    __device__ void warp_push(int nslots, int ws, int we, bool hub_mode) {
         const uint64_t *mpar = FWD ? p.seen : p.mask_nxt_ro;  // fwd: seen[y]; bwd: lvl[L-1] (parents)
         const double *S = reinterpret_cast<const double *>(p.S_cur);
         const uint64_t pol = policy_evict_first();
@@ -190,11 +270,15 @@ struct PushKernel {
                     const int4 rec = hsv[src];
                     const int hs = rec.x, y = rec.y;
                     const uint32_t gm = (uint32_t)rec.z;
-                    if (hs != cur) {  // warp-uniform: coef row of the new slot
+                    if (hs != cur) {  // warp-uniform: coef of the new slot
                         cur = hs;
-                        const double *row = S + (size_t)sm.vert[hs] * K + lane;
+                        if constexpr (FWD) {
+                            const double *row = S + (size_t)sm.vert[hs] * K + lane;
 #pragma unroll
-                        for (int j = 0; j < NG; ++j) cf[j] = row[32 * j];
+                            for (int j = 0; j < NG; ++j) cf[j] = row[32 * j];
+                        } else {
+                            slot_coef(hs, !hub_mode && sm.cd[hs] >= ws && sm.cd[hs + 1] <= we, cf);
+                        }
                     }
                     double *arow = A + (size_t)y * K + lane;
                     uint64_t myword = 0;  // fwd: thread j < W ORs word j of c into lvl[L+1][y]
@@ -263,7 +347,19 @@ struct PushKernel {
         __syncthreads();
         if (nslots > 0) {
             const int ws = bnd(wid, nitems), we = bnd(wid + 1, nitems);
-            if (ws < we) warp_push(nslots, ws, we);
+            if (ws < we) warp_push(nslots, ws, we, false);
+            if (!FWD) {
+                __syncthreads();
+                // slots split across warps: warp j finalises the slot holding boundary j
+                if (wid >= 1) {
+                    const int b = bnd(wid, nitems);
+                    if (b > 0 && b < nitems) {
+                        const int s = slot_of(sm.cd, nslots, b);
+                        if (sm.cd[s] < b && (wid == 1 || bnd(wid - 1, nitems) <= sm.cd[s]))
+                            bwd_finalize_vertex<W, false>(p, A, reinterpret_cast<double *>(p.S_cur), sm.vert[s], lane);
+                    }
+                }
+            }
         }
         __syncthreads();
     }
@@ -304,7 +400,7 @@ struct PushKernel {
             __syncthreads();
             const int nitems = b - a;
             const int ws = bnd(wid, nitems), we = bnd(wid + 1, nitems);
-            if (ws < we) warp_push(1, ws, we);
+            if (ws < we) warp_push(1, ws, we, true);
         }
         __syncthreads();
     }
