@@ -137,7 +137,10 @@ typedef enum {
     BC_OPT_RELABEL = 5,    /* 1 (default) = traverse a degree-descending relabelled copy of the graph */
     BC_OPT_SOURCE_ORDER = 6, /* batch schedule: 0 = given order, 1 = degree, 2 (default) = anchor clusters */
     BC_OPT_FWD_PUSH = 7,    /* forward levels L <= value expand in push form (default 0), later ones pull */
-    BC_OPT_BWD_MODE = 8     /* backward sweep: 0 = default, 1 = push form, 2 = pull form (successor checking) */
+    BC_OPT_BWD_MODE = 8,    /* backward sweep: 0 = default, 1 = push form, 2 = pull form (successor checking) */
+    BC_OPT_SIGMA_WIDTH = 9  /* lanes forward sigma rows: 0 or 16 (default) = uint16 rows, a batch whose
+                               sigma exceeds 65535 is re-run with fp64 rows; 64 = fp64 rows only.
+                               sigma is an integer (Alg.1 line 20), so both are exact */
 } bc_option;
 
 bc_status bc_set_option(bc_graph *g, int option, int64_t value);
@@ -165,6 +168,8 @@ typedef struct {
     int64_t bwd_hits;        /* items with >= 1 contributing lane, backward     */
     double bwd_fin_ms;       /* backward finalize kernels (BC_OPT_PROFILE)       */
     double bwd_push_ms;      /* backward push kernels (BC_OPT_PROFILE)           */
+    int64_t narrow_batches;  /* batches completed with 16-bit sigma rows          */
+    int64_t narrow_fallbacks;/* batches re-run with fp64 rows after a sigma > 65535 */
 } bc_stats;
 
 bc_status bc_get_stats(const bc_graph *g, bc_stats *out);

@@ -169,6 +169,7 @@ struct bc_graph {
     bool run_valid = false;
     int relabel = 1;
     int bwd_mode = 0;         // 0 = default, 1 = push form (bwd_push.cuh), 2 = pull form (lanes.cuh, BWD)
+    int sigma_width = 0;      // BC_OPT_SIGMA_WIDTH: 0 = 16-bit sigma rows first (fp64 re-run on overflow), 64 = fp64 only
     int fwd_push_levels = 0;  // forward levels L <= this use the push form (measured: pull is as fast at L=1)
     int src_order = 2;  // 0 given, 1 degree, 2 anchor clusters
     bool pruned = false;
@@ -185,7 +186,7 @@ struct bc_graph {
     LaneWS ws, vws;  // compute workspace, verification workspace (W = 1)
     SlicesWS sws;    // slices-mode workspace
     unsigned long long *d_stats = nullptr;  // [4]
-    int *d_work_ctr = nullptr;              // [4]
+    int *d_work_ctr = nullptr;              // [4]: level work counter, slices source counter, narrow overflow flag
     int *d_flags = nullptr;                 // [flag_cap]
     int flag_cap = 0;
     int *h_flag = nullptr;                  // pinned
@@ -482,6 +483,7 @@ struct BatchCtx {
     bool endpoint;
     std::vector<uint64_t *> *lvl_out;  // verification: level masks used (nullable)
     int *levels_out;
+    bool *narrow_failed;    // narrow forward: set when some sigma > 65535 (nothing committed)
 };
 
 // Run one batch (forward + backward) with K = 64*W lanes.
@@ -517,6 +519,10 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
     p.ntiles = c.csr->ntiles;
     p.tile_vs = c.csr->tile_vs;
     p.dbg_delta = nullptr;
+    p.narrow_ovf = g->d_work_ctr + 2;  // fixed address (d_flags may grow and move with the level count)
+    using RT = typename RowOf<SigT>::t;
+    constexpr bool NARROW = std::is_same<SigT, unsigned>::value;
+    if (NARROW) CU(cudaMemsetAsync(p.narrow_ovf, 0, sizeof(int), st));
 
     const size_t mbytes = (size_t)n * W * sizeof(uint64_t);
     CK(ensure_level(g, ws, 1));
@@ -529,8 +535,8 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
     lanes_init_kernel<W, SigT><<<c.nl, BC_NT, 0, st>>>(p, c.src, level_ptr(g, ws, 0), level_ptr(g, ws, 1));
     {
         const unsigned mb = (unsigned)(((int64_t)n * 32 + 255) / 256);
-        lanes_materialize_kernel<W, SigT><<<mb, 256, 0, st>>>(n, level_ptr(g, ws, 0), (SigT *)ws.slev[0]);
-        lanes_materialize_kernel<W, SigT><<<mb, 256, 0, st>>>(n, level_ptr(g, ws, 1), (SigT *)ws.slev[1]);
+        lanes_materialize_kernel<W, RT><<<mb, 256, 0, st>>>(n, level_ptr(g, ws, 0), (RT *)ws.slev[0]);
+        lanes_materialize_kernel<W, RT><<<mb, 256, 0, st>>>(n, level_ptr(g, ws, 1), (RT *)ws.slev[1]);
     }
     CU(cudaGetLastError());
     g->last.kernel_launches += 4;
@@ -592,7 +598,9 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
         g->last.fwd_launches += 1;
         g->last.kernel_launches += 1 + (p.nhub > 0);
         CU(cudaMemcpyAsync(g->h_flag, g->d_flags + L + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+        if (NARROW) CU(cudaMemcpyAsync(g->h_flag + 1, p.narrow_ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
+        if (NARROW && g->h_flag[1]) break;  // sigma overflowed 16 bits: stop, the batch is re-run in fp64
         if (*g->h_flag == 0) break;
         ++L;
     }
@@ -603,8 +611,19 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
         c.lvl_out->clear();
         for (int l = 0; l <= Lmax; ++l) c.lvl_out->push_back(level_ptr(g, ws, l));
     }
-    if constexpr (std::is_same<SigT, double>::value) {
+    if constexpr (NARROW) {
+        // some sigma exceeded 16 bits: nothing has been committed to BC yet,
+        // the caller re-runs this batch with fp64 rows
+        if (g->h_flag[1]) {
+            if (c.narrow_failed) *c.narrow_failed = true;
+            return BC_OK;
+        }
+    }
+    if constexpr (!std::is_same<SigT, unsigned long long>::value) {
+        bool pulled = false;
+        if constexpr (std::is_same<SigT, double>::value) {
         if (c.run_backward && g->bwd_mode == 2) {
+            pulled = true;
             // pull-form backward (successor checking, Alg.5): level-L vertices
             // gather the coef rows of their level-(L+1) children
             auto kb = lanes_level_kernel<W, SigT, true>;
@@ -637,12 +656,14 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
                 g->last.bwd_launches += 1;
                 g->last.kernel_launches += 1 + (p.nhub > 0);
             }
-        } else if (c.run_backward) {
+        }
+        }
+        if (c.run_backward && !pulled) {
             // push-form backward (bwd_push.cuh): for L >= 2 the push kernel forms
             // coef of the level-L vertices from sigma and A (fused finalize) and
             // pushes it into the parents' accumulators; hubs are finalised by a
             // warp-per-hub kernel after it, level 1 by the finalize scan
-            auto kpush = lanes_push_kernel<W, false>;
+            auto kpush = lanes_push_kernel<W, false, RT>;
             cudaFuncSetAttribute(kpush, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
             int occp = 1;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occp, kpush, BC_NT, 0);
@@ -673,10 +694,10 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
                 }
                 int nk = (l >= 2);
                 if (l == 1) {
-                    lanes_bwd_finalize_kernel<W, false><<<fin_blocks, BC_NT, 0, st>>>(p, ws.A);
+                    lanes_bwd_finalize_kernel<W, false, RT><<<fin_blocks, BC_NT, 0, st>>>(p, ws.A);
                     ++nk;
                 } else if (p.nhub > 0) {
-                    lanes_bwd_hub_fin_kernel<W><<<(p.nhub * 32 + BC_NT - 1) / BC_NT, BC_NT, 0, st>>>(p, ws.A);
+                    lanes_bwd_hub_fin_kernel<W, RT><<<(p.nhub * 32 + BC_NT - 1) / BC_NT, BC_NT, 0, st>>>(p, ws.A);
                     ++nk;
                 }
                 if (ev_b) {
@@ -864,11 +885,11 @@ static bc_status create_impl(bc_graph *g, int64_t n, const int64_t *row_ptr, con
     CU(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
     cudaStream_t st = g->own_stream;
     CU(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device));
-    CK(dalloc(&g->d_stats, 8));
+    CK(dalloc(&g->d_stats, 16));  // [0, 8) counters, [8, 16) backup across a narrow re-run
     CK(dalloc(&g->d_work_ctr, 4));
     CU(cudaMemset(g->d_work_ctr, 0, 4 * sizeof(int)));
     CK(ensure_flags(g, 64));
-    CU(cudaMallocHost((void **)&g->h_flag, sizeof(int)));
+    CU(cudaMallocHost((void **)&g->h_flag, 2 * sizeof(int)));
     CK(dalloc(&g->d_bc, (size_t)n));
     // CSR: int64 row_ptr -> int32 on device
     long long *rp64 = nullptr;
@@ -1003,6 +1024,10 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
         case BC_OPT_BWD_MODE:
             if (value < 0 || value > 2) return fail(BC_ERR_INVALID, "backward mode must be 0, 1 or 2");
             g->bwd_mode = (int)value;
+            return BC_OK;
+        case BC_OPT_SIGMA_WIDTH:
+            if (value != 0 && value != 16 && value != 64) return fail(BC_ERR_INVALID, "sigma width must be 0, 16 or 64");
+            g->sigma_width = (int)value;
             return BC_OK;
         case BC_OPT_SOURCE_ORDER:
             if (value < 0 || value > 3) return fail(BC_ERR_INVALID, "source order must be 0..3");
@@ -1150,8 +1175,27 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
         c.st = st;
         c.run_backward = true;
         c.endpoint = true;
-        CK(run_batch_w<double>(g, g->ws, W, c, g->profile ? &ef : nullptr, g->profile ? &eb : nullptr));
         g->last.batches += 1;
+        // narrow sigma first (16-bit rows, exact integers); a batch whose sigma
+        // overflows is re-run with fp64 rows from scratch (nothing of it was
+        // committed: BC is only touched by the backward sweep)
+        const bool narrow = g->sigma_width != 64 && g->hub_deg <= 65536 && g->bwd_mode != 2 && g->fwd_push_levels == 0;
+        if (narrow) {
+            bool failed = false;
+            c.narrow_failed = &failed;
+            const int64_t lv = g->last.levels_total;
+            CU(cudaMemcpyAsync(g->d_stats + 8, g->d_stats, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+            CK(run_batch_w<unsigned>(g, g->ws, W, c, g->profile ? &ef : nullptr, g->profile ? &eb : nullptr));
+            if (!failed) {
+                g->last.narrow_batches += 1;
+                continue;
+            }
+            CU(cudaMemcpyAsync(g->d_stats, g->d_stats + 8, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+            g->last.levels_total = lv;
+            g->last.narrow_fallbacks += 1;
+            c.narrow_failed = nullptr;
+        }
+        CK(run_batch_w<double>(g, g->ws, W, c, g->profile ? &ef : nullptr, g->profile ? &eb : nullptr));
     }
     if (!triv.empty()) {
         trivial_sources_kernel<<<(unsigned)((triv.size() + 255) / 256), 256, 0, st>>>(

@@ -70,9 +70,11 @@ struct PushSmem {
 // loads of a vertex are issued before its stores)
 // COEF = false: only BC and the re-zeroing of A (the fused push computes the
 // coef values itself and never reads the coef row)
-template <int W, bool COEF>
+// RT = storage type of the sigma rows (double, or uint16_t after a narrow forward)
+template <int W, bool COEF, typename RT = double>
 __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double *__restrict__ A,
-                                                    double *__restrict__ S, int x, int lane) {
+                                                    RT *__restrict__ S, int x, int lane) {
+    static_assert(!COEF || std::is_same<RT, double>::value, "coef rows are fp64");
     constexpr int K = 64 * W, NG = 2 * W;
     uint64_t m[W];
     load_mask<W>(p.mask_cur + (size_t)x * W, m);
@@ -80,7 +82,7 @@ __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double
 #pragma unroll
     for (int j = 0; j < NG; ++j) bits |= (((uint32_t)(m[j >> 1] >> ((j & 1) * 32)) >> lane) & 1u) << j;
     double *arow = A + (size_t)x * K + lane;
-    double *row = S + (size_t)x * K + lane;
+    RT *row = S + (size_t)x * K + lane;
     double av[NG], sv[NG];
 #pragma unroll
     for (int j = 0; j < NG; ++j) {
@@ -88,7 +90,7 @@ __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double
         sv[j] = 1.0;
         if (bits >> j & 1u) {
             av[j] = arow[32 * j];
-            sv[j] = row[32 * j];
+            sv[j] = (double)row[32 * j];
         }
     }
     const double om = p.omega ? (double)p.omega[x] : 0.0;
@@ -98,7 +100,7 @@ __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double
         if (bits >> j & 1u) {
             const double delta = sv[j] * av[j];
             arow[32 * j] = 0.0;
-            if (COEF) row[32 * j] = (1.0 + om + delta) / sv[j];
+            if constexpr (COEF) row[32 * j] = (1.0 + om + delta) / sv[j];
             contrib += p.lane_w1[32 * j + lane] * (delta + om);
             if (j == 0 && lane == 0 && p.dbg_delta) p.dbg_delta[x] = delta;
         }
@@ -109,11 +111,11 @@ __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double
 
 // 32 vertices per warp step: lane i tests vertex base + i, then the warp
 // finalises the ones at level L (most vertices are not at any given level)
-template <int W, bool COEF>
+template <int W, bool COEF, typename RT = double>
 __global__ void __launch_bounds__(BC_NT) lanes_bwd_finalize_kernel(LanesParams p, double *__restrict__ A) {
     const int lane = lane_id();
     const int nwarps = (int)((gridDim.x * (size_t)BC_NT) >> 5);
-    double *__restrict__ S = reinterpret_cast<double *>(p.S_cur);
+    RT *__restrict__ S = reinterpret_cast<RT *>(p.S_cur);
     for (int base = (int)(((size_t)blockIdx.x * BC_NT + threadIdx.x) >> 5) * 32; base < p.n; base += nwarps * 32) {
         bool mine = false;
         if (base + lane < p.n) {
@@ -126,14 +128,14 @@ __global__ void __launch_bounds__(BC_NT) lanes_bwd_finalize_kernel(LanesParams p
         while (todo) {
             const int x = base + __ffs(todo) - 1;
             todo &= todo - 1;
-            bwd_finalize_vertex<W, COEF>(p, A, S, x, lane);
+            bwd_finalize_vertex<W, COEF, RT>(p, A, S, x, lane);
         }
     }
 }
 
 // Hubs at level L after the fused push: BC and the re-zeroing of A (their
 // adjacency segments ran on several CTAs; warp per hub)
-template <int W>
+template <int W, typename RT = double>
 __global__ void __launch_bounds__(BC_NT) lanes_bwd_hub_fin_kernel(LanesParams p, double *__restrict__ A) {
     const int h = (int)(((size_t)blockIdx.x * BC_NT + threadIdx.x) >> 5);
     if (h >= p.nhub) return;
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__(BC_NT) lanes_bwd_hub_fin_kernel(LanesParams p,
     bool any = false;
 #pragma unroll
     for (int j = 0; j < W; ++j) any |= m[j] != 0;
-    if (any) bwd_finalize_vertex<W, false>(p, A, reinterpret_cast<double *>(p.S_cur), x, lane_id());
+    if (any) bwd_finalize_vertex<W, false, RT>(p, A, reinterpret_cast<RT *>(p.S_cur), x, lane_id());
 }
 
 // FWD = true: forward push for a small frontier (level L -> L+1): every
@@ -151,8 +153,9 @@ __global__ void __launch_bounds__(BC_NT) lanes_bwd_hub_fin_kernel(LanesParams p,
 // lanes c = lvl[L][x] & active & ~seen[y] and ORs c into lvl[L+1][y];
 // lanes_fwd_commit_kernel then turns A into the level-(L+1) sigma rows.
 // FWD = false: the backward push described above.
-template <int W, bool FWD>
+template <int W, bool FWD, typename RT = double>
 struct PushKernel {
+    static_assert(!FWD || std::is_same<RT, double>::value, "forward push uses fp64 rows");
     static constexpr int K = 64 * W, NG = 2 * W;
     static constexpr int R = (W == 4) ? BC_PR4 : 4;  // item steps in flight per warp
     const LanesParams &p;
@@ -176,7 +179,7 @@ struct PushKernel {
 #pragma unroll
         for (int j = 0; j < NG; ++j)
             bits |= (((uint32_t)(sm.u[hs * W + (j >> 1)] >> ((j & 1) * 32)) >> lane) & 1u) << j;
-        const double *row = reinterpret_cast<const double *>(p.S_cur) + (size_t)x * K + lane;
+        const RT *row = reinterpret_cast<const RT *>(p.S_cur) + (size_t)x * K + lane;
         double *arow = A + (size_t)x * K + lane;
         const double om = p.omega ? (double)p.omega[x] : 0.0;
         double contrib = 0.0;
@@ -189,7 +192,7 @@ struct PushKernel {
                 sv[q] = 1.0;
                 av[q] = 0.0;
                 if (bits >> (h + q) & 1u) {
-                    sv[q] = row[32 * (h + q)];
+                    sv[q] = (double)row[32 * (h + q)];
                     av[q] = arow[32 * (h + q)];
                 }
             }
@@ -356,7 +359,7 @@ struct PushKernel {
                     if (b > 0 && b < nitems) {
                         const int s = slot_of(sm.cd, nslots, b);
                         if (sm.cd[s] < b && (wid == 1 || bnd(wid - 1, nitems) <= sm.cd[s]))
-                            bwd_finalize_vertex<W, false>(p, A, reinterpret_cast<double *>(p.S_cur), sm.vert[s], lane);
+                            bwd_finalize_vertex<W, false, RT>(p, A, reinterpret_cast<RT *>(p.S_cur), sm.vert[s], lane);
                     }
                 }
             }
@@ -416,10 +419,10 @@ struct PushKernel {
     }
 };
 
-template <int W, bool FWD>
+template <int W, bool FWD, typename RT = double>
 __global__ void __launch_bounds__(BC_NT, BC_PUSH_MINB) lanes_push_kernel(LanesParams p, double *A) {
     __shared__ PushSmem<W> sm;
-    PushKernel<W, FWD> k(p, A, sm);
+    PushKernel<W, FWD, RT> k(p, A, sm);
     const int total = p.nseg + p.ntiles;
     for (;;) {
         if (threadIdx.x == 0) {

@@ -48,6 +48,18 @@ constexpr int TV = BC_NT;  // vertices per tile
 template <typename T> struct Vec2;
 template <> struct Vec2<double> { using t = double2; };
 template <> struct Vec2<unsigned long long> { using t = ulonglong2; };
+template <> struct Vec2<unsigned> { using t = uint2; };
+
+// Storage type of the level sigma rows for an accumulator type SigT.
+// SigT = unsigned is the *narrow* forward: sigma rows hold uint16 (4x fewer
+// row bytes gathered and written than fp64); sums are formed in 32-bit
+// registers and any sigma > 65535 raises LanesParams::narrow_ovf, after which
+// the host re-runs the batch with fp64 rows.  Integer sigma is exact, so
+// the narrow and fp64 forwards produce identical sigma wherever both fit
+// (R-MAT: max sigma ~1e4 at scale 20, SURVEY.md section 8 constants table).
+template <typename SigT> struct RowOf { using t = SigT; };
+template <> struct RowOf<unsigned> { using t = uint16_t; };
+constexpr unsigned NARROW_MAX = 65535u;
 
 // 16-byte read-only load with an L2 cache policy
 __device__ __forceinline__ double2 ld_pol(const double2 *p, uint64_t pol) {
@@ -156,6 +168,7 @@ struct LanesParams {
     int ntiles;
     const int *tile_vs;          // [ntiles+1] tile t = vertices [tile_vs[t], tile_vs[t+1]), <= TV of them
     double *dbg_delta;           // backward: delta of lane 0 (verification), nullable
+    int *narrow_ovf;             // narrow forward: set when some sigma > 65535 (batch is re-run in fp64)
     void *part;                  // [gridDim][BC_NW][2][K] SigT: partial sums of slots split across warps
 };
 
@@ -228,6 +241,8 @@ struct LanesKernel {
     static constexpr int LPT = 2 * W;           // lanes per thread
     static constexpr int R = (W == 1) ? 4 : (W == 2 ? 2 : BC_R4);  // item steps in flight per warp
     static constexpr bool VERIFY = std::is_same<SigT, unsigned long long>::value;
+    static constexpr bool NARROW = std::is_same<SigT, unsigned>::value;
+    using RT = typename RowOf<SigT>::t;  // sigma row storage
     using V = typename Vec2<SigT>::t;
     using Smem = LanesSmem<W, SigT>;
 
@@ -260,11 +275,11 @@ struct LanesKernel {
     // lane index of this thread's i-th accumulator
     __device__ __forceinline__ int lane_of(int i) const { return 64 * (i >> 1) + t2 + (i & 1); }
 
-    __device__ __forceinline__ SigT *Scur() const { return reinterpret_cast<SigT *>(p.S_cur); }
+    __device__ __forceinline__ RT *Scur() const { return reinterpret_cast<RT *>(p.S_cur); }
     __device__ __forceinline__ SigT *part_row(int w, int idx) const {
         return reinterpret_cast<SigT *>(p.part) + ((size_t)(blockIdx.x * BC_NW + w) * 2 + idx) * K;
     }
-    __device__ __forceinline__ SigT *Snxt() const { return reinterpret_cast<SigT *>(p.S_nxt); }
+    __device__ __forceinline__ RT *Snxt() const { return reinterpret_cast<RT *>(p.S_nxt); }
 
     // this thread's bits of the W words at w (shared or global, generic load)
     __device__ __forceinline__ uint32_t bits_of(const uint64_t *w) const {
@@ -275,7 +290,17 @@ struct LanesKernel {
     }
 
     // write this thread's lanes of a row: v[i] where bit i of keep, else 0
-    __device__ __forceinline__ void store_slice(SigT *row, uint32_t keep, const SigT (&v)[LPT]) {
+    __device__ __forceinline__ void store_slice(RT *row, uint32_t keep, const SigT (&v)[LPT]) {
+        if constexpr (NARROW) {
+            // lanes 2t, 2t+1 of a pair are the low / high half of one 32-bit word
+#pragma unroll
+            for (int pr = 0; pr < W; ++pr) {
+                const uint32_t lo = (keep >> (2 * pr) & 1u) ? (v[2 * pr] & 0xffffu) : 0u;
+                const uint32_t hi = (keep >> (2 * pr + 1) & 1u) ? (v[2 * pr + 1] & 0xffffu) : 0u;
+                *reinterpret_cast<uint32_t *>(row + 64 * pr + t2) = lo | (hi << 16);
+            }
+            return;
+        }
 #pragma unroll
         for (int pr = 0; pr < W; ++pr) {
             V t;
@@ -296,6 +321,12 @@ struct LanesKernel {
         aovf &= ub;
         const bool any = __any_sync(0xffffffffu, nb != 0);
         if (!any) return;  // warp-uniform
+        if constexpr (NARROW) {
+            bool big = false;
+#pragma unroll
+            for (int i = 0; i < LPT; ++i) big |= (nb >> i & 1u) && acc[i] > NARROW_MAX;
+            if (big) *p.narrow_ovf = 1;
+        }
         store_slice(Snxt() + (size_t)x * K, nb, acc);
         if (nb) {
             any_new_loc = 1;
@@ -471,6 +502,19 @@ struct LanesKernel {
                     }
                     // rows are zero outside their level: add whole pairs
                     // (lanes outside c only collect values the commit discards)
+                    if constexpr (NARROW) {
+                        // 16-bit rows: one 32-bit load per pair (lanes 2t, 2t+1)
+                        const uint32_t *roww = reinterpret_cast<const uint32_t *>(Scur() + (size_t)sv.y * K) + lane;
+#pragma unroll
+                        for (int pr = 0; pr < W; ++pr) {
+                            if (cw[pr] & (3u << sh)) {
+                                const uint32_t t = __ldg(roww + 32 * pr);
+                                acc[2 * pr] += t & 0xffffu;
+                                acc[2 * pr + 1] += t >> 16;
+                            }
+                        }
+                        continue;
+                    }
                     const V *rowv = reinterpret_cast<const V *>((BWD ? Snxt() : Scur()) + (size_t)sv.y * K + t2);
                     if constexpr (!VERIFY) {
 #pragma unroll
@@ -641,6 +685,9 @@ struct LanesKernel {
                 if (VERIFY && sum < o) ovf = true;
                 if (VERIFY && (sm.povf[(w * 2) * 32 + tl] >> ti & 1u)) ovf = true;
             }
+            // narrow: a segment partial above the limit already means overflow;
+            // otherwise each add is <= 65535 and the hub row cannot wrap
+            if (NARROW && sum > NARROW_MAX) *p.narrow_ovf = 1;
             if (sum != SigT(0)) {
                 SigT *dst = reinterpret_cast<SigT *>(p.hub_acc) + (size_t)h * K + l;
                 SigT old = atomicAdd(dst, sum);

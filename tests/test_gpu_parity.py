@@ -330,3 +330,54 @@ def test_profiling_counters_do_not_disturb_results():
             st = G.stats()
             assert st["fwd_ms"] > 0 and st["bwd_ms"] > 0
             assert abs(st["bwd_ms"] - st["bwd_fin_ms"] - st["bwd_push_ms"]) < 1e-9
+
+
+def layered(k: int, layers: int) -> "gg.CSR":
+    """Consecutive layers of k vertices joined completely: sigma from an end
+    vertex to layer d is k^(d-1), exceeding 16 bits for k = 10, d >= 6."""
+    pairs = [(a * k + i, (a + 1) * k + j) for a in range(layers - 1) for i in range(k) for j in range(k)]
+    return gg.from_pairs(k * layers, pairs)
+
+
+@pytest.mark.parametrize("width", [0, 64])
+def test_sigma_width_narrow_and_fp64_rows(width):
+    """16-bit sigma rows (default) and fp64 rows give the same exact BC."""
+    bcb = _bcb()
+    for g in SUITE[::3] + [gg.rmat(12, 16, seed=1)]:
+        want = oracle.bc(g)
+        with bcb.Graph.from_csr(g) as G:
+            G.set_option(bcb.OPT_MODE, 1)
+            G.set_option(bcb.OPT_SIGMA_WIDTH, width)
+            assert_bc_close(G.compute(), want)
+            st = G.stats()
+            if st["batches"]:
+                if width == 64:
+                    assert st["narrow_batches"] == 0
+                else:
+                    assert st["narrow_batches"] == st["batches"] and st["narrow_fallbacks"] == 0
+
+
+@pytest.mark.parametrize("words", [1, 4])
+def test_narrow_sigma_overflow_reruns_batch_in_fp64(words):
+    """sigma > 65535 in some lanes: those batches are re-run with fp64 rows,
+    the others stay narrow; BC, depth stats and the per-source counters
+    match the oracle either way."""
+    bcb = _bcb()
+    big = layered(10, 8)  # sigma up to 10^6 from the end layers
+    g = gg.disjoint_union(big, gg.rmat(9, 8, seed=3))
+    want, stats = oracle.bc(g, stats=True)
+    with bcb.Graph.from_csr(g) as G:
+        G.set_option(bcb.OPT_MODE, 1)
+        G.set_option(bcb.OPT_LANE_WORDS, words)
+        G.set_option(bcb.OPT_SOURCE_ORDER, 0)  # given order: layered sources fill the first batches
+        got = G.compute(g.non_isolated())
+        st = G.stats()
+    assert_bc_close(got, want)
+    S = g.non_isolated()
+    assert st["reached"] == int(stats[S, 0].sum())  # counters restored across the re-run
+    assert st["adj_reached"] == int(stats[S, 1].sum())
+    assert st["dag_edges"] == int(stats[S, 2].sum())
+    assert st["narrow_fallbacks"] >= 1
+    if words == 1:
+        assert st["narrow_batches"] >= 1
+    assert st["narrow_batches"] + st["narrow_fallbacks"] == st["batches"]
