@@ -189,14 +189,17 @@ def run_reference(args, cfg):
 
 def algorithmic_bytes(st, K):
     """SURVEY §8(d-iii) model split per kernel.  A = sum of
-    reached adjacency, D = DAG lane-edges, N = reached lane-vertices:
-      fwd  level kernel (pull)  A(4/K + 1/8) + 8 D + 8 N   col ids shared by K lanes,
-                                 1 mask bit per lane, sigma per DAG edge, sigma row write
-      bwd  push kernel           A(4/K + 1/8) + 8 D          coef value per DAG edge (red)
-      bwd  finalize kernel       32 N                        acc, sigma read; coef, acc write"""
+    reached adjacency, D = DAG lane-edges, N = reached lane-vertices, sb =
+    bytes per stored sigma value (2 for 16-bit rows, 8 for fp64 rows):
+      fwd  level kernel (pull)      A(4/K + 1/8) + sb D + sb N   col ids shared by K lanes,
+                                     1 mask bit per lane, sigma per DAG edge, sigma row write
+      bwd  push + finalize kernels  A(4/K + 1/8) + 8 D + (sb + 16) N   coef value per DAG edge
+                                     (red), sigma and accumulator read, accumulator re-zeroed"""
     A, D, N = st["adj_reached"], st["dag_edges"], st["reached"]
+    nb, b = st["narrow_batches"], max(1, st["batches"])
+    sb = (2.0 * nb + 8.0 * (b - nb)) / b
     scan = A * (4.0 / K + 1.0 / 8.0)
-    return {"fwd": scan + 8.0 * D + 8.0 * N, "bwd_push": scan + 8.0 * D, "bwd_fin": 32.0 * N}
+    return {"fwd": scan + sb * D + sb * N, "bwd": scan + 8.0 * D + (sb + 16.0) * N}
 
 
 def main():
@@ -273,8 +276,8 @@ def main():
     e1 = torch.cuda.Event(enable_timing=True)
     agg = {"fwd_ms": 0.0, "bwd_ms": 0.0, "bwd_push_ms": 0.0, "bwd_fin_ms": 0.0, "fwd_launches": 0,
            "bwd_launches": 0, "kernel_launches": 0, "reached": 0, "adj_reached": 0, "dag_edges": 0,
-           "num_sources": 0, "levels_total": 0, "batches": 0}
-    kbytes = {"fwd": 0.0, "bwd_push": 0.0, "bwd_fin": 0.0}
+           "num_sources": 0, "levels_total": 0, "batches": 0, "narrow_batches": 0, "narrow_fallbacks": 0}
+    kbytes = {"fwd": 0.0, "bwd": 0.0}
     lanes = 0
     e0.record(stream)
     for i in range(args.steps):
@@ -324,16 +327,16 @@ def main():
 
     if rank == 0:
         pk, pk_kind = peaks()
-        kms = {"fwd": agg["fwd_ms"], "bwd_push": agg["bwd_push_ms"], "bwd_fin": agg["bwd_fin_ms"]}
-        names = {"fwd": "lanes_level_kernel<fwd> (pull)", "bwd_push": "lanes_push_kernel<bwd>",
-                 "bwd_fin": "lanes_bwd_finalize_kernel"}
+        kms = {"fwd": agg["fwd_ms"], "bwd": agg["bwd_ms"]}
+        names = {"fwd": "lanes_level_kernel<fwd> (pull; + hub finalize)",
+                 "bwd": "lanes_push_kernel<bwd> (+ finalize kernels)"}
         dom = max(kms, key=lambda k: kms[k])
         dom_ms = kms[dom]
         achieved = kbytes[dom] / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
         traffic = None
         try:
             tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-            traffic = tr.get(cfg, {}).get(dom)
+            traffic = tr.get(cfg, {}).get(dom, {}).get("dram_bytes_per_launch")
         except Exception:
             pass
         roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
@@ -352,11 +355,12 @@ def main():
                        "sources_per_gpu_per_step": per_gpu, "lanes_per_batch": lanes, "pruning": prune,
                        "teps_sources": "|S+| (pruned: each source counts 1 + omega(s))" if prune else "|S|",
                        "parallelism": f"source-sharded x{world} + NCCL BC all-reduce" if world > 1 else "1 GPU",
-                       "l2": "inputs exceed L2 (per step: CSR 4*2m B streamed + sigma/coef rows 8*K*n B); no flush"},
+                       "l2": "inputs exceed L2 (per step: CSR 4*2m B streamed per level, sigma rows 2*K*n B per level, accumulators 8*K*n B); no flush"},
             "teps_paper_convention": 2 * value,
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
             "gpu_launches": agg["kernel_launches"],
-            "stats": {k: agg[k] for k in ("levels_total", "batches", "reached", "adj_reached", "dag_edges")},
+            "stats": {k: agg[k] for k in ("levels_total", "batches", "narrow_batches", "narrow_fallbacks",
+                                          "reached", "adj_reached", "dag_edges")},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -35,6 +35,14 @@ namespace bcb {
 __device__ __forceinline__ void red_add_f64(double *p, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
+// predicated form: no branch around the red (the per-lane condition is data
+// dependent, a branch would diverge)
+__device__ __forceinline__ void red_add_f64_if(double *p, double v, uint32_t pred) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.global.add.f64 [%0], %1;\n\t}" ::"l"(p), "d"(v),
+        "r"(pred)
+        : "memory");
+}
 
 // 1/x for x >= 1 (sigma): hardware approximation + two Newton steps, within
 // ~1 ulp, no division subroutine (which costs registers in the push loop)
@@ -300,10 +308,8 @@ struct PushKernel {
                     for (int j = 0; j < NG; ++j) {
                         if (gm >> j & 1u) {  // uniform
                             const uint32_t cw = (uint32_t)(cwords[j >> 1] >> ((j & 1) * 32));
-                            if (cw >> lane & 1u) {
-                                red_add_f64(arow + 32 * j, cf[j]);
-                                if (FWD) ++st_dag;
-                            }
+                            red_add_f64_if(arow + 32 * j, cf[j], cw >> lane & 1u);
+                            if (FWD) st_dag += cw >> lane & 1u;
                             if (FWD && lane == (j >> 1)) myword |= (uint64_t)cw << ((j & 1) * 32);
                         }
                     }

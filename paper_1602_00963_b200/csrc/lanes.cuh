@@ -263,11 +263,19 @@ struct LanesKernel {
         __syncthreads();
     }
 
+    // warp-reduce the thread counters (bounded by one work unit, so the 32-bit
+    // sums cannot wrap), then one shared atomic per counter per warp
     __device__ void flush_stats() {
-        const unsigned long long v[6] = {st_reach, st_adj, st_dag, st_dsum, st_items, st_hits};
+        const unsigned long long v[6] = {__reduce_add_sync(0xffffffffu, st_reach), warp_sum_u64(st_adj),
+                                         __reduce_add_sync(0xffffffffu, st_dag),
+                                         __reduce_add_sync(0xffffffffu, st_dsum),
+                                         __reduce_add_sync(0xffffffffu, st_items),
+                                         __reduce_add_sync(0xffffffffu, st_hits)};
+        if (lane == 0) {
 #pragma unroll
-        for (int i = 0; i < 6; ++i)
-            if (v[i]) atomicAdd(&sm.st[i], v[i]);
+            for (int i = 0; i < 6; ++i)
+                if (v[i]) atomicAdd(&sm.st[i], v[i]);
+        }
         st_reach = st_dag = st_dsum = st_items = st_hits = 0;
         st_adj = 0;
     }
