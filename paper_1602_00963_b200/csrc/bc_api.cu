@@ -141,6 +141,7 @@ struct LaneWS {
 };
 
 constexpr int LCH = 8;           // levels per mask chunk
+constexpr int FLAG_RING = 4;     // pinned per-level flag slots (termination test one level behind)
 constexpr int TILE_ITEMS = 8192; // non-hub adjacency items per level-kernel tile (soft cap)
 
 }  // namespace
@@ -189,7 +190,8 @@ struct bc_graph {
     int *d_work_ctr = nullptr;              // [4]: level work counter, slices source counter, narrow overflow flag
     int *d_flags = nullptr;                 // [flag_cap]
     int flag_cap = 0;
-    int *h_flag = nullptr;                  // pinned
+    int *h_flag = nullptr;                  // pinned [FLAG_RING][2]: level flag, narrow overflow
+    cudaEvent_t ev_ring[FLAG_RING] = {};    // flags of level L copied
     int *d_src = nullptr;
     int64_t src_cap = 0;
     double *d_bc = nullptr;   // BC in compute (relabelled) ids
@@ -395,8 +397,9 @@ bc_status cluster_sources(bc_graph *g, DevCSR &run, int ns, cudaStream_t st) {
 
 bc_status ensure_flags(bc_graph *g, int need) {
     if (g->flag_cap >= need) return BC_OK;
-    int cap = std::max(need, 2 * g->flag_cap);
-    cap = std::max(cap, 64);
+    // sized for the deepest possible BFS (n levels) on first use: the buffer
+    // must not move while a level kernel reads its predecessor's flag
+    int cap = (int)std::max<int64_t>(need, std::max<int64_t>(g->n + 3, 2 * (int64_t)g->flag_cap));
     dfree(g->d_flags);
     CK(dalloc(&g->d_flags, cap));
     g->flag_cap = cap;
@@ -551,7 +554,8 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
     }
     const int hub_grid = (c.csr->nhub * 32 + BC_NT - 1) / BC_NT;
 
-    int L = 1;
+    int L = 1, Lmax = 0;
+    bool narrow_bad = false;
     for (;;) {
         CK(ensure_level(g, ws, L + 1));
         CK(ensure_flags(g, L + 2));
@@ -564,6 +568,7 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
         p.mask_nxt = level_ptr(g, ws, L + 1);
         p.mask_nxt_ro = nullptr;
         p.any_new = g->d_flags + L + 1;
+        p.prev_new = g->d_flags + L;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (ev_f) {
             cudaEventCreate(&e0);
@@ -597,14 +602,27 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
         CU(cudaGetLastError());
         g->last.fwd_launches += 1;
         g->last.kernel_launches += 1 + (p.nhub > 0);
-        CU(cudaMemcpyAsync(g->h_flag, g->d_flags + L + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
-        if (NARROW) CU(cudaMemcpyAsync(g->h_flag + 1, p.narrow_ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
-        CU(cudaStreamSynchronize(st));
-        if (NARROW && g->h_flag[1]) break;  // sigma overflowed 16 bits: stop, the batch is re-run in fp64
-        if (*g->h_flag == 0) break;
+        // termination (the paper's all-reduce of nq) one level
+        // behind: the host waits for level L-1's flags while level L runs, so
+        // the GPU never idles on the test; the launch past the last level is
+        // a no-op (prev_new == 0)
+        int *hs = g->h_flag + 2 * (L % FLAG_RING);
+        CU(cudaMemcpyAsync(hs, g->d_flags + L + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+        if (NARROW) CU(cudaMemcpyAsync(hs + 1, p.narrow_ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CU(cudaEventRecord(g->ev_ring[L % FLAG_RING], st));
+        if (L >= 2) {
+            const int *hp = g->h_flag + 2 * ((L - 1) % FLAG_RING);
+            CU(cudaEventSynchronize(g->ev_ring[(L - 1) % FLAG_RING]));
+            if (NARROW && hp[1]) narrow_bad = true;  // sigma overflowed 16 bits: the batch is re-run in fp64
+            if (narrow_bad || hp[0] == 0) {
+                Lmax = L - 1;
+                g->last.fwd_launches -= 1;  // the no-op launch
+                break;
+            }
+        }
         ++L;
     }
-    const int Lmax = L;
+    p.prev_new = nullptr;  // forward-only gate
     g->last.levels_total += Lmax;
     if (c.levels_out) *c.levels_out = Lmax;
     if (c.lvl_out) {
@@ -614,7 +632,7 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
     if constexpr (NARROW) {
         // some sigma exceeded 16 bits: nothing has been committed to BC yet,
         // the caller re-runs this batch with fp64 rows
-        if (g->h_flag[1]) {
+        if (narrow_bad) {
             if (c.narrow_failed) *c.narrow_failed = true;
             return BC_OK;
         }
@@ -873,6 +891,8 @@ bc_status bc_destroy(bc_graph *g) {
         if (g->cl_tmp) cudaFree(g->cl_tmp);
         dfree(g->d_tmp);
         if (g->h_flag) cudaFreeHost(g->h_flag);
+        for (auto &e : g->ev_ring)
+            if (e) cudaEventDestroy(e);
         if (g->own_stream) cudaStreamDestroy(g->own_stream);
     }
     delete g;
@@ -889,7 +909,8 @@ static bc_status create_impl(bc_graph *g, int64_t n, const int64_t *row_ptr, con
     CK(dalloc(&g->d_work_ctr, 4));
     CU(cudaMemset(g->d_work_ctr, 0, 4 * sizeof(int)));
     CK(ensure_flags(g, 64));
-    CU(cudaMallocHost((void **)&g->h_flag, 2 * sizeof(int)));
+    CU(cudaMallocHost((void **)&g->h_flag, 2 * FLAG_RING * sizeof(int)));
+    for (auto &e : g->ev_ring) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CK(dalloc(&g->d_bc, (size_t)n));
     // CSR: int64 row_ptr -> int32 on device
     long long *rp64 = nullptr;

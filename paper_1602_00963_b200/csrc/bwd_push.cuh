@@ -308,7 +308,11 @@ struct PushKernel {
                     for (int j = 0; j < NG; ++j) {
                         if (gm >> j & 1u) {  // uniform
                             const uint32_t cw = (uint32_t)(cwords[j >> 1] >> ((j & 1) * 32));
+#ifdef BC_EXP_NORED  // experiment build only: traversal cost without the reds (wrong results)
+                            red_add_f64_if(arow + 32 * j, cf[j], (cw >> lane & 1u) & (cf[j] == -1.0));
+#else
                             red_add_f64_if(arow + 32 * j, cf[j], cw >> lane & 1u);
+#endif
                             if (FWD) st_dag += cw >> lane & 1u;
                             if (FWD && lane == (j >> 1)) myword |= (uint64_t)cw << ((j & 1) * 32);
                         }
@@ -427,6 +431,7 @@ struct PushKernel {
 
 template <int W, bool FWD, typename RT = double>
 __global__ void __launch_bounds__(BC_NT, BC_PUSH_MINB) lanes_push_kernel(LanesParams p, double *A) {
+    if (FWD && p.prev_new && *p.prev_new == 0) return;
     __shared__ PushSmem<W> sm;
     PushKernel<W, FWD, RT> k(p, A, sm);
     const int total = p.nseg + p.ntiles;
@@ -452,6 +457,7 @@ __global__ void __launch_bounds__(BC_NT, BC_PUSH_MINB) lanes_push_kernel(LanesPa
 template <int W>
 __global__ void __launch_bounds__(BC_NT) lanes_fwd_commit_kernel(LanesParams p, double *__restrict__ A) {
     constexpr int K = 64 * W, NG = 2 * W;
+    if (p.prev_new && *p.prev_new == 0) return;
     __shared__ double ns_sm[K];
     const int lane = lane_id();
     if (p.lane_ns) {

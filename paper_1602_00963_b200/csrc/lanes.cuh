@@ -169,6 +169,8 @@ struct LanesParams {
     const int *tile_vs;          // [ntiles+1] tile t = vertices [tile_vs[t], tile_vs[t+1]), <= TV of them
     double *dbg_delta;           // backward: delta of lane 0 (verification), nullable
     int *narrow_ovf;             // narrow forward: set when some sigma > 65535 (batch is re-run in fp64)
+    const int *prev_new;         // forward: flag "level L is non-empty"; 0 -> the launch is a no-op
+                                 // (levels are launched one ahead of the host's termination test)
     void *part;                  // [gridDim][BC_NW][2][K] SigT: partial sums of slots split across warps
 };
 
@@ -734,6 +736,7 @@ struct LanesKernel {
 template <int W, typename SigT, bool BWD = false>
 __global__ void __launch_bounds__(BC_NT, (W == 4 ? BC_MINB4 : BC_MINB)) lanes_level_kernel(LanesParams p) {
     extern __shared__ __align__(16) unsigned char smraw[];
+    if (p.prev_new && *p.prev_new == 0) return;  // speculative launch past the last level
     LanesSmem<W, SigT> &sm = *reinterpret_cast<LanesSmem<W, SigT> *>(smraw);
     LanesKernel<W, SigT, BWD> k(p, sm);
     const int total = p.nseg + p.ntiles;
@@ -759,6 +762,7 @@ template <int W, typename SigT, bool BWD = false>
 __global__ void __launch_bounds__(BC_NT) lanes_hub_finalize(LanesParams p) {
     using KK = LanesKernel<W, SigT, BWD>;
     constexpr int K = KK::K, LPT = KK::LPT;
+    if (p.prev_new && *p.prev_new == 0) return;
     extern __shared__ __align__(16) unsigned char smraw[];
     LanesSmem<W, SigT> &sm = *reinterpret_cast<LanesSmem<W, SigT> *>(smraw);
     KK k(p, sm);
