@@ -310,6 +310,8 @@ struct PushKernel {
                             const uint32_t cw = (uint32_t)(cwords[j >> 1] >> ((j & 1) * 32));
 #ifdef BC_EXP_NORED  // experiment build only: traversal cost without the reds (wrong results)
                             red_add_f64_if(arow + 32 * j, cf[j], (cw >> lane & 1u) & (cf[j] == -1.0));
+#elif defined(BC_EXP_REDZERO)  // experiment: unpredicated red of 0.0 outside c (more L2 sectors, no branches)
+                            red_add_f64(arow + 32 * j, (cw >> lane & 1u) ? cf[j] : 0.0);
 #else
                             red_add_f64_if(arow + 32 * j, cf[j], cw >> lane & 1u);
 #endif
