@@ -130,7 +130,8 @@ bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma,
 
 /* Tuning options (bc_set_option).  Values are validated. */
 typedef enum {
-    BC_OPT_LANE_WORDS = 1, /* 0 = auto, else 1, 2 or 4: K = 64*value source lanes per batch */
+    BC_OPT_LANE_WORDS = 1, /* 0 = auto (8 for n <= 2^18, else 4, fewer for small source sets or short HBM),
+                              else 1, 2, 4 or 8: K = 64*value source lanes per batch */
     BC_OPT_HUB_DEGREE = 2, /* vertices with degree > value are processed as split hubs (>= 32) */
     BC_OPT_PROFILE = 3,    /* 1 = record CUDA events around the level kernels (bc_get_stats) */
     BC_OPT_MODE = 4,       /* 0 = auto, 1 = lanes (bit-lane batches), 2 = slices (CTA per source) */
@@ -140,7 +141,9 @@ typedef enum {
     BC_OPT_BWD_MODE = 8,    /* backward sweep: 0 = default, 1 = push form, 2 = pull form (successor checking) */
     BC_OPT_SIGMA_WIDTH = 9  /* lanes forward sigma rows: 0 or 16 (default) = uint16 rows, a batch whose
                                sigma exceeds 65535 is re-run with fp64 rows; 64 = fp64 rows only.
-                               sigma is an integer (Alg.1 line 20), so both are exact */
+                               sigma is an integer (Alg.1 line 20), so both are exact */,
+    BC_OPT_STREAMS = 10     /* lanes mode: concurrent batch pipelines, 1..4 (default 3; fewer if HBM is short).
+                               Batches are independent (BC is additive over sources) */
 } bc_option;
 
 bc_status bc_set_option(bc_graph *g, int option, int64_t value);

@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 #include <algorithm>
+#include <thread>
 
 #include "bc.h"
 #include "util.cuh"
@@ -143,6 +144,45 @@ struct LaneWS {
 constexpr int LCH = 8;           // levels per mask chunk
 constexpr int FLAG_RING = 4;     // pinned per-level flag slots (termination test one level behind)
 constexpr int TILE_ITEMS = 8192; // non-hub adjacency items per level-kernel tile (soft cap)
+constexpr int MAX_STREAMS = 4;   // concurrent batch pipelines (BC_OPT_STREAMS)
+
+// One batch pipeline: a workspace, a stream and the per-stream control state.
+// bc_compute runs up to MAX_STREAMS of them concurrently (one host thread
+// each), so the level kernels of one batch fill the tails and the host-test
+// gaps of another and a forward (L1-bound gathers) overlaps a backward (L2
+// reds) on the same SMs.
+struct LaneCtx {
+    LaneWS ws;
+    cudaStream_t st = nullptr;   // stream of the current call (own, or the caller's)
+    cudaStream_t own = nullptr;
+    unsigned long long *d_stats = nullptr;  // [16]: counters, backup across a narrow re-run
+    int *d_work_ctr = nullptr;              // [4]: level work counter, -, narrow overflow flag
+    int *d_flags = nullptr;                 // [flag_cap] per-level "non-empty" flags
+    int flag_cap = 0;
+    int *h_flag = nullptr;                  // pinned [FLAG_RING][2]: level flag, narrow overflow
+    cudaEvent_t ev_ring[FLAG_RING] = {};
+    cudaEvent_t done = nullptr;
+    double *d_bc = nullptr;                 // BC accumulator this pipeline adds into
+    double *own_bc = nullptr;               // private partial BC (pipelines > 0)
+    bc_stats last{};                        // host counters of the current call
+    std::vector<cudaEvent_t> ef, eb, epush; // profile intervals
+    bool ready = false;
+    void release() {
+        ws.release();
+        dfree(d_stats);
+        dfree(d_work_ctr);
+        dfree(d_flags);
+        dfree(own_bc);
+        flag_cap = 0;
+        if (h_flag) cudaFreeHost(h_flag);
+        h_flag = nullptr;
+        for (auto &e : ev_ring)
+            if (e) cudaEventDestroy(e), e = nullptr;
+        if (done) cudaEventDestroy(done), done = nullptr;
+        if (own) cudaStreamDestroy(own), own = nullptr;
+        ready = false;
+    }
+};
 
 }  // namespace
 
@@ -184,14 +224,12 @@ struct bc_graph {
     int mode = 0;
     int num_sms = 148;
     cudaStream_t own_stream = nullptr;
-    LaneWS ws, vws;  // compute workspace, verification workspace (W = 1)
+    LaneCtx ctx[MAX_STREAMS];  // batch pipelines of bc_compute
+    LaneCtx vctx, sctx;        // bc_sssp: integer verification (W = 1, uint64) and its fp64 delta pass
+    int streams_opt = 3;       // BC_OPT_STREAMS (S20: 1 / 2 / 3 pipelines = 332 / 319 / 316 ms per 8192 sources)
     SlicesWS sws;    // slices-mode workspace
-    unsigned long long *d_stats = nullptr;  // [4]
-    int *d_work_ctr = nullptr;              // [4]: level work counter, slices source counter, narrow overflow flag
-    int *d_flags = nullptr;                 // [flag_cap]
-    int flag_cap = 0;
-    int *h_flag = nullptr;                  // pinned [FLAG_RING][2]: level flag, narrow overflow
-    cudaEvent_t ev_ring[FLAG_RING] = {};    // flags of level L copied
+    unsigned long long *d_stats = nullptr;  // [16] slices mode / trivial sources counters
+    int *d_work_ctr = nullptr;              // [4]: -, slices source counter
     int *d_src = nullptr;
     int64_t src_cap = 0;
     double *d_bc = nullptr;   // BC in compute (relabelled) ids
@@ -199,7 +237,6 @@ struct bc_graph {
     int *d_tmp = nullptr;  // scan scratch
     int64_t tmp_cap = 0;
     bc_stats last{};
-    std::vector<cudaEvent_t> ev_push;  // profile: push-kernel intervals of the last compute
     unsigned long long *cl_kin = nullptr, *cl_kout = nullptr;  // source clustering scratch
     int *cl_vout = nullptr;
     int64_t cl_cap = 0;
@@ -395,14 +432,29 @@ bc_status cluster_sources(bc_graph *g, DevCSR &run, int ns, cudaStream_t st) {
     return BC_OK;
 }
 
-bc_status ensure_flags(bc_graph *g, int need) {
-    if (g->flag_cap >= need) return BC_OK;
+bc_status ensure_flags(bc_graph *g, LaneCtx &x, int need) {
+    if (x.flag_cap >= need) return BC_OK;
     // sized for the deepest possible BFS (n levels) on first use: the buffer
     // must not move while a level kernel reads its predecessor's flag
-    int cap = (int)std::max<int64_t>(need, std::max<int64_t>(g->n + 3, 2 * (int64_t)g->flag_cap));
-    dfree(g->d_flags);
-    CK(dalloc(&g->d_flags, cap));
-    g->flag_cap = cap;
+    int cap = (int)std::max<int64_t>(need, std::max<int64_t>(g->n + 3, 2 * (int64_t)x.flag_cap));
+    dfree(x.d_flags);
+    CK(dalloc(&x.d_flags, cap));
+    x.flag_cap = cap;
+    return BC_OK;
+}
+
+bc_status ctx_init(bc_graph *g, LaneCtx &x) {
+    if (x.ready) return BC_OK;
+    CU(cudaStreamCreateWithFlags(&x.own, cudaStreamNonBlocking));
+    CK(dalloc(&x.d_stats, 16));
+    CU(cudaMemset(x.d_stats, 0, 16 * sizeof(unsigned long long)));
+    CK(dalloc(&x.d_work_ctr, 4));
+    CU(cudaMemset(x.d_work_ctr, 0, 4 * sizeof(int)));
+    CK(ensure_flags(g, x, 64));
+    CU(cudaMallocHost((void **)&x.h_flag, 2 * FLAG_RING * sizeof(int)));
+    for (auto &e : x.ev_ring) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&x.done, cudaEventDisableTiming));
+    x.ready = true;
     return BC_OK;
 }
 
@@ -491,11 +543,12 @@ struct BatchCtx {
 
 // Run one batch (forward + backward) with K = 64*W lanes.
 template <int W, typename SigT>
-bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cudaEvent_t> *ev_f,
+bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cudaEvent_t> *ev_f,
                     std::vector<cudaEvent_t> *ev_b) {
     constexpr int K = 64 * W;
     const int n = (int)g->n;
-    cudaStream_t st = c.st;
+    cudaStream_t st = x.st;
+    LaneWS &ws = x.ws;
     LanesParams p{};
     p.n = n;
     p.rp = c.csr->rp;
@@ -503,12 +556,12 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
     p.omega = c.omega;
     p.seen = ws.seen;
     p.ovf = ws.ovf;
-    p.bc = g->d_bc;
+    p.bc = x.d_bc;
     p.lane_w1 = ws.lane_w1;
     p.lane_ns = c.omega ? ws.lane_ns : nullptr;
-    p.stats = g->d_stats;
-    p.work_ctr = g->d_work_ctr;
-    for (int j = 0; j < 4; ++j) p.active[j] = 0;
+    p.stats = x.d_stats;
+    p.work_ctr = x.d_work_ctr;
+    for (int j = 0; j < 8; ++j) p.active[j] = 0;
     for (int l = 0; l < c.nl; ++l) p.active[l >> 6] |= 1ull << (l & 63);
     p.hub_deg = g->hub_deg;
     p.nhub = c.csr->nhub;
@@ -522,7 +575,7 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
     p.ntiles = c.csr->ntiles;
     p.tile_vs = c.csr->tile_vs;
     p.dbg_delta = nullptr;
-    p.narrow_ovf = g->d_work_ctr + 2;  // fixed address (d_flags may grow and move with the level count)
+    p.narrow_ovf = x.d_work_ctr + 2;  // fixed address (d_flags may grow and move with the level count)
     using RT = typename RowOf<SigT>::t;
     constexpr bool NARROW = std::is_same<SigT, unsigned>::value;
     if (NARROW) CU(cudaMemsetAsync(p.narrow_ovf, 0, sizeof(int), st));
@@ -534,7 +587,7 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
     if (ws.ovf) CU(cudaMemsetAsync(ws.ovf, 0, mbytes, st));
     CU(cudaMemsetAsync(level_ptr(g, ws, 0), 0, mbytes, st));
     CU(cudaMemsetAsync(level_ptr(g, ws, 1), 0, mbytes, st));
-    p.any_new = g->d_flags + 1;
+    p.any_new = x.d_flags + 1;
     lanes_init_kernel<W, SigT><<<c.nl, BC_NT, 0, st>>>(p, c.src, level_ptr(g, ws, 0), level_ptr(g, ws, 1));
     {
         const unsigned mb = (unsigned)(((int64_t)n * 32 + 255) / 256);
@@ -542,7 +595,7 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
         lanes_materialize_kernel<W, RT><<<mb, 256, 0, st>>>(n, level_ptr(g, ws, 1), (RT *)ws.slev[1]);
     }
     CU(cudaGetLastError());
-    g->last.kernel_launches += 4;
+    x.last.kernel_launches += 4;
 
     auto kf = lanes_level_kernel<W, SigT>;
     const int units = p.nseg + p.ntiles;
@@ -558,17 +611,17 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
     bool narrow_bad = false;
     for (;;) {
         CK(ensure_level(g, ws, L + 1));
-        CK(ensure_flags(g, L + 2));
+        CK(ensure_flags(g, x, L + 2));
         CU(cudaMemsetAsync(level_ptr(g, ws, L + 1), 0, mbytes, st));
-        CU(cudaMemsetAsync(g->d_flags + L + 1, 0, sizeof(int), st));
+        CU(cudaMemsetAsync(x.d_flags + L + 1, 0, sizeof(int), st));
         p.level = L;
         p.S_cur = ws.slev[L];
         p.S_nxt = ws.slev[L + 1];
         p.mask_cur = level_ptr(g, ws, L);
         p.mask_nxt = level_ptr(g, ws, L + 1);
         p.mask_nxt_ro = nullptr;
-        p.any_new = g->d_flags + L + 1;
-        p.prev_new = g->d_flags + L;
+        p.any_new = x.d_flags + L + 1;
+        p.prev_new = x.d_flags + L;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (ev_f) {
             cudaEventCreate(&e0);
@@ -600,30 +653,30 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
             ev_f->push_back(e1);
         }
         CU(cudaGetLastError());
-        g->last.fwd_launches += 1;
-        g->last.kernel_launches += 1 + (p.nhub > 0);
+        x.last.fwd_launches += 1;
+        x.last.kernel_launches += 1 + (p.nhub > 0);
         // termination (the paper's all-reduce of nq) one level
         // behind: the host waits for level L-1's flags while level L runs, so
         // the GPU never idles on the test; the launch past the last level is
         // a no-op (prev_new == 0)
-        int *hs = g->h_flag + 2 * (L % FLAG_RING);
-        CU(cudaMemcpyAsync(hs, g->d_flags + L + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+        int *hs = x.h_flag + 2 * (L % FLAG_RING);
+        CU(cudaMemcpyAsync(hs, x.d_flags + L + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
         if (NARROW) CU(cudaMemcpyAsync(hs + 1, p.narrow_ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
-        CU(cudaEventRecord(g->ev_ring[L % FLAG_RING], st));
+        CU(cudaEventRecord(x.ev_ring[L % FLAG_RING], st));
         if (L >= 2) {
-            const int *hp = g->h_flag + 2 * ((L - 1) % FLAG_RING);
-            CU(cudaEventSynchronize(g->ev_ring[(L - 1) % FLAG_RING]));
+            const int *hp = x.h_flag + 2 * ((L - 1) % FLAG_RING);
+            CU(cudaEventSynchronize(x.ev_ring[(L - 1) % FLAG_RING]));
             if (NARROW && hp[1]) narrow_bad = true;  // sigma overflowed 16 bits: the batch is re-run in fp64
             if (narrow_bad || hp[0] == 0) {
                 Lmax = L - 1;
-                g->last.fwd_launches -= 1;  // the no-op launch
+                x.last.fwd_launches -= 1;  // the no-op launch
                 break;
             }
         }
         ++L;
     }
     p.prev_new = nullptr;  // forward-only gate
-    g->last.levels_total += Lmax;
+    x.last.levels_total += Lmax;
     if (c.levels_out) *c.levels_out = Lmax;
     if (c.lvl_out) {
         c.lvl_out->clear();
@@ -656,7 +709,7 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
                 p.mask_cur = level_ptr(g, ws, l);
                 p.mask_nxt_ro = level_ptr(g, ws, l + 1);  // all zero for l == Lmax
                 p.mask_nxt = nullptr;
-                p.any_new = g->d_flags;  // unused
+                p.any_new = x.d_flags;  // unused
                 cudaEvent_t e0 = nullptr, e1 = nullptr;
                 if (ev_b) {
                     cudaEventCreate(&e0);
@@ -671,8 +724,8 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
                     ev_b->push_back(e1);
                 }
                 CU(cudaGetLastError());
-                g->last.bwd_launches += 1;
-                g->last.kernel_launches += 1 + (p.nhub > 0);
+                x.last.bwd_launches += 1;
+                x.last.kernel_launches += 1 + (p.nhub > 0);
             }
         }
         }
@@ -696,7 +749,7 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
                 p.mask_cur = level_ptr(g, ws, l);
                 p.mask_nxt_ro = level_ptr(g, ws, l - 1);  // parents
                 p.mask_nxt = nullptr;
-                p.any_new = g->d_flags;  // unused
+                p.any_new = x.d_flags;  // unused
                 cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
                 if (ev_b) {
                     cudaEventCreate(&e0);
@@ -720,19 +773,19 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
                 }
                 if (ev_b) {
                     cudaEventRecord(e3, st);
-                    g->ev_push.push_back(e0);
-                    g->ev_push.push_back(e1);
+                    x.epush.push_back(e0);
+                    x.epush.push_back(e1);
                     ev_b->push_back(e2);
                     ev_b->push_back(e3);
                 }
                 CU(cudaGetLastError());
-                g->last.bwd_launches += 1;
-                g->last.kernel_launches += nk;
+                x.last.bwd_launches += 1;
+                x.last.kernel_launches += nk;
             }
         }
         if (c.run_backward && c.endpoint && c.omega) {
-            lanes_endpoint_kernel<<<(c.nl + 255) / 256, 256, 0, st>>>(c.src, c.nl, c.omega, ws.lane_ns, g->d_bc);
-            g->last.kernel_launches += 1;
+            lanes_endpoint_kernel<<<(c.nl + 255) / 256, 256, 0, st>>>(c.src, c.nl, c.omega, ws.lane_ns, x.d_bc);
+            x.last.kernel_launches += 1;
         }
     }
     CU(cudaGetLastError());
@@ -740,12 +793,13 @@ bc_status run_batch(bc_graph *g, LaneWS &ws, const BatchCtx &c, std::vector<cuda
 }
 
 template <typename SigT>
-bc_status run_batch_w(bc_graph *g, LaneWS &ws, int W, const BatchCtx &c, std::vector<cudaEvent_t> *ef,
+bc_status run_batch_w(bc_graph *g, LaneCtx &x, int W, const BatchCtx &c, std::vector<cudaEvent_t> *ef,
                       std::vector<cudaEvent_t> *eb) {
     switch (W) {
-        case 1: return run_batch<1, SigT>(g, ws, c, ef, eb);
-        case 2: return run_batch<2, SigT>(g, ws, c, ef, eb);
-        case 4: return run_batch<4, SigT>(g, ws, c, ef, eb);
+        case 1: return run_batch<1, SigT>(g, x, c, ef, eb);
+        case 2: return run_batch<2, SigT>(g, x, c, ef, eb);
+        case 4: return run_batch<4, SigT>(g, x, c, ef, eb);
+        case 8: return run_batch<8, SigT>(g, x, c, ef, eb);
         default: return fail(BC_ERR_INTERNAL, "bad lane words %d", W);
     }
 }
@@ -835,6 +889,14 @@ bool is_device_ptr(const void *p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+__global__ void add_kernel(int n, const double *src, double *dst) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) dst[v] += src[v];
+}
+__global__ void add_stats_kernel(const unsigned long long *src, unsigned long long *dst) {
+    if (threadIdx.x < 8) dst[threadIdx.x] += src[threadIdx.x];
+}
+
 double sum_events(std::vector<cudaEvent_t> &ev) {
     double tot = 0;
     for (size_t i = 0; i + 1 < ev.size(); i += 2) {
@@ -876,12 +938,12 @@ bc_status bc_destroy(bc_graph *g) {
         g->res.release();
         dfree(g->omega);
         dfree(g->removed);
-        g->ws.release();
-        g->vws.release();
+        for (auto &x : g->ctx) x.release();
+        g->vctx.release();
+        g->sctx.release();
         g->sws.release();
         dfree(g->d_stats);
         dfree(g->d_work_ctr);
-        dfree(g->d_flags);
         dfree(g->d_src);
         dfree(g->d_bc);
         dfree(g->d_bc2);
@@ -890,9 +952,6 @@ bc_status bc_destroy(bc_graph *g) {
         dfree(g->cl_vout);
         if (g->cl_tmp) cudaFree(g->cl_tmp);
         dfree(g->d_tmp);
-        if (g->h_flag) cudaFreeHost(g->h_flag);
-        for (auto &e : g->ev_ring)
-            if (e) cudaEventDestroy(e);
         if (g->own_stream) cudaStreamDestroy(g->own_stream);
     }
     delete g;
@@ -908,9 +967,6 @@ static bc_status create_impl(bc_graph *g, int64_t n, const int64_t *row_ptr, con
     CK(dalloc(&g->d_stats, 16));  // [0, 8) counters, [8, 16) backup across a narrow re-run
     CK(dalloc(&g->d_work_ctr, 4));
     CU(cudaMemset(g->d_work_ctr, 0, 4 * sizeof(int)));
-    CK(ensure_flags(g, 64));
-    CU(cudaMallocHost((void **)&g->h_flag, 2 * FLAG_RING * sizeof(int)));
-    for (auto &e : g->ev_ring) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CK(dalloc(&g->d_bc, (size_t)n));
     // CSR: int64 row_ptr -> int32 on device
     long long *rp64 = nullptr;
@@ -1025,8 +1081,8 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
     if (!g) return fail(BC_ERR_INVALID, "NULL handle");
     switch (option) {
         case BC_OPT_LANE_WORDS:
-            if (value != 0 && value != 1 && value != 2 && value != 4)
-                return fail(BC_ERR_INVALID, "lane words must be 0, 1, 2 or 4");
+            if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8)
+                return fail(BC_ERR_INVALID, "lane words must be 0, 1, 2, 4 or 8");
             g->lane_words_opt = (int)value;
             return BC_OK;
         case BC_OPT_HUB_DEGREE: {
@@ -1049,6 +1105,10 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
         case BC_OPT_SIGMA_WIDTH:
             if (value != 0 && value != 16 && value != 64) return fail(BC_ERR_INVALID, "sigma width must be 0, 16 or 64");
             g->sigma_width = (int)value;
+            return BC_OK;
+        case BC_OPT_STREAMS:
+            if (value < 1 || value > MAX_STREAMS) return fail(BC_ERR_INVALID, "streams must be 1..%d", MAX_STREAMS);
+            g->streams_opt = (int)value;
             return BC_OK;
         case BC_OPT_SOURCE_ORDER:
             if (value < 0 || value > 3) return fail(BC_ERR_INVALID, "source order must be 0..3");
@@ -1153,18 +1213,38 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     int W = g->lane_words_opt;
     if (W == 0) {
         W = trav.size() > 128 ? 4 : (trav.size() > 64 ? 2 : 1);
+        // K = 512 halves the items per source again but doubles the lanes a
+        // thread carries: faster only where per-batch overhead dominates
+        // (S16: 74 -> 60 ms per 16384 sources; S20: 319 -> 362 ms)
+        if (trav.size() > 256 && g->n <= (1 << 18)) W = 8;
         // level rows cost n*512*W bytes per BFS level: keep ~10 levels within
         // half of the free HBM (S23 -> W = 2)
         size_t free_b = 0, total_b = 0;
         if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-            free_b += (size_t)g->ws.slev.size() * (size_t)g->n * 512 * (size_t)g->ws.W;  // reusable
+            for (auto &x : g->ctx) free_b += (size_t)x.ws.slev.size() * (size_t)g->n * 512 * (size_t)x.ws.W;  // reusable
             while (W > 1 && (double)10 * g->n * 512.0 * W > 0.5 * (double)free_b) W >>= 1;
         }
         (void)cudaGetLastError();
     }
     const int K = 64 * W;
     g->last.lanes = K;
-    if (mode == 1) CK(ensure_ws(g, g->ws, W, false, std::max(run.nhub, g->orig.nhub)));
+    // concurrent batch pipelines: bounded by the option, the batch count and
+    // memory (each holds ~10 levels of rows plus the accumulators)
+    const int nbatch = (int)((trav.size() + K - 1) / K);
+    int NS = mode == 1 ? std::max(1, std::min(g->streams_opt, nbatch)) : 1;
+    if (NS > 1) {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+            for (auto &x : g->ctx) free_b += (size_t)x.ws.slev.size() * (size_t)g->n * 512 * (size_t)x.ws.W;
+            while (NS > 1 && (double)NS * 11 * g->n * 512.0 * W > 0.6 * (double)free_b) --NS;
+        }
+        (void)cudaGetLastError();
+    }
+    if (mode == 1)
+        for (int i = 0; i < NS; ++i) {
+            CK(ctx_init(g, g->ctx[i]));
+            CK(ensure_ws(g, g->ctx[i].ws, W, false, std::max(run.nhub, g->orig.nhub)));
+        }
     const int64_t need = (int64_t)(trav.size() + triv.size());
     if (g->src_cap < need) {
         dfree(g->d_src);
@@ -1185,38 +1265,104 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
         CU(cudaMemcpyAsync(g->d_src + trav.size(), triv.data(), triv.size() * 4, cudaMemcpyHostToDevice, st));
     CU(cudaMemsetAsync(g->d_bc, 0, (size_t)n * 8, st));
     CU(cudaMemsetAsync(g->d_stats, 0, 8 * sizeof(unsigned long long), st));
-    std::vector<cudaEvent_t> ef, eb;
+    std::vector<cudaEvent_t> ef;
     if (mode == 2 && !trav.empty()) CK(run_slices(g, run, g->d_src, (int)trav.size(), st, g->profile ? &ef : nullptr));
-    for (size_t off = 0; mode == 1 && off < trav.size(); off += K) {
-        BatchCtx c{};
-        c.csr = &run;
-        c.omega = g->pruned ? run.omega : nullptr;
-        c.src = g->d_src + off;
-        c.nl = (int)std::min<size_t>(K, trav.size() - off);
-        c.st = st;
-        c.run_backward = true;
-        c.endpoint = true;
-        g->last.batches += 1;
-        // narrow sigma first (16-bit rows, exact integers); a batch whose sigma
-        // overflows is re-run with fp64 rows from scratch (nothing of it was
-        // committed: BC is only touched by the backward sweep)
-        const bool narrow = g->sigma_width != 64 && g->hub_deg <= 65536 && g->bwd_mode != 2 && g->fwd_push_levels == 0;
-        if (narrow) {
-            bool failed = false;
-            c.narrow_failed = &failed;
-            const int64_t lv = g->last.levels_total;
-            CU(cudaMemcpyAsync(g->d_stats + 8, g->d_stats, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
-            CK(run_batch_w<unsigned>(g, g->ws, W, c, g->profile ? &ef : nullptr, g->profile ? &eb : nullptr));
-            if (!failed) {
-                g->last.narrow_batches += 1;
-                continue;
-            }
-            CU(cudaMemcpyAsync(g->d_stats, g->d_stats + 8, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
-            g->last.levels_total = lv;
-            g->last.narrow_fallbacks += 1;
-            c.narrow_failed = nullptr;
+    if (mode == 1 && !trav.empty()) {
+        // pipeline i runs batches i, i + NS, ...; pipeline 0 adds into d_bc,
+        // the others into private partials summed at the end
+        cudaEvent_t start = nullptr;
+        if (NS > 1) {
+            CU(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+            CU(cudaEventRecord(start, st));
         }
-        CK(run_batch_w<double>(g, g->ws, W, c, g->profile ? &ef : nullptr, g->profile ? &eb : nullptr));
+        bc_status sts[MAX_STREAMS];
+        std::string msgs[MAX_STREAMS];
+        auto worker = [&](int i) {
+            LaneCtx &x = g->ctx[i];
+            DeviceGuard dgw(g->device);
+            x.last = bc_stats{};
+            x.st = NS > 1 ? x.own : st;
+            bc_status r = BC_OK;
+            auto body = [&]() -> bc_status {
+                cudaStream_t xs = x.st;
+                if (NS > 1) CU(cudaStreamWaitEvent(xs, start, 0));
+                CU(cudaMemsetAsync(x.d_stats, 0, 8 * sizeof(unsigned long long), xs));
+                if (i == 0) {
+                    x.d_bc = g->d_bc;
+                } else {
+                    if (!x.own_bc) CK(dalloc(&x.own_bc, (size_t)n));
+                    x.d_bc = x.own_bc;
+                    CU(cudaMemsetAsync(x.d_bc, 0, (size_t)n * 8, xs));
+                }
+                for (size_t off = (size_t)i * K; off < trav.size(); off += (size_t)NS * K) {
+                    BatchCtx c{};
+                    c.csr = &run;
+                    c.omega = g->pruned ? run.omega : nullptr;
+                    c.src = g->d_src + off;
+                    c.nl = (int)std::min<size_t>(K, trav.size() - off);
+                    c.st = xs;
+                    c.run_backward = true;
+                    c.endpoint = true;
+                    x.last.batches += 1;
+                    // narrow sigma first (16-bit rows, exact integers); a batch whose sigma
+                    // overflows is re-run with fp64 rows from scratch (nothing of it was
+                    // committed: BC is only touched by the backward sweep)
+                    const bool narrow =
+                        g->sigma_width != 64 && g->hub_deg <= 65536 && g->bwd_mode != 2 && g->fwd_push_levels == 0;
+                    auto *pef = g->profile ? &x.ef : nullptr;
+                    auto *peb = g->profile ? &x.eb : nullptr;
+                    if (narrow) {
+                        bool failed = false;
+                        c.narrow_failed = &failed;
+                        const int64_t lv = x.last.levels_total;
+                        CU(cudaMemcpyAsync(x.d_stats + 8, x.d_stats, 8 * sizeof(unsigned long long),
+                                           cudaMemcpyDeviceToDevice, xs));
+                        CK(run_batch_w<unsigned>(g, x, W, c, pef, peb));
+                        if (!failed) {
+                            x.last.narrow_batches += 1;
+                            continue;
+                        }
+                        CU(cudaMemcpyAsync(x.d_stats, x.d_stats + 8, 8 * sizeof(unsigned long long),
+                                           cudaMemcpyDeviceToDevice, xs));
+                        x.last.levels_total = lv;
+                        x.last.narrow_fallbacks += 1;
+                        c.narrow_failed = nullptr;
+                    }
+                    CK(run_batch_w<double>(g, x, W, c, pef, peb));
+                }
+                CU(cudaEventRecord(x.done, xs));
+                return BC_OK;
+            };
+            r = body();
+            sts[i] = r;
+            if (r != BC_OK) msgs[i] = bc_last_error();
+        };
+        if (NS == 1) {
+            worker(0);
+        } else {
+            std::vector<std::thread> th;
+            for (int i = 0; i < NS; ++i) th.emplace_back(worker, i);
+            for (auto &t : th) t.join();
+        }
+        if (start) cudaEventDestroy(start);
+        for (int i = 0; i < NS; ++i)
+            if (sts[i] != BC_OK) return fail(sts[i], "%s", msgs[i].c_str());
+        for (int i = 0; i < NS; ++i) {
+            LaneCtx &x = g->ctx[i];
+            if (NS > 1) CU(cudaStreamWaitEvent(st, x.done, 0));
+            if (i > 0) {
+                add_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((int)n, x.d_bc, g->d_bc);
+                g->last.kernel_launches += 1;
+            }
+            add_stats_kernel<<<1, 32, 0, st>>>(x.d_stats, g->d_stats);
+            g->last.batches += x.last.batches;
+            g->last.levels_total += x.last.levels_total;
+            g->last.fwd_launches += x.last.fwd_launches;
+            g->last.bwd_launches += x.last.bwd_launches;
+            g->last.kernel_launches += x.last.kernel_launches;
+            g->last.narrow_batches += x.last.narrow_batches;
+            g->last.narrow_fallbacks += x.last.narrow_fallbacks;
+        }
     }
     if (!triv.empty()) {
         trivial_sources_kernel<<<(unsigned)((triv.size() + 255) / 256), 256, 0, st>>>(
@@ -1246,8 +1392,11 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     g->last.bwd_hits = (int64_t)hst[7];
     if (g->profile) {
         g->last.fwd_ms = sum_events(ef);
-        g->last.bwd_fin_ms = sum_events(eb);
-        g->last.bwd_push_ms = sum_events(g->ev_push);
+        for (auto &x : g->ctx) {
+            g->last.fwd_ms += sum_events(x.ef);
+            g->last.bwd_fin_ms += sum_events(x.eb);
+            g->last.bwd_push_ms += sum_events(x.epush);
+        }
         g->last.bwd_ms = g->last.bwd_fin_ms + g->last.bwd_push_ms;
         float ms = 0;
         cudaEventElapsedTime(&ms, t0, t1);
@@ -1266,7 +1415,10 @@ bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma, 
     const int n = (int)g->n;
     cudaStream_t st = g->own_stream;
     bc_stats keep = g->last;
-    CK(ensure_ws(g, g->vws, 1, true, std::max(g->orig.nhub, g->run.nhub)));
+    CK(ctx_init(g, g->vctx));
+    CK(ensure_ws(g, g->vctx.ws, 1, true, std::max(g->orig.nhub, g->run.nhub)));
+    g->vctx.st = st;
+    g->vctx.d_bc = g->d_bc;
     if (g->src_cap < 1) {
         dfree(g->d_src);
         CK(dalloc(&g->d_src, 1));
@@ -1296,7 +1448,7 @@ bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma, 
         c.lvl_out = &lv;
         int Lmax = 0;
         c.levels_out = &Lmax;
-        s = run_batch<1, unsigned long long>(g, g->vws, c, nullptr, nullptr);
+        s = run_batch<1, unsigned long long>(g, g->vctx, c, nullptr, nullptr);
         if (s == BC_OK) {
             for (int l = 0; l <= Lmax; ++l)
                 depth_from_mask_kernel<<<(n + 255) / 256, 256, 0, st>>>(lv[l], n, 1, l, d_depth);
@@ -1304,9 +1456,12 @@ bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma, 
             CU(cudaMemsetAsync(d_ov, 0, (size_t)n, st));
             for (int l = 0; l <= Lmax; ++l)
                 gather_level_lane0_kernel<unsigned long long><<<(n + 255) / 256, 256, 0, st>>>(
-                    n, lv[l], 1, (const unsigned long long *)g->vws.slev[l], 64, g->vws.ovf, d_sig, d_ov);
-            // fp64 pass for delta (uses the compute workspace at W = 1)
-            s = ensure_ws(g, g->ws, 1, false, std::max(g->orig.nhub, g->run.nhub));
+                    n, lv[l], 1, (const unsigned long long *)g->vctx.ws.slev[l], 64, g->vctx.ws.ovf, d_sig, d_ov);
+            // fp64 pass for delta (its own W = 1 pipeline)
+            s = ctx_init(g, g->sctx);
+            if (s == BC_OK) s = ensure_ws(g, g->sctx.ws, 1, false, std::max(g->orig.nhub, g->run.nhub));
+            g->sctx.st = st;
+            g->sctx.d_bc = g->d_bc;
             if (s == BC_OK) {
                 CU(cudaMemsetAsync(g->d_bc, 0, (size_t)n * 8, st));
                 BatchCtx c2 = c;
@@ -1315,7 +1470,7 @@ bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma, 
                 c2.dbg_delta = d_delta;
                 c2.lvl_out = nullptr;
                 c2.levels_out = nullptr;
-                s = run_batch<1, double>(g, g->ws, c2, nullptr, nullptr);
+                s = run_batch<1, double>(g, g->sctx, c2, nullptr, nullptr);
             }
         }
     } else {

@@ -61,6 +61,9 @@ __device__ __forceinline__ double rcp_f64(double x) {
 #ifndef BC_PUSH_MINB
 #define BC_PUSH_MINB 4  // push kernels need fewer registers: 4 CTAs (32 warps) per SM
 #endif
+#ifndef BC_PUSH_MINB8
+#define BC_PUSH_MINB8 3  // ... W = 8: 16 coef values per thread
+#endif
 
 template <int W>
 struct PushSmem {
@@ -165,7 +168,7 @@ template <int W, bool FWD, typename RT = double>
 struct PushKernel {
     static_assert(!FWD || std::is_same<RT, double>::value, "forward push uses fp64 rows");
     static constexpr int K = 64 * W, NG = 2 * W;
-    static constexpr int R = (W == 4) ? BC_PR4 : 4;  // item steps in flight per warp
+    static constexpr int R = (W >= 4) ? BC_PR4 : 4;  // item steps in flight per warp
     const LanesParams &p;
     double *A;
     PushSmem<W> &sm;
@@ -432,7 +435,7 @@ struct PushKernel {
 };
 
 template <int W, bool FWD, typename RT = double>
-__global__ void __launch_bounds__(BC_NT, BC_PUSH_MINB) lanes_push_kernel(LanesParams p, double *A) {
+__global__ void __launch_bounds__(BC_NT, (W == 8 ? BC_PUSH_MINB8 : BC_PUSH_MINB)) lanes_push_kernel(LanesParams p, double *A) {
     if (FWD && p.prev_new && *p.prev_new == 0) return;
     __shared__ PushSmem<W> sm;
     PushKernel<W, FWD, RT> k(p, A, sm);

@@ -120,13 +120,20 @@ __device__ __forceinline__ void load_mask_smem(const uint64_t *p, uint64_t (&m)[
 // W 32-bit halves to / from shared memory with vector accesses
 template <int W>
 __device__ __forceinline__ void store_halves(uint32_t *d, const uint32_t (&h)[W]) {
-    if constexpr (W == 4) *reinterpret_cast<uint4 *>(d) = make_uint4(h[0], h[1], h[2], h[3]);
+    if constexpr (W == 8) {
+        reinterpret_cast<uint4 *>(d)[0] = make_uint4(h[0], h[1], h[2], h[3]);
+        reinterpret_cast<uint4 *>(d)[1] = make_uint4(h[4], h[5], h[6], h[7]);
+    } else if constexpr (W == 4) *reinterpret_cast<uint4 *>(d) = make_uint4(h[0], h[1], h[2], h[3]);
     else if constexpr (W == 2) *reinterpret_cast<uint2 *>(d) = make_uint2(h[0], h[1]);
     else d[0] = h[0];
 }
 template <int W>
 __device__ __forceinline__ void load_halves(const uint32_t *d, uint32_t (&h)[W]) {
-    if constexpr (W == 4) {
+    if constexpr (W == 8) {
+        const uint4 t = reinterpret_cast<const uint4 *>(d)[0], u = reinterpret_cast<const uint4 *>(d)[1];
+        h[0] = t.x; h[1] = t.y; h[2] = t.z; h[3] = t.w;
+        h[4] = u.x; h[5] = u.y; h[6] = u.z; h[7] = u.w;
+    } else if constexpr (W == 4) {
         const uint4 t = *reinterpret_cast<const uint4 *>(d);
         h[0] = t.x; h[1] = t.y; h[2] = t.z; h[3] = t.w;
     } else if constexpr (W == 2) {
@@ -156,7 +163,7 @@ struct LanesParams {
     int level;                   // L (forward: lvl[L] -> lvl[L+1]; backward: lvl[L])
     int *any_new;
     int *work_ctr;               // self-resetting dynamic tile counter
-    uint64_t active[4];          // lanes in use
+    uint64_t active[8];          // lanes in use (K <= 512)
     int hub_deg;
     int nhub;
     const int *hub_ids;
@@ -241,7 +248,7 @@ template <int W, typename SigT, bool BWD = false>
 struct LanesKernel {
     static constexpr int K = 64 * W;
     static constexpr int LPT = 2 * W;           // lanes per thread
-    static constexpr int R = (W == 1) ? 4 : (W == 2 ? 2 : BC_R4);  // item steps in flight per warp
+    static constexpr int R = (W == 1) ? 4 : (W == 2 ? 2 : BC_R4);  // item steps in flight per warp (W >= 4: BC_R4)
     static constexpr bool VERIFY = std::is_same<SigT, unsigned long long>::value;
     static constexpr bool NARROW = std::is_same<SigT, unsigned>::value;
     using RT = typename RowOf<SigT>::t;  // sigma row storage
@@ -732,9 +739,12 @@ struct LanesKernel {
 #ifndef BC_MINB4
 #define BC_MINB4 4  // ... and at W = 4: 32 resident warps (64 registers, no spills)
 #endif
+#ifndef BC_MINB8
+#define BC_MINB8 3  // ... and at W = 8 (16 lanes per thread)
+#endif
 
 template <int W, typename SigT, bool BWD = false>
-__global__ void __launch_bounds__(BC_NT, (W == 4 ? BC_MINB4 : BC_MINB)) lanes_level_kernel(LanesParams p) {
+__global__ void __launch_bounds__(BC_NT, (W == 8 ? BC_MINB8 : (W == 4 ? BC_MINB4 : BC_MINB))) lanes_level_kernel(LanesParams p) {
     extern __shared__ __align__(16) unsigned char smraw[];
     if (p.prev_new && *p.prev_new == 0) return;  // speculative launch past the last level
     LanesSmem<W, SigT> &sm = *reinterpret_cast<LanesSmem<W, SigT> *>(smraw);

@@ -53,7 +53,7 @@ def small_suite():
 SUITE = small_suite()
 
 
-@pytest.mark.parametrize("words", [1, 2, 4])
+@pytest.mark.parametrize("words", [1, 2, 4, 8])
 @pytest.mark.parametrize("hub", [32, 4096])
 @pytest.mark.parametrize("relabel", [0, 1])
 def test_small_suite_all_sources(words, hub, relabel):
@@ -67,7 +67,7 @@ def test_small_suite_all_sources(words, hub, relabel):
 
 
 @pytest.mark.parametrize("bwd", [1, 2])
-@pytest.mark.parametrize("words", [1, 4])
+@pytest.mark.parametrize("words", [1, 4, 8])
 def test_backward_forms_push_and_pull(bwd, words):
     """Both backward forms (push: bwd_push.cuh; pull / successor checking:
     lanes.cuh BWD) on the small suite with split hubs, unpruned and pruned,
@@ -164,10 +164,10 @@ def test_pruned_partial_sources_equal_S_plus():
 def test_multibatch_ragged_tail_and_additivity():
     bcb = _bcb()
     g = gg.rmat(11, 16, seed=4)
-    S = g.non_isolated()[:300]  # 256 + 44 at K = 256, 64*4 + 44 at K = 64
+    S = g.non_isolated()[:600]  # ragged last batch at K = 64, 256 and 512
     want = oracle.bc(g, S)
     with bcb.Graph.from_csr(g) as G:
-        for words in (1, 4):
+        for words in (1, 4, 8):
             G.set_option(bcb.OPT_LANE_WORDS, words)
             got = G.compute(S)
             assert_bc_close(got, want)
@@ -357,7 +357,7 @@ def test_sigma_width_narrow_and_fp64_rows(width):
                     assert st["narrow_batches"] == st["batches"] and st["narrow_fallbacks"] == 0
 
 
-@pytest.mark.parametrize("words", [1, 4])
+@pytest.mark.parametrize("words", [1, 4, 8])
 def test_narrow_sigma_overflow_reruns_batch_in_fp64(words):
     """sigma > 65535 in some lanes: those batches are re-run with fp64 rows,
     the others stay narrow; BC, depth stats and the per-source counters

@@ -24,6 +24,7 @@ ap.add_argument("--order", type=int, default=2)
 ap.add_argument("--fwd-push", type=int, default=0)
 ap.add_argument("--bwd", type=int, default=0)
 ap.add_argument("--sigma", type=int, default=0)
+ap.add_argument("--streams", type=int, default=2)
 ap.add_argument("--sort", default="none", choices=["none", "deg", "degasc"])
 a = ap.parse_args()
 g = gg.grid(a.grid, a.grid) if a.grid else gg.rmat(a.scale, a.ef, seed=1)
@@ -39,6 +40,7 @@ G.set_option(bcb.OPT_SOURCE_ORDER, a.order)
 G.set_option(bcb.OPT_FWD_PUSH, a.fwd_push)
 G.set_option(bcb.OPT_BWD_MODE, a.bwd)
 G.set_option(bcb.OPT_SIGMA_WIDTH, a.sigma)
+G.set_option(bcb.OPT_STREAMS, a.streams)
 if a.sort != "none":
     d = g.degrees[S]
     S = S[np.argsort(-d if a.sort == "deg" else d, kind="stable")]
