@@ -48,6 +48,8 @@ def _lib():
         L.oracle_sssp.argtypes = [ctypes.c_int64, i64p, i32p, ctypes.c_int32, i32p, u64p, u8p, f64p, f64p]
         L.oracle_prune_degree1.argtypes = [ctypes.c_int64, i64p, i32p, u32p, u8p, i64p, i32p, i64p]
         L.oracle_bc_pruned.argtypes = [ctypes.c_int64, i64p, i32p, i32p, ctypes.c_int64, ctypes.c_int, f64p]
+        L.oracle_two_degree_tree.argtypes = [ctypes.c_int64, ctypes.c_int32, i32p, u64p, u8p, i32p, u64p, u8p, i32p,
+                                             u64p, u8p]
         L.oracle_num_threads.restype = ctypes.c_int
         _lib_handle = L
     return _lib_handle
@@ -93,6 +95,45 @@ def sssp(g, s: int):
     if rc:
         raise RuntimeError("oracle_sssp failed")
     return d, su, ov, sf, de
+
+
+def two_degree_tree(g, c: int, literal_alg7: bool = False):
+    """Alg.7 / Eq.(6): (depth, sigma uint64, overflow) of the 2-degree vertex
+    ``c`` derived from the oracle BFS trees of its two neighbours (Lemma 1).
+    ``literal_alg7`` evaluates the listing as printed (its ``else`` overwrites
+    the equal-level case, reading R23) -- only for the test that shows it is
+    wrong."""
+    n, rp, col = _csr(g)
+    if rp[c + 1] - rp[c] != 2:
+        raise ValueError("c must have degree 2")
+    a, b = int(col[rp[c]]), int(col[rp[c] + 1])
+    da, sa, oa, _, _ = sssp(g, a)
+    db, sb, ob, _, _ = sssp(g, b)
+    if literal_alg7:
+        # PAPER.md:703-716 line by line, unreached = infinity
+        inf = np.iinfo(np.int64).max
+        la = np.where(da < 0, inf, da.astype(np.int64))
+        lb = np.where(db < 0, inf, db.astype(np.int64))
+        sc = np.zeros(n, np.uint64)
+        lc = np.full(n, inf, np.int64)
+        for v in range(n):
+            if la[v] == lb[v]:
+                sc[v] = sa[v] + sb[v]
+                lc[v] = la[v] + 1
+            if la[v] < lb[v]:
+                sc[v] = sa[v]
+                lc[v] = la[v] + 1
+            else:
+                sc[v] = sb[v]
+                lc[v] = lb[v] + 1
+        return lc, sc
+    dc = np.empty(n, np.int32)
+    sc = np.empty(n, np.uint64)
+    oc = np.empty(n, np.uint8)
+    _lib().oracle_two_degree_tree(n, int(c), _p(da, ctypes.c_int32), _p(sa, ctypes.c_uint64), _p(oa, ctypes.c_uint8),
+                                  _p(db, ctypes.c_int32), _p(sb, ctypes.c_uint64), _p(ob, ctypes.c_uint8),
+                                  _p(dc, ctypes.c_int32), _p(sc, ctypes.c_uint64), _p(oc, ctypes.c_uint8))
+    return dc, sc, oc
 
 
 def prune_degree1(g):

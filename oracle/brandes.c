@@ -185,6 +185,46 @@ int oracle_sssp(int64_t n, const int64_t *rp, const int32_t *col, int32_t s, int
     return 0;
 }
 
+/* Alg.7 "Shortest-path tree computation of a 2-degree vertex from its own
+ * neighbors", Lemma 1 and Eq.(6)
+ * (PAPER.md:673-681): c has exactly the neighbours a and b; from their BFS
+ * trees (depth d_a, d_b with -1 = unreached; sigma as uint64 + overflow flag)
+ *     lvl_c(v)   = min(lvl_a(v), lvl_b(v)) + 1
+ *     sigma_c(v) = sigma_a(v)             if lvl_a(v) < lvl_b(v)
+ *                  sigma_b(v)             if lvl_a(v) > lvl_b(v)
+ *                  sigma_a(v) + sigma_b(v) if equal
+ * Two readings (R23): Alg.7's listing lets the `else` branch of its
+ * second test overwrite the equal case with sigma_b alone -- Eq.(6) and the
+ * text decide, the three cases are exclusive here; and Lemma 1 does not hold
+ * for v = c itself (min + 1 = 2), whose level is 0 and sigma 1 by definition
+ * (Alg.1 lines 7-8).  A vertex reached from neither neighbour stays unreached. */
+int oracle_two_degree_tree(int64_t n, int32_t c, const int32_t *d_a, const uint64_t *sig_a, const uint8_t *ovf_a,
+                           const int32_t *d_b, const uint64_t *sig_b, const uint8_t *ovf_b, int32_t *d_c,
+                           uint64_t *sig_c, uint8_t *ovf_c) {
+    for (int64_t v = 0; v < n; ++v) {
+        int32_t la = d_a[v], lb = d_b[v];
+        d_c[v] = -1;
+        sig_c[v] = 0;
+        ovf_c[v] = 0;
+        if (v == c) {
+            d_c[v] = 0;
+            sig_c[v] = 1;
+        } else if (la >= 0 && (lb < 0 || la < lb)) {
+            d_c[v] = la + 1;
+            sig_c[v] = sig_a[v];
+            ovf_c[v] = ovf_a[v];
+        } else if (lb >= 0 && (la < 0 || lb < la)) {
+            d_c[v] = lb + 1;
+            sig_c[v] = sig_b[v];
+            ovf_c[v] = ovf_b[v];
+        } else if (la >= 0) { /* la == lb */
+            d_c[v] = la + 1;
+            ovf_c[v] = (uint8_t)(ovf_a[v] | ovf_b[v] | __builtin_add_overflow(sig_a[v], sig_b[v], &sig_c[v]));
+        }
+    }
+    return 0;
+}
+
 /* Alg.6, one processor (#P = 1): edges are the CSR entries, already sorted
  * by u.  For each (u,v): if u has no other edge (deg(u) = 1) append (v,u) to
  * R and omega[v]++, else append (u,v) to E'.  Then the symmetric edge (v,u)
