@@ -140,10 +140,14 @@ typedef enum {
     BC_OPT_FWD_PUSH = 7,    /* forward levels L <= value expand in push form (default 0), later ones pull */
     BC_OPT_BWD_MODE = 8,    /* backward sweep: 0 = default, 1 = push form, 2 = pull form (successor checking) */
     BC_OPT_SIGMA_WIDTH = 9  /* lanes forward sigma rows: 0 or 16 (default) = uint16 rows, a batch whose
-                               sigma exceeds 65535 is re-run with fp64 rows; 64 = fp64 rows only.
+                               sigma exceeds 65535 is re-run with uint32 rows, then (sigma >= 2^32)
+                               with fp64 rows; 64 = fp64 rows only.
                                sigma is an integer (Alg.1 line 20), so both are exact */,
-    BC_OPT_STREAMS = 10     /* lanes mode: concurrent batch pipelines, 1..4 (default 3; fewer if HBM is short).
+    BC_OPT_STREAMS = 10,    /* lanes mode: concurrent batch pipelines, 1..8 (default 4; fewer if HBM is short).
                                Batches are independent (BC is additive over sources) */
+    BC_OPT_TWO_DEGREE = 11  /* lanes mode: 1 = 2-degree heuristic: a degree-2 source
+                               whose two neighbours are also sources gets its shortest-path tree derived
+                               from theirs (Lemma 1, Eq.(6)) instead of a traversal; default 0 */
 } bc_option;
 
 bc_status bc_set_option(bc_graph *g, int option, int64_t value);
@@ -172,7 +176,9 @@ typedef struct {
     double bwd_fin_ms;       /* backward finalize kernels (BC_OPT_PROFILE)       */
     double bwd_push_ms;      /* backward push kernels (BC_OPT_PROFILE)           */
     int64_t narrow_batches;  /* batches completed with 16-bit sigma rows          */
-    int64_t narrow_fallbacks;/* batches re-run with fp64 rows after a sigma > 65535 */
+    int64_t narrow_fallbacks;/* batches re-run with wider rows after a sigma > 65535 */
+    int64_t mid_batches;     /* ... of which completed with 32-bit rows (the rest: fp64) */
+    int64_t derived_lanes;   /* 2-degree sources whose tree was derived (BC_OPT_TWO_DEGREE) */
 } bc_stats;
 
 bc_status bc_get_stats(const bc_graph *g, bc_stats *out);

@@ -61,7 +61,8 @@ class bc_stats(ctypes.Structure):
         ("total_ms", ctypes.c_double), ("kernel_launches", ctypes.c_int64), ("dist_sum", ctypes.c_int64),
         ("fwd_items", ctypes.c_int64), ("fwd_hits", ctypes.c_int64), ("bwd_items", ctypes.c_int64),
         ("bwd_hits", ctypes.c_int64), ("bwd_fin_ms", ctypes.c_double), ("bwd_push_ms", ctypes.c_double),
-        ("narrow_batches", ctypes.c_int64), ("narrow_fallbacks", ctypes.c_int64),
+        ("narrow_batches", ctypes.c_int64), ("narrow_fallbacks", ctypes.c_int64), ("mid_batches", ctypes.c_int64),
+        ("derived_lanes", ctypes.c_int64),
     ]
 
     def as_dict(self):

@@ -123,7 +123,13 @@ struct LaneWS {
     double *lane_ns = nullptr;
     void *part = nullptr;  // split-slot partial sums [max CTAs][BC_NW][2][K]
     double *A = nullptr;   // push-backward accumulators [n][K], zero between batches
+    uint64_t **d_lv = nullptr;  // device copies of the level mask / row pointers (2-degree derive)
+    void **d_rows = nullptr;
+    int dptr_cap = 0;
     void release() {
+        dfree(d_lv);
+        dfree(d_rows);
+        dptr_cap = 0;
         dfree(part);
         dfree(A);
         for (auto &q : slev) dfree(q);
@@ -144,7 +150,7 @@ struct LaneWS {
 constexpr int LCH = 8;           // levels per mask chunk
 constexpr int FLAG_RING = 4;     // pinned per-level flag slots (termination test one level behind)
 constexpr int TILE_ITEMS = 8192; // non-hub adjacency items per level-kernel tile (soft cap)
-constexpr int MAX_STREAMS = 4;   // concurrent batch pipelines (BC_OPT_STREAMS)
+constexpr int MAX_STREAMS = 8;   // concurrent batch pipelines (BC_OPT_STREAMS)
 
 // One batch pipeline: a workspace, a stream and the per-stream control state.
 // bc_compute runs up to MAX_STREAMS of them concurrently (one host thread
@@ -226,7 +232,17 @@ struct bc_graph {
     cudaStream_t own_stream = nullptr;
     LaneCtx ctx[MAX_STREAMS];  // batch pipelines of bc_compute
     LaneCtx vctx, sctx;        // bc_sssp: integer verification (W = 1, uint64) and its fp64 delta pass
-    int streams_opt = 3;       // BC_OPT_STREAMS (S20: 1 / 2 / 3 pipelines = 332 / 319 / 316 ms per 8192 sources)
+    int two_degree = 0;        // BC_OPT_TWO_DEGREE (NEXT-1)
+    int *td_buf = nullptr;     // 2-degree planning scratch (grow-only)
+    int64_t td_cap = 0;
+    struct TdBatch {
+        int64_t off;
+        int nl;
+        uint64_t active[8], derived[8];
+    };
+    std::vector<TdBatch> td_plan;
+    std::vector<int> td_lanes;
+    int streams_opt = 4;       // BC_OPT_STREAMS (S20: 1 / 2 / 3 pipelines = 332 / 319 / 316 ms per 8192 sources)
     SlicesWS sws;    // slices-mode workspace
     unsigned long long *d_stats = nullptr;  // [16] slices mode / trivial sources counters
     int *d_work_ctr = nullptr;              // [4]: -, slices source counter
@@ -432,6 +448,121 @@ bc_status cluster_sources(bc_graph *g, DevCSR &run, int ns, cudaStream_t st) {
     return BC_OK;
 }
 
+bc_status cluster_sources(bc_graph *g, DevCSR &run, int ns, cudaStream_t st);
+__global__ void two_nbr_kernel(const int *cand, int nc, const int *rp, const int *col, int *out);
+
+// NEXT-1 batch plan ("2-degree scheduling"): a source c of
+// degree 2 whose neighbours a, b are also sources, none of the three in
+// another triple (the paper's restriction: the adjacencies of a 2-degree
+// vertex are not adjacencies of another one), becomes a *derived* lane next
+// to a and b: lanes 3t, 3t+1, 3t+2 of a word (21 triples per word), so
+// lanes_derive_kernel maps a, b onto c with two shifts.  The remaining
+// sources fill the other lanes; batches follow the anchor-clustered order of
+// the traversed sources, a triple never straddles batches.
+bc_status plan_two_degree(bc_graph *g, DevCSR &run, const std::vector<int> &trav, int K, int W, cudaStream_t st,
+                          bc_stats &last) {
+    const int64_t n = g->n;
+    std::vector<int> cand;
+    for (int v : trav)
+        if (run.h_deg[v] == 2) cand.push_back(v);
+    const int64_t need = std::max<int64_t>((int64_t)cand.size() * 3, (int64_t)trav.size());
+    if (g->td_cap < need) {
+        dfree(g->td_buf);
+        CK(dalloc(&g->td_buf, (size_t)need));
+        g->td_cap = need;
+    }
+    std::vector<int> nb(2 * cand.size());
+    if (!cand.empty()) {
+        CU(cudaMemcpyAsync(g->td_buf, cand.data(), cand.size() * 4, cudaMemcpyHostToDevice, st));
+        two_nbr_kernel<<<(unsigned)((cand.size() + 255) / 256), 256, 0, st>>>(g->td_buf, (int)cand.size(), run.rp,
+                                                                              run.col, g->td_buf + cand.size());
+        CU(cudaMemcpyAsync(nb.data(), g->td_buf + cand.size(), nb.size() * 4, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+    }
+    std::vector<uint8_t> role((size_t)n, 0);  // 1 = source, 2 = a/b of a triple, 3 = derived c
+    for (int v : trav) role[v] = 1;
+    std::vector<int> tri_of((size_t)n, -1);
+    std::vector<int> tri;  // a, b, c
+    for (size_t i = 0; i < cand.size(); ++i) {
+        const int c = cand[i], a = nb[2 * i], b = nb[2 * i + 1];
+        if (a == b || role[c] != 1 || role[a] != 1 || role[b] != 1) continue;
+        role[a] = role[b] = 2;
+        role[c] = 3;
+        tri_of[a] = tri_of[b] = (int)(tri.size() / 3);
+        tri.push_back(a);
+        tri.push_back(b);
+        tri.push_back(c);
+    }
+    // traversed sources in anchor-clustered order
+    std::vector<int> reals;
+    for (int v : trav)
+        if (role[v] != 3) reals.push_back(v);
+    if (g->src_cap < (int64_t)reals.size()) {
+        dfree(g->d_src);
+        CK(dalloc(&g->d_src, reals.size()));
+        g->src_cap = (int64_t)reals.size();
+    }
+    CU(cudaMemcpyAsync(g->d_src, reals.data(), reals.size() * 4, cudaMemcpyHostToDevice, st));
+    if (g->src_order >= 2 && reals.size() > (size_t)K) {
+        CK(cluster_sources(g, run, (int)reals.size(), st));
+        CU(cudaMemcpyAsync(reals.data(), g->d_src, reals.size() * 4, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+    }
+    // pack items (single sources and triples) into batches
+    g->td_plan.clear();
+    g->td_lanes.clear();
+    const int TMAX = 21 * W;
+    std::vector<int> bt, bs;  // current batch: triple ids, singles
+    std::vector<uint8_t> emitted(tri.size() / 3, 0);
+    auto close = [&]() {
+        if (bt.empty() && bs.empty()) return;
+        bc_graph::TdBatch b{};
+        b.off = (int64_t)g->td_lanes.size();
+        std::vector<int> lanes(K, -1);
+        for (size_t t = 0; t < bt.size(); ++t) {
+            const int base = 64 * (int)(t / 21) + 3 * (int)(t % 21);
+            for (int r = 0; r < 3; ++r) lanes[base + r] = tri[3 * bt[t] + r];
+            b.derived[base / 64] |= 1ull << ((base + 2) & 63);
+        }
+        size_t si = 0;
+        int nl = 0;
+        for (int l = 0; l < K; ++l) {
+            if (lanes[l] < 0 && si < bs.size()) lanes[l] = bs[si++];
+            if (lanes[l] >= 0) nl = l + 1;
+        }
+        for (int l = 0; l < nl; ++l)
+            if (lanes[l] >= 0 && !(b.derived[l >> 6] >> (l & 63) & 1ull)) b.active[l >> 6] |= 1ull << (l & 63);
+        b.nl = nl;
+        g->td_lanes.insert(g->td_lanes.end(), lanes.begin(), lanes.begin() + nl);
+        g->td_plan.push_back(b);
+        bt.clear();
+        bs.clear();
+    };
+    for (int v : reals) {
+        if (role[v] == 2) {
+            const int t = tri_of[v];
+            if (emitted[t]) continue;
+            if ((int)bt.size() + 1 > TMAX || 3 * ((int)bt.size() + 1) + (int)bs.size() > K) close();
+            emitted[t] = 1;
+            bt.push_back(t);
+        } else {
+            if (3 * (int)bt.size() + (int)bs.size() + 1 > K) close();
+            bs.push_back(v);
+        }
+    }
+    close();
+    last.derived_lanes = (int64_t)(tri.size() / 3);
+    const int64_t tot = (int64_t)g->td_lanes.size();
+    if (g->src_cap < tot) {
+        dfree(g->d_src);
+        CK(dalloc(&g->d_src, (size_t)tot));
+        g->src_cap = tot;
+    }
+    CU(cudaMemcpyAsync(g->d_src, g->td_lanes.data(), (size_t)tot * 4, cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));  // td_lanes is pageable host memory
+    return BC_OK;
+}
+
 bc_status ensure_flags(bc_graph *g, LaneCtx &x, int need) {
     if (x.flag_cap >= need) return BC_OK;
     // sized for the deepest possible BFS (n levels) on first use: the buffer
@@ -499,6 +630,7 @@ bc_status ensure_level(bc_graph *g, LaneWS &ws, int L) {
         CK(dalloc(&c, (size_t)g->n * ws.W * LCH));
         ws.chunks.push_back(c);
     }
+    const int had = (int)ws.slev.size();
     while ((int)ws.slev.size() <= L) {
         double *q = nullptr;
         bc_status st = dalloc(&q, (size_t)g->n * 64 * ws.W);
@@ -507,12 +639,27 @@ bc_status ensure_level(bc_graph *g, LaneWS &ws, int L) {
                         (int)ws.slev.size(), (double)g->n * 512.0 * ws.W / 1e9, g_err.c_str());
         ws.slev.push_back(q);
     }
+    if ((int)ws.slev.size() != had || ws.dptr_cap < (int)ws.slev.size()) {
+        // pointer tables for lanes_derive_kernel (grow-only; rare, synchronous)
+        const int cap = (int)ws.slev.size();
+        if (ws.dptr_cap < cap) {
+            dfree(ws.d_lv);
+            dfree(ws.d_rows);
+            CK(dalloc(&ws.d_lv, (size_t)cap + 8));
+            CK(dalloc(&ws.d_rows, (size_t)cap + 8));
+            ws.dptr_cap = cap;
+        }
+        std::vector<uint64_t *> lv(cap);
+        for (int l = 0; l < cap; ++l) lv[l] = level_ptr(g, ws, l);
+        CU(cudaMemcpy(ws.d_lv, lv.data(), (size_t)cap * sizeof(void *), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(ws.d_rows, ws.slev.data(), (size_t)cap * sizeof(void *), cudaMemcpyHostToDevice));
+    }
     return BC_OK;
 }
 
 __global__ void lane_setup_kernel(const int *src, int nl, int K, const uint32_t *omega, double *w1) {
     int l = blockIdx.x * blockDim.x + threadIdx.x;
-    if (l < K) w1[l] = (l < nl && omega) ? 1.0 + (double)omega[src[l]] : 1.0;
+    if (l < K) w1[l] = (l < nl && omega && src[l] >= 0) ? 1.0 + (double)omega[src[l]] : 1.0;
 }
 
 // occupancy-derived grid for the level kernels
@@ -539,6 +686,9 @@ struct BatchCtx {
     std::vector<uint64_t *> *lvl_out;  // verification: level masks used (nullable)
     int *levels_out;
     bool *narrow_failed;    // narrow forward: set when some sigma > 65535 (nothing committed)
+    bool layout;            // 2-degree layout: lanes with src < 0 are unused, derived lanes below
+    uint64_t active[8];     // ... lanes traversed by the forward (layout only)
+    uint64_t derived[8];    // ... 2-degree lanes (tree derived after the forward)
 };
 
 // Run one batch (forward + backward) with K = 64*W lanes.
@@ -563,6 +713,12 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
     p.work_ctr = x.d_work_ctr;
     for (int j = 0; j < 8; ++j) p.active[j] = 0;
     for (int l = 0; l < c.nl; ++l) p.active[l >> 6] |= 1ull << (l & 63);
+    bool any_derived = false;
+    for (int j = 0; j < 8; ++j) {
+        p.derived[j] = c.layout ? c.derived[j] : 0;
+        if (c.layout) p.active[j] = c.active[j];
+        any_derived |= p.derived[j] != 0;
+    }
     p.hub_deg = g->hub_deg;
     p.nhub = c.csr->nhub;
     p.hub_ids = c.csr->hub_ids;
@@ -577,7 +733,8 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
     p.dbg_delta = nullptr;
     p.narrow_ovf = x.d_work_ctr + 2;  // fixed address (d_flags may grow and move with the level count)
     using RT = typename RowOf<SigT>::t;
-    constexpr bool NARROW = std::is_same<SigT, unsigned>::value;
+    // integer rows with a limit (16-bit or 32-bit): re-run the batch wider on overflow
+    constexpr bool NARROW = std::is_same<SigT, unsigned>::value || std::is_same<SigT, long long>::value;
     if (NARROW) CU(cudaMemsetAsync(p.narrow_ovf, 0, sizeof(int), st));
 
     const size_t mbytes = (size_t)n * W * sizeof(uint64_t);
@@ -690,6 +847,34 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
             return BC_OK;
         }
     }
+    int Lb = Lmax;  // deepest level of the backward sweep
+    if (any_derived && !std::is_same<SigT, unsigned long long>::value) {
+        // 2-degree lanes (NEXT-1): derive their trees from lanes a, b; they may
+        // reach one level deeper than the traversed lanes (levels <= Lmax + 1
+        // are allocated and their masks zeroed by the level loop)
+        CK(ensure_level(g, ws, Lmax + 1));
+        DeriveParams q{};
+        q.n = n;
+        q.nlev = Lmax + 1;
+        q.lvl = ws.d_lv;
+        q.rows = ws.d_rows;
+        q.rp = c.csr->rp;
+        for (int j = 0; j < 8; ++j) q.cmask[j] = p.derived[j];
+        q.stats = x.d_stats;
+        q.ovf = p.narrow_ovf;
+        lanes_derive_kernel<W, RT><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(q);
+        if (p.lane_ns) derive_ns_kernel<<<(K + 255) / 256, 256, 0, st>>>(K, q, ws.lane_ns);
+        x.last.kernel_launches += 1 + (p.lane_ns != nullptr);
+        if constexpr (NARROW) {
+            CU(cudaMemcpyAsync(x.h_flag + 1, p.narrow_ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CU(cudaStreamSynchronize(st));
+            if (x.h_flag[1]) {
+                if (c.narrow_failed) *c.narrow_failed = true;
+                return BC_OK;
+            }
+        }
+        Lb = Lmax + 1;
+    }
     if constexpr (!std::is_same<SigT, unsigned long long>::value) {
         bool pulled = false;
         if constexpr (std::is_same<SigT, double>::value) {
@@ -702,7 +887,7 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
             auto khb = lanes_hub_finalize<W, SigT, true>;
             cudaFuncSetAttribute(khb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
             p.dbg_delta = c.dbg_delta;
-            for (int l = Lmax; l >= 1; --l) {
+            for (int l = Lb; l >= 1; --l) {
                 p.level = l;
                 p.S_cur = ws.slev[l];
                 p.S_nxt = ws.slev[l + 1];
@@ -742,7 +927,7 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
             const unsigned fin_blocks = (unsigned)std::min<int64_t>(((int64_t)n * 32 + BC_NT - 1) / BC_NT,
                                                                     (int64_t)g->num_sms * 8);
             p.dbg_delta = c.dbg_delta;
-            for (int l = Lmax; l >= 1; --l) {
+            for (int l = Lb; l >= 1; --l) {
                 p.level = l;
                 p.S_cur = ws.slev[l];
                 p.S_nxt = nullptr;
@@ -889,6 +1074,15 @@ bool is_device_ptr(const void *p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+__global__ void two_nbr_kernel(const int *cand, int nc, const int *rp, const int *col, int *out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nc) {
+        const int e = rp[cand[i]];
+        out[2 * i] = col[e];
+        out[2 * i + 1] = col[e + 1];
+    }
+}
+
 __global__ void add_kernel(int n, const double *src, double *dst) {
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v < n) dst[v] += src[v];
@@ -945,6 +1139,7 @@ bc_status bc_destroy(bc_graph *g) {
         dfree(g->d_stats);
         dfree(g->d_work_ctr);
         dfree(g->d_src);
+        dfree(g->td_buf);
         dfree(g->d_bc);
         dfree(g->d_bc2);
         dfree(g->cl_kin);
@@ -1106,6 +1301,10 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
             if (value != 0 && value != 16 && value != 64) return fail(BC_ERR_INVALID, "sigma width must be 0, 16 or 64");
             g->sigma_width = (int)value;
             return BC_OK;
+        case BC_OPT_TWO_DEGREE:
+            if (value != 0 && value != 1) return fail(BC_ERR_INVALID, "two-degree must be 0 or 1");
+            g->two_degree = (int)value;
+            return BC_OK;
         case BC_OPT_STREAMS:
             if (value < 1 || value > MAX_STREAMS) return fail(BC_ERR_INVALID, "streams must be 1..%d", MAX_STREAMS);
             g->streams_opt = (int)value;
@@ -1230,8 +1429,7 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     g->last.lanes = K;
     // concurrent batch pipelines: bounded by the option, the batch count and
     // memory (each holds ~10 levels of rows plus the accumulators)
-    const int nbatch = (int)((trav.size() + K - 1) / K);
-    int NS = mode == 1 ? std::max(1, std::min(g->streams_opt, nbatch)) : 1;
+    int NS = mode == 1 ? std::max(1, g->streams_opt) : 1;
     if (NS > 1) {
         size_t free_b = 0, total_b = 0;
         if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
@@ -1240,11 +1438,6 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
         }
         (void)cudaGetLastError();
     }
-    if (mode == 1)
-        for (int i = 0; i < NS; ++i) {
-            CK(ctx_init(g, g->ctx[i]));
-            CK(ensure_ws(g, g->ctx[i].ws, W, false, std::max(run.nhub, g->orig.nhub)));
-        }
     const int64_t need = (int64_t)(trav.size() + triv.size());
     if (g->src_cap < need) {
         dfree(g->d_src);
@@ -1257,17 +1450,63 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
         cudaEventCreate(&t1);
         cudaEventRecord(t0, st);
     }
-    if (!trav.empty()) {
+    // batch plan: consecutive K-lane slices of the (clustered) source list, or
+    // with the 2-degree heuristic an explicit lane layout per batch
+    struct Plan {
+        int64_t off;
+        int nl;
+        bool layout;
+        uint64_t active[8], derived[8];
+    };
+    std::vector<Plan> plan;
+    int64_t nlanes = (int64_t)trav.size();  // entries of d_src used by the batches
+    if (mode == 1 && g->two_degree && !trav.empty()) {
+        CK(plan_two_degree(g, run, trav, K, W, st, g->last));
+        nlanes = (int64_t)g->td_lanes.size();
+        for (auto &b : g->td_plan) {
+            Plan q{};
+            q.off = b.off;
+            q.nl = b.nl;
+            q.layout = true;
+            for (int j = 0; j < 8; ++j) {
+                q.active[j] = b.active[j];
+                q.derived[j] = b.derived[j];
+            }
+            plan.push_back(q);
+        }
+    } else if (!trav.empty()) {
         CU(cudaMemcpyAsync(g->d_src, trav.data(), trav.size() * 4, cudaMemcpyHostToDevice, st));
         if (mode == 1 && g->src_order >= 2 && trav.size() > (size_t)K) CK(cluster_sources(g, run, (int)trav.size(), st));
+        for (size_t off = 0; mode == 1 && off < trav.size(); off += K) {
+            Plan q{};
+            q.off = (int64_t)off;
+            q.nl = (int)std::min<size_t>(K, trav.size() - off);
+            plan.push_back(q);
+        }
     }
-    if (!triv.empty())
-        CU(cudaMemcpyAsync(g->d_src + trav.size(), triv.data(), triv.size() * 4, cudaMemcpyHostToDevice, st));
+    if (!triv.empty()) {
+        if (g->src_cap < nlanes + (int64_t)triv.size()) {
+            // grow, keeping the batch lanes (stream-ordered copy through a new buffer)
+            int *nbuf = nullptr;
+            CK(dalloc(&nbuf, (size_t)(nlanes + (int64_t)triv.size())));
+            if (nlanes) CU(cudaMemcpyAsync(nbuf, g->d_src, (size_t)nlanes * 4, cudaMemcpyDeviceToDevice, st));
+            CU(cudaStreamSynchronize(st));
+            dfree(g->d_src);
+            g->d_src = nbuf;
+            g->src_cap = nlanes + (int64_t)triv.size();
+        }
+        CU(cudaMemcpyAsync(g->d_src + nlanes, triv.data(), triv.size() * 4, cudaMemcpyHostToDevice, st));
+    }
     CU(cudaMemsetAsync(g->d_bc, 0, (size_t)n * 8, st));
     CU(cudaMemsetAsync(g->d_stats, 0, 8 * sizeof(unsigned long long), st));
     std::vector<cudaEvent_t> ef;
     if (mode == 2 && !trav.empty()) CK(run_slices(g, run, g->d_src, (int)trav.size(), st, g->profile ? &ef : nullptr));
     if (mode == 1 && !trav.empty()) {
+        NS = std::max(1, std::min(NS, (int)plan.size()));
+        for (int i = 0; i < NS; ++i) {
+            CK(ctx_init(g, g->ctx[i]));
+            CK(ensure_ws(g, g->ctx[i].ws, W, false, std::max(run.nhub, g->orig.nhub)));
+        }
         // pipeline i runs batches i, i + NS, ...; pipeline 0 adds into d_bc,
         // the others into private partials summed at the end
         cudaEvent_t start = nullptr;
@@ -1294,12 +1533,18 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
                     x.d_bc = x.own_bc;
                     CU(cudaMemsetAsync(x.d_bc, 0, (size_t)n * 8, xs));
                 }
-                for (size_t off = (size_t)i * K; off < trav.size(); off += (size_t)NS * K) {
+                for (size_t bi = (size_t)i; bi < plan.size(); bi += (size_t)NS) {
+                    const Plan &pb = plan[bi];
                     BatchCtx c{};
                     c.csr = &run;
                     c.omega = g->pruned ? run.omega : nullptr;
-                    c.src = g->d_src + off;
-                    c.nl = (int)std::min<size_t>(K, trav.size() - off);
+                    c.src = g->d_src + pb.off;
+                    c.nl = pb.nl;
+                    c.layout = pb.layout;
+                    for (int j = 0; j < 8; ++j) {
+                        c.active[j] = pb.active[j];
+                        c.derived[j] = pb.derived[j];
+                    }
                     c.st = xs;
                     c.run_backward = true;
                     c.endpoint = true;
@@ -1312,6 +1557,7 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
                     auto *pef = g->profile ? &x.ef : nullptr;
                     auto *peb = g->profile ? &x.eb : nullptr;
                     if (narrow) {
+                        // 16-bit rows, then 32-bit rows, then fp64
                         bool failed = false;
                         c.narrow_failed = &failed;
                         const int64_t lv = x.last.levels_total;
@@ -1326,6 +1572,15 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
                                            cudaMemcpyDeviceToDevice, xs));
                         x.last.levels_total = lv;
                         x.last.narrow_fallbacks += 1;
+                        failed = false;
+                        CK(run_batch_w<long long>(g, x, W, c, pef, peb));
+                        if (!failed) {
+                            x.last.mid_batches += 1;
+                            continue;
+                        }
+                        CU(cudaMemcpyAsync(x.d_stats, x.d_stats + 8, 8 * sizeof(unsigned long long),
+                                           cudaMemcpyDeviceToDevice, xs));
+                        x.last.levels_total = lv;
                         c.narrow_failed = nullptr;
                     }
                     CK(run_batch_w<double>(g, x, W, c, pef, peb));
@@ -1362,11 +1617,12 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
             g->last.kernel_launches += x.last.kernel_launches;
             g->last.narrow_batches += x.last.narrow_batches;
             g->last.narrow_fallbacks += x.last.narrow_fallbacks;
+            g->last.mid_batches += x.last.mid_batches;
         }
     }
     if (!triv.empty()) {
         trivial_sources_kernel<<<(unsigned)((triv.size() + 255) / 256), 256, 0, st>>>(
-            g->d_src + trav.size(), (int)triv.size(), run.omega, g->d_bc);
+            g->d_src + nlanes, (int)triv.size(), run.omega, g->d_bc);
         g->last.kernel_launches += 1;
     }
     CU(cudaGetLastError());

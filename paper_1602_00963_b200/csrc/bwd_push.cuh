@@ -297,6 +297,7 @@ struct PushKernel {
                     double *arow = A + (size_t)y * K + lane;
                     uint64_t myword = 0;  // fwd: thread j < W ORs word j of c into lvl[L+1][y]
                     uint64_t cwords[W];
+                    static_assert(W <= 8, "");
 #pragma unroll
                     for (int j = 0; j < W; j += (W >= 2 ? 2 : 1)) {
                         if constexpr (W >= 2) {
@@ -306,6 +307,11 @@ struct PushKernel {
                         } else {
                             cwords[0] = sm.hc[wid * 32 + src];
                         }
+                    }
+                    if (!FWD && lane == 0) {
+                        // DAG edges of 2-degree lanes (their forward was derived, not traversed)
+#pragma unroll
+                        for (int j = 0; j < W; ++j) st_dag += __popcll(cwords[j] & p.derived[j]);
                     }
 #pragma unroll
                     for (int j = 0; j < NG; ++j) {

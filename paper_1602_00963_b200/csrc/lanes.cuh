@@ -49,6 +49,7 @@ template <typename T> struct Vec2;
 template <> struct Vec2<double> { using t = double2; };
 template <> struct Vec2<unsigned long long> { using t = ulonglong2; };
 template <> struct Vec2<unsigned> { using t = uint2; };
+template <> struct Vec2<long long> { using t = longlong2; };
 
 // Storage type of the level sigma rows for an accumulator type SigT.
 // SigT = unsigned is the *narrow* forward: sigma rows hold uint16 (4x fewer
@@ -57,9 +58,14 @@ template <> struct Vec2<unsigned> { using t = uint2; };
 // the host re-runs the batch with fp64 rows.  Integer sigma is exact, so
 // the narrow and fp64 forwards produce identical sigma wherever both fit
 // (R-MAT: max sigma ~1e4 at scale 20, SURVEY.md section 8 constants table).
+// SigT = long long is the *mid* tier: uint32 rows, 64-bit sums, limit
+// 2^32 - 1 (the fallback of a 16-bit batch before fp64).
 template <typename SigT> struct RowOf { using t = SigT; };
 template <> struct RowOf<unsigned> { using t = uint16_t; };
-constexpr unsigned NARROW_MAX = 65535u;
+template <> struct RowOf<long long> { using t = uint32_t; };
+template <typename SigT> struct RowLimit { static constexpr unsigned long long v = 0; };
+template <> struct RowLimit<unsigned> { static constexpr unsigned long long v = 65535ull; };
+template <> struct RowLimit<long long> { static constexpr unsigned long long v = 4294967295ull; };
 
 // 16-byte read-only load with an L2 cache policy
 __device__ __forceinline__ double2 ld_pol(const double2 *p, uint64_t pol) {
@@ -176,6 +182,7 @@ struct LanesParams {
     const int *tile_vs;          // [ntiles+1] tile t = vertices [tile_vs[t], tile_vs[t+1]), <= TV of them
     double *dbg_delta;           // backward: delta of lane 0 (verification), nullable
     int *narrow_ovf;             // narrow forward: set when some sigma > 65535 (batch is re-run in fp64)
+    uint64_t derived[8];         // 2-degree lanes (NEXT-1): tree derived from lanes l-2, l-1 after the forward
     const int *prev_new;         // forward: flag "level L is non-empty"; 0 -> the launch is a no-op
                                  // (levels are launched one ahead of the host's termination test)
     void *part;                  // [gridDim][BC_NW][2][K] SigT: partial sums of slots split across warps
@@ -251,6 +258,9 @@ struct LanesKernel {
     static constexpr int R = (W == 1) ? 4 : (W == 2 ? 2 : BC_R4);  // item steps in flight per warp (W >= 4: BC_R4)
     static constexpr bool VERIFY = std::is_same<SigT, unsigned long long>::value;
     static constexpr bool NARROW = std::is_same<SigT, unsigned>::value;
+    static constexpr bool MID = std::is_same<SigT, long long>::value;
+    static constexpr bool INTROW = NARROW || MID;  // integer rows with a limit (re-run when exceeded)
+    static constexpr unsigned long long LIMIT = RowLimit<SigT>::v;
     using RT = typename RowOf<SigT>::t;  // sigma row storage
     using V = typename Vec2<SigT>::t;
     using Smem = LanesSmem<W, SigT>;
@@ -318,6 +328,16 @@ struct LanesKernel {
             }
             return;
         }
+        if constexpr (MID) {
+#pragma unroll
+            for (int pr = 0; pr < W; ++pr) {
+                uint2 t;
+                t.x = (keep >> (2 * pr) & 1u) ? (uint32_t)v[2 * pr] : 0u;
+                t.y = (keep >> (2 * pr + 1) & 1u) ? (uint32_t)v[2 * pr + 1] : 0u;
+                *reinterpret_cast<uint2 *>(row + 64 * pr + t2) = t;
+            }
+            return;
+        }
 #pragma unroll
         for (int pr = 0; pr < W; ++pr) {
             V t;
@@ -338,10 +358,10 @@ struct LanesKernel {
         aovf &= ub;
         const bool any = __any_sync(0xffffffffu, nb != 0);
         if (!any) return;  // warp-uniform
-        if constexpr (NARROW) {
+        if constexpr (INTROW) {
             bool big = false;
 #pragma unroll
-            for (int i = 0; i < LPT; ++i) big |= (nb >> i & 1u) && acc[i] > NARROW_MAX;
+            for (int i = 0; i < LPT; ++i) big |= (nb >> i & 1u) && (unsigned long long)acc[i] > LIMIT;
             if (big) *p.narrow_ovf = 1;
         }
         store_slice(Snxt() + (size_t)x * K, nb, acc);
@@ -532,6 +552,19 @@ struct LanesKernel {
                         }
                         continue;
                     }
+                    if constexpr (MID) {
+                        // 32-bit rows: one 8-byte load per pair
+                        const uint2 *rowp = reinterpret_cast<const uint2 *>(Scur() + (size_t)sv.y * K + t2);
+#pragma unroll
+                        for (int pr = 0; pr < W; ++pr) {
+                            if (cw[pr] & (3u << sh)) {
+                                const uint2 t = __ldg(rowp + 32 * pr);
+                                acc[2 * pr] += t.x;
+                                acc[2 * pr + 1] += t.y;
+                            }
+                        }
+                        continue;
+                    }
                     const V *rowv = reinterpret_cast<const V *>((BWD ? Snxt() : Scur()) + (size_t)sv.y * K + t2);
                     if constexpr (!VERIFY) {
 #pragma unroll
@@ -704,10 +737,14 @@ struct LanesKernel {
             }
             // narrow: a segment partial above the limit already means overflow;
             // otherwise each add is <= 65535 and the hub row cannot wrap
-            if (NARROW && sum > NARROW_MAX) *p.narrow_ovf = 1;
+            if (INTROW && (unsigned long long)sum > LIMIT) *p.narrow_ovf = 1;
             if (sum != SigT(0)) {
                 SigT *dst = reinterpret_cast<SigT *>(p.hub_acc) + (size_t)h * K + l;
-                SigT old = atomicAdd(dst, sum);
+                SigT old;
+                if constexpr (MID)
+                    old = (SigT)atomicAdd(reinterpret_cast<unsigned long long *>(dst), (unsigned long long)sum);
+                else
+                    old = atomicAdd(dst, sum);
                 if (VERIFY && old + sum < old) ovf = true;
             }
             if (VERIFY && ovf) atomicOr((unsigned long long *)(p.hub_ovf + (size_t)h * W + (l >> 6)), 1ull << (l & 63));
@@ -816,12 +853,24 @@ __global__ void __launch_bounds__(BC_NT) lanes_init_kernel(LanesParams p, const 
     __shared__ unsigned long long red_u[BC_NW];
     const int l = blockIdx.x;
     const int s = src[l];
+    if (s < 0) return;  // unused lane of a 2-degree batch layout
     const int word = l >> 6;
     const uint64_t bit = 1ull << (l & 63);
     const int rs = p.rp[s], re = p.rp[s + 1];
     if (threadIdx.x == 0) {
         atomicOr((unsigned long long *)(mask0 + (size_t)s * W + word), (unsigned long long)bit);
         atomicOr((unsigned long long *)(p.seen + (size_t)s * W + word), (unsigned long long)bit);
+    }
+    if (p.derived[word] & bit) {
+        // 2-degree source (NEXT-1): only level 0 here; levels >= 1 come from
+        // lanes_derive_kernel after the forward.  Counters: the source itself
+        // and its two DAG edges to a and b.
+        if (threadIdx.x == 0) {
+            atomicAdd(p.stats + 0, 1ull);
+            atomicAdd(p.stats + 1, (unsigned long long)(re - rs));
+            atomicAdd(p.stats + 2, (unsigned long long)(re - rs));
+        }
+        return;
     }
     double cnt = 0.0;
     unsigned long long adj = 0;
@@ -854,6 +903,104 @@ __global__ void __launch_bounds__(BC_NT) lanes_init_kernel(LanesParams p, const 
         atomicAdd(p.stats + 3, (unsigned long long)deg);
         if (deg > 0) *p.any_new = 1;
     }
+}
+
+// NEXT-1, the 2-degree heuristic (Lemma 1, Eq.(6), Alg.7
+// with reading R23): a 2-degree source c whose neighbours a, b are lanes of
+// the same batch sits in lane 3t+2 of a word whose lanes 3t, 3t+1 hold a, b
+// (cmask = bits of such lanes).  After the forward sweep of the other lanes,
+// its tree is derived per vertex v without traversing the graph:
+//   lvl_c(v) = min(lvl_a(v), lvl_b(v)) + 1,  sigma_c(v) = sum of sigma_x(v)
+//   over x in {a, b} at that minimum (Eq.(6), equal levels: both).
+// Bit-parallel over the levels L = 0, 1, ...: a lane-c bit becomes set at
+// L+1 when the a- or b-bit (shifted onto the c position) is set at L and c
+// has no level yet; c's own vertex is at level 0 (set by the init kernel),
+// so Lemma 1's exception v = c needs no special case.  The backward sweep
+// then treats lane c like any other lane (the Dynamic Merging of Frontiers
+// of Alg.8-9 is what a lane-parallel backward does anyway).
+struct DeriveParams {
+    int n;
+    int nlev;                      // levels 0 .. nlev-1 hold the forward's vertices (nlev = Lmax + 1)
+    uint64_t *const *lvl;          // [nlev + 1] level masks (level nlev pre-zeroed)
+    void *const *rows;             // [nlev + 1] sigma rows (RT)
+    const int *rp;
+    uint64_t cmask[8];
+    unsigned long long *stats;
+    int *ovf;                      // integer rows: set when a derived sigma exceeds the row type
+};
+
+template <int W, typename RT>
+__global__ void __launch_bounds__(256) lanes_derive_kernel(DeriveParams q) {
+    constexpr int K = 64 * W;
+    constexpr unsigned long long LIMIT = std::is_same<RT, uint16_t>::value ? 65535ull
+                                       : (std::is_same<RT, uint32_t>::value ? 4294967295ull : 0ull);
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long st_reach = 0, st_adj = 0, st_dsum = 0;
+    if (v < q.n) {
+        const int deg = q.rp[v + 1] - q.rp[v];
+        uint64_t done[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) done[j] = 0;
+        bool big = false;
+        for (int L = 0; L < q.nlev; ++L) {
+            const uint64_t *ml = q.lvl[L] + (size_t)v * W;
+            const RT *rl = reinterpret_cast<const RT *>(q.rows[L]) + (size_t)v * K;
+            uint64_t *mn = q.lvl[L + 1] + (size_t)v * W;
+            RT *rn = reinterpret_cast<RT *>(q.rows[L + 1]) + (size_t)v * K;
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                const uint64_t cm = q.cmask[j];
+                if (!cm) continue;
+                const uint64_t M = ml[j];
+                done[j] |= M & cm;                   // c itself (level 0) / set earlier
+                const uint64_t ma = (M << 2) & cm, mb = (M << 1) & cm;
+                uint64_t nw = (ma | mb) & ~done[j];
+                if (!nw) continue;
+                done[j] |= nw;
+                mn[j] |= nw;
+                const int cnt = __popcll(nw);
+                st_reach += cnt;
+                st_adj += (unsigned long long)cnt * deg;
+                st_dsum += (unsigned long long)cnt * (L + 1);
+                while (nw) {
+                    const int b = __ffsll((long long)nw) - 1;
+                    nw &= nw - 1;
+                    const int lc = 64 * j + b;
+                    double sa = 0.0;
+                    unsigned long long ia = 0;
+                    if (ma >> b & 1ull) {
+                        sa += (double)rl[lc - 2];
+                        ia += (unsigned long long)rl[lc - 2];
+                    }
+                    if (mb >> b & 1ull) {
+                        sa += (double)rl[lc - 1];
+                        ia += (unsigned long long)rl[lc - 1];
+                    }
+                    if constexpr (LIMIT != 0) {
+                        big |= ia > LIMIT;
+                        rn[lc] = (RT)ia;
+                    } else {
+                        rn[lc] = (RT)sa;
+                    }
+                }
+            }
+        }
+        if (big) *q.ovf = 1;
+    }
+    st_reach = warp_sum_u64(st_reach);
+    st_adj = warp_sum_u64(st_adj);
+    st_dsum = warp_sum_u64(st_dsum);
+    if (lane_id() == 0 && st_reach) {
+        atomicAdd(q.stats + 0, st_reach);
+        atomicAdd(q.stats + 1, st_adj);
+        atomicAdd(q.stats + 3, st_dsum);
+    }
+}
+
+// n_s of a derived lane = n_s of its lane a (same component)
+__global__ void derive_ns_kernel(int K, DeriveParams q, double *lane_ns) {
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l < K && (q.cmask[l >> 6] >> (l & 63) & 1ull)) lane_ns[l] = lane_ns[l - 2];
 }
 
 // Rows of levels 0 and 1: sigma = 1 in the lanes of the level mask, 0 elsewhere
@@ -897,7 +1044,7 @@ __global__ void gather_level_lane0_kernel(int n, const uint64_t *mask, int W, co
 __global__ void lanes_endpoint_kernel(const int *src, int nlanes, const uint32_t *omega, const double *lane_ns,
                                       double *bc) {
     const int l = blockIdx.x * blockDim.x + threadIdx.x;
-    if (l < nlanes) {
+    if (l < nlanes && src[l] >= 0) {
         const int s = src[l];
         const double om = (double)omega[s];
         if (om != 0.0) bc[s] += om * (lane_ns[l] - 2.0);

@@ -358,12 +358,14 @@ def test_sigma_width_narrow_and_fp64_rows(width):
 
 
 @pytest.mark.parametrize("words", [1, 4, 8])
-def test_narrow_sigma_overflow_reruns_batch_in_fp64(words):
-    """sigma > 65535 in some lanes: those batches are re-run with fp64 rows,
-    the others stay narrow; BC, depth stats and the per-source counters
-    match the oracle either way."""
+@pytest.mark.parametrize("layers", [8, 12])
+def test_narrow_sigma_overflow_reruns_batch_wider(words, layers):
+    """sigma > 65535 in some lanes: those batches are re-run with 32-bit rows
+    (layers = 8: sigma <= 10^6) or, past 2^32, with fp64 rows (layers = 12:
+    sigma up to 10^10); the others stay 16-bit.  BC and the per-source
+    counters match the oracle either way."""
     bcb = _bcb()
-    big = layered(10, 8)  # sigma up to 10^6 from the end layers
+    big = layered(10, layers)
     g = gg.disjoint_union(big, gg.rmat(9, 8, seed=3))
     want, stats = oracle.bc(g, stats=True)
     with bcb.Graph.from_csr(g) as G:
@@ -374,10 +376,65 @@ def test_narrow_sigma_overflow_reruns_batch_in_fp64(words):
         st = G.stats()
     assert_bc_close(got, want)
     S = g.non_isolated()
-    assert st["reached"] == int(stats[S, 0].sum())  # counters restored across the re-run
+    assert st["reached"] == int(stats[S, 0].sum())  # counters restored across the re-runs
     assert st["adj_reached"] == int(stats[S, 1].sum())
     assert st["dag_edges"] == int(stats[S, 2].sum())
     assert st["narrow_fallbacks"] >= 1
+    if layers == 8:
+        assert st["mid_batches"] == st["narrow_fallbacks"]
+    else:
+        assert st["mid_batches"] < st["narrow_fallbacks"]
     if words == 1:
         assert st["narrow_batches"] >= 1
     assert st["narrow_batches"] + st["narrow_fallbacks"] == st["batches"]
+
+
+def _two_degree_graphs():
+    return SUITE[::2] + [gg.cycle(9), gg.cycle(64), gg.grid(12, 12), gg.rmat(12, 16, seed=1),
+                         gg.disjoint_union(gg.cycle(10), gg.grid(5, 7), gg.rmat(8, 4, seed=2))]
+
+
+@pytest.mark.parametrize("words", [1, 4, 8])
+def test_two_degree_heuristic_all_sources(words):
+    """NEXT-1: degree-2 sources whose neighbours are sources get their tree
+    derived (Lemma 1 / Eq.(6)) instead of traversed; BC and the per-source
+    counters (n_s, A_s, D_s) equal the oracle's."""
+    bcb = _bcb()
+    derived = 0
+    for g in _two_degree_graphs():
+        want, stats = oracle.bc(g, stats=True)
+        with bcb.Graph.from_csr(g) as G:
+            G.set_option(bcb.OPT_MODE, 1)
+            G.set_option(bcb.OPT_LANE_WORDS, words)
+            G.set_option(bcb.OPT_TWO_DEGREE, 1)
+            got = G.compute()
+            st = G.stats()
+        assert_bc_close(got, want)
+        derived += st["derived_lanes"]
+        S = g.non_isolated()  # isolated sources are not traversed (and add 0)
+        assert st["reached"] == int(stats[S, 0].sum())
+        assert st["adj_reached"] == int(stats[S, 1].sum())
+        assert st["dag_edges"] == int(stats[S, 2].sum())
+    assert derived > 100
+
+
+def test_two_degree_heuristic_partial_pruned_and_wide_sigma():
+    bcb = _bcb()
+    g = gg.rmat(11, 8, seed=6)
+    S = gg.sample_sources(g, 700, seed=3)
+    with bcb.Graph.from_csr(g) as G:
+        G.set_option(bcb.OPT_TWO_DEGREE, 1)
+        assert_bc_close(G.compute(S), oracle.bc(g, S))
+        assert G.stats()["derived_lanes"] > 0
+        G.prune_degree1()
+        assert_bc_close(G.compute(), oracle.bc(g))
+        assert G.stats()["derived_lanes"] > 0
+    # 40x40 grid in lanes mode: corners are degree 2, sigma reaches C(78, 39) > 2^64,
+    # so the 16- and 32-bit batches overflow and the derivation runs in fp64 too
+    g = gg.grid(40, 40)
+    with bcb.Graph.from_csr(g) as G:
+        G.set_option(bcb.OPT_MODE, 1)
+        G.set_option(bcb.OPT_TWO_DEGREE, 1)
+        assert_bc_close(G.compute(), oracle.bc(g))
+        st = G.stats()
+        assert st["derived_lanes"] > 0 and st["narrow_fallbacks"] > 0

@@ -24,7 +24,8 @@ ap.add_argument("--order", type=int, default=2)
 ap.add_argument("--fwd-push", type=int, default=0)
 ap.add_argument("--bwd", type=int, default=0)
 ap.add_argument("--sigma", type=int, default=0)
-ap.add_argument("--streams", type=int, default=2)
+ap.add_argument("--streams", type=int, default=4)
+ap.add_argument("--two-degree", type=int, default=0)
 ap.add_argument("--sort", default="none", choices=["none", "deg", "degasc"])
 a = ap.parse_args()
 g = gg.grid(a.grid, a.grid) if a.grid else gg.rmat(a.scale, a.ef, seed=1)
@@ -41,6 +42,7 @@ G.set_option(bcb.OPT_FWD_PUSH, a.fwd_push)
 G.set_option(bcb.OPT_BWD_MODE, a.bwd)
 G.set_option(bcb.OPT_SIGMA_WIDTH, a.sigma)
 G.set_option(bcb.OPT_STREAMS, a.streams)
+G.set_option(bcb.OPT_TWO_DEGREE, a.two_degree)
 if a.sort != "none":
     d = g.degrees[S]
     S = S[np.argsort(-d if a.sort == "deg" else d, kind="stable")]
@@ -56,4 +58,4 @@ for r in range(a.repeat):
           f"levels={st['levels_total']} launches={st['kernel_launches']} TEPS={len(S)*g.m/dt/1e9:.1f}G "
           f"A={st['adj_reached']} D={st['dag_edges']} N={st['reached']} fi={st['fwd_items']} fh={st['fwd_hits']} "
           f"bi={st['bwd_items']} bh={st['bwd_hits']} narrow={st['narrow_batches']} fallback={st['narrow_fallbacks']} "
-          f"push={st['bwd_push_ms']:.2f}ms")
+          f"push={st['bwd_push_ms']:.2f}ms derived={st['derived_lanes']}")
