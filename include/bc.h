@@ -143,7 +143,8 @@ typedef enum {
                                sigma exceeds 65535 is re-run with uint32 rows, then (sigma >= 2^32)
                                with fp64 rows; 64 = fp64 rows only.
                                sigma is an integer (Alg.1 line 20), so both are exact */,
-    BC_OPT_STREAMS = 10,    /* lanes mode: concurrent batch pipelines, 1..8 (default 4; fewer if HBM is short).
+    BC_OPT_STREAMS = 10,    /* lanes mode: concurrent batch pipelines, 0 = auto (8 for n <= 2^18, else 3;
+                               fewer if HBM is short), or 1..8.
                                Batches are independent (BC is additive over sources) */
     BC_OPT_TWO_DEGREE = 11  /* lanes mode: 1 = 2-degree heuristic: a degree-2 source
                                whose two neighbours are also sources gets its shortest-path tree derived

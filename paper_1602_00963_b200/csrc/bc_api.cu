@@ -242,7 +242,7 @@ struct bc_graph {
     };
     std::vector<TdBatch> td_plan;
     std::vector<int> td_lanes;
-    int streams_opt = 4;       // BC_OPT_STREAMS (S20: 1 / 2 / 3 pipelines = 332 / 319 / 316 ms per 8192 sources)
+    int streams_opt = 0;       // 0 = auto: 8 pipelines for n <= 2^18 (launch/sync-bound batches), else 3       // BC_OPT_STREAMS (S20: 1 / 2 / 3 pipelines = 332 / 319 / 316 ms per 8192 sources)
     SlicesWS sws;    // slices-mode workspace
     unsigned long long *d_stats = nullptr;  // [16] slices mode / trivial sources counters
     int *d_work_ctr = nullptr;              // [4]: -, slices source counter
@@ -1306,7 +1306,7 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
             g->two_degree = (int)value;
             return BC_OK;
         case BC_OPT_STREAMS:
-            if (value < 1 || value > MAX_STREAMS) return fail(BC_ERR_INVALID, "streams must be 1..%d", MAX_STREAMS);
+            if (value < 0 || value > MAX_STREAMS) return fail(BC_ERR_INVALID, "streams must be 0 (auto) .. %d", MAX_STREAMS);
             g->streams_opt = (int)value;
             return BC_OK;
         case BC_OPT_SOURCE_ORDER:
@@ -1429,7 +1429,10 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     g->last.lanes = K;
     // concurrent batch pipelines: bounded by the option, the batch count and
     // memory (each holds ~10 levels of rows plus the accumulators)
-    int NS = mode == 1 ? std::max(1, g->streams_opt) : 1;
+    // measured (tools/small_probe.py, prof_batch): S12 1/4/8 pipelines 21.5/6.2/4.0 ms,
+    // S16 352/114/110 ms, S20 332/316 (3)/332 (4) ms
+    const int ns_auto = g->n <= (1 << 18) ? 8 : 3;
+    int NS = mode == 1 ? (g->streams_opt > 0 ? g->streams_opt : ns_auto) : 1;
     if (NS > 1) {
         size_t free_b = 0, total_b = 0;
         if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {

@@ -24,7 +24,7 @@ ap.add_argument("--order", type=int, default=2)
 ap.add_argument("--fwd-push", type=int, default=0)
 ap.add_argument("--bwd", type=int, default=0)
 ap.add_argument("--sigma", type=int, default=0)
-ap.add_argument("--streams", type=int, default=4)
+ap.add_argument("--streams", type=int, default=0)
 ap.add_argument("--two-degree", type=int, default=0)
 ap.add_argument("--sort", default="none", choices=["none", "deg", "degasc"])
 a = ap.parse_args()
