@@ -83,6 +83,8 @@ def peaks():
 
 
 def clocks_sampler_start(idx):
+    if os.environ.get("BC_BENCH_NO_CLOCKS"):  # diagnosis only: the line then carries no clocks
+        return None, None, ""
     try:
         f = open(os.path.join(ROOT, "gpurun_out", f"clocks_rank{idx}.csv") if os.path.isdir(
             os.path.join(ROOT, "gpurun_out")) else os.devnull, "w")
@@ -90,14 +92,18 @@ def clocks_sampler_start(idx):
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         p = subprocess.Popen(["nvidia-smi", "-i", str(idx), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                              "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        return p, f
+                              "-lms", "500"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        # wait for the first sample: nvidia-smi's start-up (NVML init, driver
+        # locks) must not overlap the timed region -- it stalls CUDA launches
+        first = p.stdout.readline()
+        return p, f, first
     except Exception:
-        return None, None
+        return None, None, ""
+
 
 
 def clocks_sampler_stop(h):
-    p, f = h
+    p, f, first = h
     if p is None:
         return None
     p.terminate()
@@ -106,6 +112,7 @@ def clocks_sampler_stop(h):
     except Exception:
         p.kill()
         out = ""
+    out = first + out
     if f:
         f.write(out)
         f.close()
@@ -133,7 +140,9 @@ def cpu_baseline(g, sources, budget_s=15.0):
     """The oracle as it stands, on this host's cores, on a bounded sample."""
     import oracle
 
-    cores = oracle.num_threads()
+    # every core this process may run on (torchrun sets OMP_NUM_THREADS=1 per
+    # rank; the oracle leg runs on rank 0 alone and gets the whole host)
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else oracle.num_threads()
     rng = np.random.default_rng(7)
     pool = rng.permutation(sources)
     first = pool[:cores]
@@ -161,7 +170,9 @@ def run_reference(args, cfg):
 
     g = make_graph(cfg)
     S = source_list(g, cfg)
-    cores = oracle.num_threads()
+    # every core this process may run on (torchrun sets OMP_NUM_THREADS=1 per
+    # rank; the oracle leg runs on rank 0 alone and gets the whole host)
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else oracle.num_threads()
     # bounded sample per step: one source per core (whole run stays within minutes)
     per_step = cores if cfg not in ("rmat12",) else min(len(S), 16 * cores)
     rng = np.random.default_rng(11)

@@ -112,6 +112,7 @@ struct DevCSR {
 struct LaneWS {
     int W = 0;
     bool verify = false;
+    int row_bytes = 8;  // bytes per lane of the level sigma rows: 4 holds the 16- and 32-bit tiers
     std::vector<void *> slev;  // per-level sigma/coef rows, n*K 8-byte values each
     uint64_t *seen = nullptr;
     uint64_t *ovf = nullptr;
@@ -589,11 +590,29 @@ bc_status ctx_init(bc_graph *g, LaneCtx &x) {
     return BC_OK;
 }
 
-bc_status ensure_ws(bc_graph *g, LaneWS &ws, int W, bool verify, int nhub) {
+// fp64 rows on a workspace sized for integer rows: drop the level rows, they
+// are re-allocated at 8 bytes per lane by ensure_level (rare: sigma >= 2^32)
+bc_status widen_rows(bc_graph *g, LaneWS &ws) {
+    if (ws.row_bytes >= 8) return BC_OK;
+    CU(cudaDeviceSynchronize());
+    for (auto &q : ws.slev) dfree(q);
+    ws.slev.clear();
+    ws.row_bytes = 8;
+    return BC_OK;
+}
+
+bc_status ensure_ws(bc_graph *g, LaneWS &ws, int W, bool verify, int nhub, int row_bytes = 8) {
     const size_t n = (size_t)g->n;
     const int K = 64 * W;
+    if (ws.W == W && ws.verify == verify && ws.row_bytes != row_bytes) {
+        CU(cudaDeviceSynchronize());
+        for (auto &q : ws.slev) dfree(q);
+        ws.slev.clear();
+        ws.row_bytes = row_bytes;
+    }
     if (ws.W != W || ws.verify != verify) {
         ws.release();
+        ws.row_bytes = row_bytes;
         CK(dalloc(&ws.seen, n * W));
         if (verify) CK(dalloc(&ws.ovf, n * W));
         CK(dalloc(&ws.lane_w1, K));
@@ -633,10 +652,10 @@ bc_status ensure_level(bc_graph *g, LaneWS &ws, int L) {
     const int had = (int)ws.slev.size();
     while ((int)ws.slev.size() <= L) {
         double *q = nullptr;
-        bc_status st = dalloc(&q, (size_t)g->n * 64 * ws.W);
+        bc_status st = dalloc(&q, (size_t)g->n * 8 * ws.W * ws.row_bytes);  // n * K * row_bytes bytes
         if (st != BC_OK)
             return fail(st, "cannot allocate level-%d sigma rows (%.1f GB per level; lower BC_OPT_LANE_WORDS): %s",
-                        (int)ws.slev.size(), (double)g->n * 512.0 * ws.W / 1e9, g_err.c_str());
+                        (int)ws.slev.size(), (double)g->n * 64.0 * ws.W * ws.row_bytes / 1e9, g_err.c_str());
         ws.slev.push_back(q);
     }
     if ((int)ws.slev.size() != had || ws.dptr_cap < (int)ws.slev.size()) {
@@ -1409,6 +1428,9 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     // diameter); auto picks slices for large sparse graphs (mean degree < 6)
     int mode = g->mode;
     if (mode == 0) mode = (g->n > 65536 && (double)run.nnz / (double)g->n < 6.0) ? 2 : 1;
+    // level-row width: 4 bytes per lane (the 16- and 32-bit sigma tiers) unless
+    // fp64 rows are requested; a batch that needs fp64 widens them (widen_rows)
+    const int rb = g->sigma_width == 64 || g->bwd_mode == 2 || g->fwd_push_levels > 0 ? 8 : 4;
     int W = g->lane_words_opt;
     if (W == 0) {
         W = trav.size() > 128 ? 4 : (trav.size() > 64 ? 2 : 1);
@@ -1416,12 +1438,15 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
         // thread carries: faster only where per-batch overhead dominates
         // (S16: 74 -> 60 ms per 16384 sources; S20: 319 -> 362 ms)
         if (trav.size() > 256 && g->n <= (1 << 18)) W = 8;
-        // level rows cost n*512*W bytes per BFS level: keep ~10 levels within
-        // half of the free HBM (S23 -> W = 2)
+        // level rows cost n*64*W*row_bytes per BFS level, the accumulators
+        // n*512*W: keep ~10 levels plus the accumulators within half of the
+        // free HBM (S23 at 4-byte rows -> W = 4)
         size_t free_b = 0, total_b = 0;
         if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-            for (auto &x : g->ctx) free_b += (size_t)x.ws.slev.size() * (size_t)g->n * 512 * (size_t)x.ws.W;  // reusable
-            while (W > 1 && (double)10 * g->n * 512.0 * W > 0.5 * (double)free_b) W >>= 1;
+            for (auto &x : g->ctx)
+                free_b += (size_t)x.ws.slev.size() * (size_t)g->n * 64 * (size_t)x.ws.W * (size_t)x.ws.row_bytes +
+                          (x.ws.A ? (size_t)g->n * 512 * (size_t)x.ws.W : 0);  // reusable
+            while (W > 1 && (double)g->n * 64.0 * W * (10.0 * rb + 8.0) > 0.5 * (double)free_b) W >>= 1;
         }
         (void)cudaGetLastError();
     }
@@ -1436,8 +1461,10 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     if (NS > 1) {
         size_t free_b = 0, total_b = 0;
         if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-            for (auto &x : g->ctx) free_b += (size_t)x.ws.slev.size() * (size_t)g->n * 512 * (size_t)x.ws.W;
-            while (NS > 1 && (double)NS * 11 * g->n * 512.0 * W > 0.6 * (double)free_b) --NS;
+            for (auto &x : g->ctx)
+                free_b += (size_t)x.ws.slev.size() * (size_t)g->n * 64 * (size_t)x.ws.W * (size_t)x.ws.row_bytes +
+                          (x.ws.A ? (size_t)g->n * 512 * (size_t)x.ws.W : 0);
+            while (NS > 1 && (double)NS * g->n * 64.0 * W * (11.0 * rb + 8.0) > 0.6 * (double)free_b) --NS;
         }
         (void)cudaGetLastError();
     }
@@ -1508,7 +1535,7 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
         NS = std::max(1, std::min(NS, (int)plan.size()));
         for (int i = 0; i < NS; ++i) {
             CK(ctx_init(g, g->ctx[i]));
-            CK(ensure_ws(g, g->ctx[i].ws, W, false, std::max(run.nhub, g->orig.nhub)));
+            CK(ensure_ws(g, g->ctx[i].ws, W, false, std::max(run.nhub, g->orig.nhub), rb));
         }
         // pipeline i runs batches i, i + NS, ...; pipeline 0 adds into d_bc,
         // the others into private partials summed at the end
@@ -1586,6 +1613,7 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
                         x.last.levels_total = lv;
                         c.narrow_failed = nullptr;
                     }
+                    CK(widen_rows(g, x.ws));
                     CK(run_batch_w<double>(g, x, W, c, pef, peb));
                 }
                 CU(cudaEventRecord(x.done, xs));
