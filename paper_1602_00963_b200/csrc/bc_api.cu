@@ -1439,14 +1439,14 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
         // (S16: 74 -> 60 ms per 16384 sources; S20: 319 -> 362 ms)
         if (trav.size() > 256 && g->n <= (1 << 18)) W = 8;
         // level rows cost n*64*W*row_bytes per BFS level, the accumulators
-        // n*512*W: keep ~10 levels plus the accumulators within half of the
-        // free HBM (S23 at 4-byte rows -> W = 4)
+        // n*512*W: keep ~9 levels plus the accumulators within 60 % of the
+        // free HBM (S23 at 4-byte rows -> W = 4; R-MAT depth <= ~9)
         size_t free_b = 0, total_b = 0;
         if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
             for (auto &x : g->ctx)
                 free_b += (size_t)x.ws.slev.size() * (size_t)g->n * 64 * (size_t)x.ws.W * (size_t)x.ws.row_bytes +
                           (x.ws.A ? (size_t)g->n * 512 * (size_t)x.ws.W : 0);  // reusable
-            while (W > 1 && (double)g->n * 64.0 * W * (10.0 * rb + 8.0) > 0.5 * (double)free_b) W >>= 1;
+            while (W > 1 && (double)g->n * 64.0 * W * (9.0 * rb + 8.0) > 0.6 * (double)free_b) W >>= 1;
         }
         (void)cudaGetLastError();
     }

@@ -230,6 +230,9 @@ struct PushKernel {
 
     __device__ void warp_push(int nslots, int ws, int we, bool hub_mode) {
         const uint64_t *mpar = FWD ? p.seen : p.mask_nxt_ro;  // fwd: seen[y]; bwd: lvl[L-1] (parents)
+        bool has_derived = false;
+#pragma unroll
+        for (int j = 0; j < W; ++j) has_derived |= p.derived[j] != 0;
         const double *S = reinterpret_cast<const double *>(p.S_cur);
         const uint64_t pol = policy_evict_first();
         int cur = -1;
@@ -308,10 +311,12 @@ struct PushKernel {
                             cwords[0] = sm.hc[wid * 32 + src];
                         }
                     }
-                    if (!FWD && lane == 0) {
+                    if (!FWD && has_derived) {  // uniform; only with BC_OPT_TWO_DEGREE
                         // DAG edges of 2-degree lanes (their forward was derived, not traversed)
+                        if (lane == 0) {
 #pragma unroll
-                        for (int j = 0; j < W; ++j) st_dag += __popcll(cwords[j] & p.derived[j]);
+                            for (int j = 0; j < W; ++j) st_dag += __popcll(cwords[j] & p.derived[j]);
+                        }
                     }
 #pragma unroll
                     for (int j = 0; j < NG; ++j) {
