@@ -766,7 +766,7 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
     p.any_new = x.d_flags + 1;
     lanes_init_kernel<W, SigT><<<c.nl, BC_NT, 0, st>>>(p, c.src, level_ptr(g, ws, 0), level_ptr(g, ws, 1));
     {
-        const unsigned mb = (unsigned)(((int64_t)n * 32 + 255) / 256);
+        const unsigned mb = (unsigned)(((int64_t)n + 255) / 256);  // thread per vertex
         lanes_materialize_kernel<W, RT><<<mb, 256, 0, st>>>(n, level_ptr(g, ws, 0), (RT *)ws.slev[0]);
         lanes_materialize_kernel<W, RT><<<mb, 256, 0, st>>>(n, level_ptr(g, ws, 1), (RT *)ws.slev[1]);
     }
@@ -1627,7 +1627,13 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
             worker(0);
         } else {
             std::vector<std::thread> th;
-            for (int i = 0; i < NS; ++i) th.emplace_back(worker, i);
+            try {
+                for (int i = 0; i < NS; ++i) th.emplace_back(worker, i);
+            } catch (...) {  // no exception may cross the C ABI
+                for (auto &t : th) t.join();
+                if (start) cudaEventDestroy(start);
+                return fail(BC_ERR_INTERNAL, "cannot start %d pipeline threads", NS);
+            }
             for (auto &t : th) t.join();
         }
         if (start) cudaEventDestroy(start);

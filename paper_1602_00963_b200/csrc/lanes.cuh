@@ -1007,26 +1007,29 @@ __global__ void derive_ns_kernel(int K, DeriveParams q, double *lane_ns) {
 // (warp per vertex; vertices outside the level skip).
 template <int W, typename SigT>
 __global__ void lanes_materialize_kernel(int n, const uint64_t *mask, SigT *S) {
+    // thread per vertex finds the vertices of the level, then the warp
+    // writes each of their rows (most vertices are at neither level)
     constexpr int K = 64 * W, LPT = 2 * W;
-    const int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (v >= n) return;
+    const int base = (int)(((size_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(size_t)31);
     const int lane = lane_id();
-    uint64_t m[W];
-    bool any = false;
+    bool mine = false;
+    if (base + lane < n) {
 #pragma unroll
-    for (int j = 0; j < W; ++j) {
-        m[j] = mask[(size_t)v * W + j];
-        any |= m[j] != 0;
+        for (int j = 0; j < W; ++j) mine |= mask[(size_t)(base + lane) * W + j] != 0;
     }
-    if (!any) return;
+    unsigned todo = __ballot_sync(0xffffffffu, mine);
     const int word = (lane * LPT) >> 6, off = (lane * LPT) & 63;
-    uint64_t mw = 0;
+    while (todo) {
+        const int v = base + __ffs(todo) - 1;
+        todo &= todo - 1;
+        uint64_t mw = 0;
 #pragma unroll
-    for (int j = 0; j < W; ++j)
-        if (j == word) mw = m[j];
-    SigT *row = S + (size_t)v * K + lane * LPT;
+        for (int j = 0; j < W; ++j)
+            if (j == word) mw = mask[(size_t)v * W + j];
+        SigT *row = S + (size_t)v * K + lane * LPT;
 #pragma unroll
-    for (int i = 0; i < LPT; ++i) row[i] = (mw >> (off + i) & 1ull) ? SigT(1) : SigT(0);
+        for (int i = 0; i < LPT; ++i) row[i] = (mw >> (off + i) & 1ull) ? SigT(1) : SigT(0);
+    }
 }
 
 // verification: sigma of lane 0 for the vertices at level L

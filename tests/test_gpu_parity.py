@@ -438,3 +438,18 @@ def test_two_degree_heuristic_partial_pruned_and_wide_sigma():
         assert_bc_close(G.compute(), oracle.bc(g))
         st = G.stats()
         assert st["derived_lanes"] > 0 and st["narrow_fallbacks"] > 0
+
+
+def test_concurrent_pipelines_agree():
+    """BC_OPT_STREAMS: 1, 3 and 8 concurrent batch pipelines (host threads,
+    private BC partials summed at the end) give the oracle's BC."""
+    bcb = _bcb()
+    g = gg.rmat(12, 16, seed=2)
+    S = g.non_isolated()
+    want = oracle.bc(g, S)
+    with bcb.Graph.from_csr(g) as G:
+        for ns in (1, 3, 8):
+            G.set_option(bcb.OPT_STREAMS, ns)
+            G.set_option(bcb.OPT_LANE_WORDS, 1)  # many batches
+            assert_bc_close(G.compute(S), want)
+            assert G.stats()["batches"] == (len(S) + 63) // 64
