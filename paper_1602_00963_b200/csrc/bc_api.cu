@@ -197,15 +197,19 @@ struct SlicesWS {
     int rows = 0;  // CTAs (private rows)
     int *queue = nullptr, *loff = nullptr;
     unsigned *bm = nullptr;
-    double *sigma = nullptr, *cf = nullptr, *bcp = nullptr;
+    double *sigma = nullptr, *cf = nullptr, *bcp = nullptr;  // cf / bcp: slices_kernel only
+    bool full = false;     // cf and bcp allocated
+    int4 *ell = nullptr;   // [n] padded neighbours (max degree <= 4)
     void release() {
         dfree(bm);
+        dfree(ell);
         dfree(queue);
         dfree(loff);
         dfree(sigma);
         dfree(cf);
         dfree(bcp);
         rows = 0;
+        full = false;
     }
 };
 
@@ -1008,25 +1012,29 @@ bc_status run_batch_w(bc_graph *g, LaneCtx &x, int W, const BatchCtx &c, std::ve
     }
 }
 
-bc_status ensure_slices(bc_graph *g, int rows) {
-    if (g->sws.rows >= rows) return BC_OK;
+bc_status ensure_slices(bc_graph *g, int rows, bool full) {
+    if (g->sws.rows >= rows && (g->sws.full || !full)) return BC_OK;
     g->sws.release();
     const size_t n = (size_t)g->n;
     SlicesWS &w = g->sws;
     const size_t bmw = (n + 31) / 32;
+    const size_t cnt = n * rows;
     CK(dalloc(&w.bm, 3 * bmw * rows));
     CK(dalloc(&w.queue, n * rows));
     CK(dalloc(&w.loff, (n + 2) * rows));
-    CK(dalloc(&w.sigma, n * rows));
-    CK(dalloc(&w.cf, n * rows));
-    CK(dalloc(&w.bcp, n * rows));
-    const size_t cnt = n * rows;
+    CK(dalloc(&w.sigma, cnt));
+    CK(dalloc(&w.ell, n));
     if (w.bm) CU(cudaMemset(w.bm, 0, 3 * bmw * rows * sizeof(unsigned)));
     CU(cudaMemset(w.sigma, 0, cnt * 8));
-    CU(cudaMemset(w.cf, 0, cnt * 8));
-    CU(cudaMemset(w.bcp, 0, cnt * 8));
+    if (full) {
+        CK(dalloc(&w.cf, cnt));
+        CK(dalloc(&w.bcp, cnt));
+        CU(cudaMemset(w.cf, 0, cnt * 8));
+        CU(cudaMemset(w.bcp, 0, cnt * 8));
+    }
     CU(cudaDeviceSynchronize());
     w.rows = rows;
+    w.full = full;
     return BC_OK;
 }
 
@@ -1036,18 +1044,39 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
 #ifndef BC_SLICES_SMEM_BM
 #define BC_SLICES_SMEM_BM 0  // shared-memory bitmaps cost occupancy; global (L2-resident) ones measured faster
 #endif
-    const bool smem_bm = BC_SLICES_SMEM_BM && g->n <= (int64_t)SLICES_SMEM_BM_WORDS * 32;
-    const size_t dsm = smem_bm ? 2 * SLICES_SMEM_BM_WORDS * sizeof(unsigned) : 0;
+#ifndef BC_SLICES_ELL
+#define BC_SLICES_ELL 1
+#endif
+#ifndef BC_SLICES_SM2
+#define BC_SLICES_SM2 1  // 2-bit per-vertex state in shared memory when it fits (BC_SLICES_SM2_MAXB)
+#endif
+#ifndef BC_SLICES_SM2_MAXB
+#define BC_SLICES_SM2_MAXB (72 * 1024)
+#endif
     int maxdeg = 0;
     for (int d : run.h_deg) maxdeg = std::max(maxdeg, d);
     const bool lowdeg = maxdeg <= BC_LOWDEG;  // vertex-per-thread pull variant, no fp atomics
-    auto kern = lowdeg ? slices_lowdeg_kernel : (smem_bm ? slices_kernel<true> : slices_kernel<false>);
+    const bool ell = BC_SLICES_ELL && maxdeg <= 4;  // neighbours as one int4 load
+    const size_t sm2_bytes = (size_t)((g->n + 15) / 16) * sizeof(unsigned);
+    const bool sm2 = lowdeg && BC_SLICES_SM2 && sm2_bytes <= (size_t)BC_SLICES_SM2_MAXB;
+    const bool smem_bm = !lowdeg && BC_SLICES_SMEM_BM && g->n <= (int64_t)SLICES_SMEM_BM_WORDS * 32;
+    const size_t dsm = sm2 ? sm2_bytes : smem_bm ? 2 * SLICES_SMEM_BM_WORDS * sizeof(unsigned) : 0;
+    auto kern = sm2      ? (ell ? slices_lowdeg_sm_kernel<true> : slices_lowdeg_sm_kernel<false>)
+                : lowdeg ? (ell ? slices_lowdeg_kernel<true> : slices_lowdeg_kernel<false>)
+                         : (smem_bm ? slices_kernel<true> : slices_kernel<false>);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
     int occ = 1;
-    const int nt = lowdeg ? BC_SL_NT : BC_NT;
+    const int nt = sm2 ? BC_SM_NT : lowdeg ? BC_SL_NT : BC_NT;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, dsm);
+#ifdef BC_SL_OCC
+    if (lowdeg) occ = std::min(occ, BC_SL_OCC);  // experiment builds: cap the sources in flight per SM
+#endif
     const int rows = std::max(1, std::min(ns, g->num_sms * std::max(1, occ)));
-    CK(ensure_slices(g, rows));
+    CK(ensure_slices(g, rows, !lowdeg));
+    if (ell) {
+        build_ell4_kernel<<<(unsigned)((g->n + 255) / 256), 256, 0, st>>>((int)g->n, run.rp, run.col, g->sws.ell);
+        g->last.kernel_launches += 1;
+    }
     SlicesParams p{};
     p.n = (int)g->n;
     p.rp = run.rp;
@@ -1063,6 +1092,8 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
     p.queue = g->sws.queue;
     p.loff = g->sws.loff;
     p.bcp = g->sws.bcp;
+    p.bc = g->d_bc;
+    p.ell4 = ell ? g->sws.ell : nullptr;
     p.stats = g->d_stats;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ev) {
@@ -1076,9 +1107,10 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
         ev->push_back(e0);
         ev->push_back(e1);
     }
-    slices_reduce_kernel<<<(unsigned)((g->n + 255) / 256), 256, 0, st>>>((int)g->n, rows, g->sws.bcp, g->d_bc);
+    if (!lowdeg)  // the degree-bounded kernel adds into d_bc directly
+        slices_reduce_kernel<<<(unsigned)((g->n + 255) / 256), 256, 0, st>>>((int)g->n, rows, g->sws.bcp, g->d_bc);
     CU(cudaGetLastError());
-    g->last.kernel_launches += 2;
+    g->last.kernel_launches += lowdeg ? 1 : 2;
     g->last.batches += 1;
     g->last.lanes = 1;
     return BC_OK;

@@ -46,7 +46,9 @@ struct SlicesParams {
     double *cf;             // acc -> coef; 0 between sources
     int *queue;
     int *loff;
-    double *bcp;            // private BC rows
+    double *bcp;            // private BC rows (slices_kernel)
+    double *bc;             // shared BC vector (slices_lowdeg_kernel adds into it)
+    const int4 *ell4;       // max degree <= 4: neighbours padded with -1, one 16-byte load per vertex
     unsigned *bm;           // global bitmaps [gridDim.x][2][bm_words] (when not in shared memory)
     int bm_words;
     unsigned long long *stats;  // [4] reached, adjacency, dag edges, depth sum
@@ -253,26 +255,64 @@ __global__ void __launch_bounds__(BC_NT) slices_kernel(SlicesParams p) {
 
 // Degree-bounded graphs (max degree <= BC_LOWDEG, e.g. the 2-D grid): one
 // thread per frontier vertex instead of the CD item mapping (no scan, no
-// binary search), and no floating-point atomics at all -- discovery pushes
-// only bits (visited bitmap + queue append), sigma is then *pulled* by each
-// newly discovered vertex from its level-L neighbours (Alg.1 lines 16-19 read
-// from the child's side), and the backward step pulls coef from the level-(L+1)
-// neighbours.  Level membership is two bitmaps (levels L and L+1).
+// binary search), and no floating-point atomics in the sweeps -- discovery
+// pushes only bits (visited bitmap + queue append), sigma is then *pulled* by
+// each newly discovered vertex from its level-L neighbours (Alg.1 lines 16-19
+// read from the child's side), and the backward step pulls coef from the
+// level-(L+1) neighbours.  Level membership is two bitmaps (levels L and L+1).
+//
+// Graphs with max degree <= 4 (the grid) read a vertex's neighbours as one
+// int4 of a padded (ELL) copy of the CSR: one dependent load fewer per
+// vertex on every level's critical path.
+//
+// Per-source state is one fp64 slot per vertex: sigma(w) is *assigned* by the
+// pull (never accumulated, so it needs no reset between sources) and
+// overwritten in place by coef(w) = (1 + omega(w) + delta(w)) / sigma(w) in
+// the backward step of w's level -- after that step sigma(w) is never read
+// again and the parents at level L-1 read only coef(w).  BC is added straight
+// into the shared BC vector (one fp64 red per reached vertex, L2-resident)
+// instead of a CTA-private row: per source and reached vertex the CTA touches
+// one 8-byte slot (written forward, read and rewritten backward) and 4 bytes
+// of queue, which keeps the concurrently swept frontiers of all CTAs inside
+// L2.  Neighbour lists are read BC_LD_GRP edges at a time with all loads of a
+// group issued before their use (the grid's 4 neighbours in one round trip).
 constexpr int BC_LOWDEG = 64;
 #ifndef BC_SL_NT
 #define BC_SL_NT 256  // threads per CTA of the degree-bounded slices kernel (more sources in flight)
 #endif
+#ifndef BC_SL_MINB
+#define BC_SL_MINB 4  // resident CTAs per SM the register budget is sized for (measured best on the grid)
+#endif
+constexpr int BC_LD_GRP = 4;
 
-__global__ void __launch_bounds__(BC_SL_NT, 1) slices_lowdeg_kernel(SlicesParams p) {
+// The neighbours of v as groups of BC_LD_GRP ids (-1 = none); with ELL the
+// whole list is one int4 load (max degree <= 4), else CSR reads.
+template <bool ELL, typename F>
+__device__ __forceinline__ void lowdeg_nbrs(const SlicesParams &p, int v, F &&f) {
+    if (ELL) {
+        const int4 q = p.ell4[v];
+        int w[BC_LD_GRP] = {q.x, q.y, q.z, q.w};
+        f(w);
+    } else {
+        const int a = p.rp[v], b = p.rp[v + 1];
+        for (int e = a; e < b; e += BC_LD_GRP) {
+            int w[BC_LD_GRP];
+#pragma unroll
+            for (int k = 0; k < BC_LD_GRP; ++k) w[k] = e + k < b ? p.col[e + k] : -1;
+            f(w);
+        }
+    }
+}
+
+template <bool ELL>
+__global__ void __launch_bounds__(BC_SL_NT, BC_SL_MINB) slices_lowdeg_kernel(SlicesParams p) {
     __shared__ SlicesSmem sm;
     const size_t n = (size_t)p.n;
-    double *sigma = p.sigma + blockIdx.x * n;
-    double *cf = p.cf + blockIdx.x * n;
+    double *sc = p.sigma + blockIdx.x * n;  // sigma, then coef (in place)
     int *Q = p.queue + blockIdx.x * n;
     int *loff = p.loff + blockIdx.x * (n + 2);
-    double *bcp = p.bcp + blockIdx.x * n;
     unsigned *vis = p.bm + (size_t)blockIdx.x * 3 * p.bm_words;
-    unsigned *lb0 = vis + p.bm_words;      // level bitmaps, alternating
+    unsigned *lb0 = vis + p.bm_words;  // level bitmaps, alternating
     unsigned *lb1 = lb0 + p.bm_words;
     const int lane = lane_id();
     unsigned long long st_reach = 0, st_adj = 0, st_dag = 0, st_dsum = 0;
@@ -291,7 +331,7 @@ __global__ void __launch_bounds__(BC_SL_NT, 1) slices_lowdeg_kernel(SlicesParams
         if (threadIdx.x == 0) {
             atomicOr(&vis[s >> 5], 1u << (s & 31));
             atomicOr(&lb0[s >> 5], 1u << (s & 31));
-            sigma[s] = 1.0;
+            sc[s] = 1.0;
             Q[0] = s;
             loff[0] = 0;
             loff[1] = 1;
@@ -304,31 +344,41 @@ __global__ void __launch_bounds__(BC_SL_NT, 1) slices_lowdeg_kernel(SlicesParams
             // (1) discovery: frontier vertices push visited bits
             for (int i = qs + threadIdx.x; i < qe; i += BC_SL_NT) {
                 const int v = Q[i];
-                const int a = p.rp[v], b = p.rp[v + 1];
-                for (int e = a; e < b; ++e) {
-                    const int w = p.col[e];
-                    const unsigned bit = 1u << (w & 31);
-                    if (!(vis[w >> 5] & bit) && !(atomicOr(&vis[w >> 5], bit) & bit)) {
-                        atomicOr(&lnxt[w >> 5], bit);
-                        Q[atomicAdd(&sm.tail, 1)] = w;
+                lowdeg_nbrs<ELL>(p, v, [&](const int *w) {
+                    unsigned wd[BC_LD_GRP];
+#pragma unroll
+                    for (int k = 0; k < BC_LD_GRP; ++k) wd[k] = w[k] >= 0 ? vis[w[k] >> 5] : ~0u;
+#pragma unroll
+                    for (int k = 0; k < BC_LD_GRP; ++k) {
+                        const unsigned bit = 1u << (w[k] & 31);
+                        if (!(wd[k] & bit) && !(atomicOr(&vis[w[k] >> 5], bit) & bit)) {
+                            atomicOr(&lnxt[w[k] >> 5], bit);
+                            Q[atomicAdd(&sm.tail, 1)] = w[k];
+                        }
                     }
-                }
+                });
             }
             __syncthreads();
             const int ne = sm.tail;
             // (2) sigma pull: each new vertex sums sigma of its level-L neighbours
             for (int i = qe + threadIdx.x; i < ne; i += BC_SL_NT) {
                 const int w = Q[i];
-                const int a = p.rp[w], b = p.rp[w + 1];
                 double sg = 0.0;
-                for (int e = a; e < b; ++e) {
-                    const int v = p.col[e];
-                    if (lcur[v >> 5] & (1u << (v & 31))) {
-                        sg += sigma[v];
-                        ++st_dag;
+                lowdeg_nbrs<ELL>(p, w, [&](const int *v) {
+                    unsigned wd[BC_LD_GRP];
+#pragma unroll
+                    for (int k = 0; k < BC_LD_GRP; ++k) wd[k] = v[k] >= 0 ? lcur[v[k] >> 5] : 0u;
+                    double x[BC_LD_GRP];
+#pragma unroll
+                    for (int k = 0; k < BC_LD_GRP; ++k) {
+                        const bool par = (wd[k] >> (v[k] & 31)) & 1u;
+                        x[k] = par ? sc[v[k]] : 0.0;
+                        st_dag += par;
                     }
-                }
-                sigma[w] = sg;
+#pragma unroll
+                    for (int k = 0; k < BC_LD_GRP; ++k) sg += x[k];
+                });
+                sc[w] = sg;
             }
             __syncthreads();
             // (3) retire level L's bits
@@ -345,7 +395,7 @@ __global__ void __launch_bounds__(BC_SL_NT, 1) slices_lowdeg_kernel(SlicesParams
             lcur = lnxt;
             lnxt = t;
         }
-        // lcur holds the (empty) last level; clear nothing more
+        // both level bitmaps are empty again here
         const int Lmax = L - 1;
         const int reached = qe;
         const double ws1 = 1.0 + (p.omega ? (double)p.omega[s] : 0.0);
@@ -361,18 +411,27 @@ __global__ void __launch_bounds__(BC_SL_NT, 1) slices_lowdeg_kernel(SlicesParams
             for (int i = a + threadIdx.x; i < b; i += BC_SL_NT) {
                 const int w = Q[i];
                 double acc = 0.0;
-                const int ea = p.rp[w], eb = p.rp[w + 1];
-                for (int e = ea; e < eb; ++e) {
-                    const int v = p.col[e];
-                    if (lb0[v >> 5] & (1u << (v & 31))) acc += cf[v];
-                }
+                const double sg = sc[w];
+                lowdeg_nbrs<ELL>(p, w, [&](const int *v) {
+                    unsigned wd[BC_LD_GRP];
+#pragma unroll
+                    for (int k = 0; k < BC_LD_GRP; ++k) wd[k] = v[k] >= 0 ? lb0[v[k] >> 5] : 0u;
+                    double x[BC_LD_GRP];
+#pragma unroll
+                    for (int k = 0; k < BC_LD_GRP; ++k) x[k] = ((wd[k] >> (v[k] & 31)) & 1u) ? sc[v[k]] : 0.0;
+#pragma unroll
+                    for (int k = 0; k < BC_LD_GRP; ++k) {
+                        acc += x[k];
+                        st_adj += v[k] >= 0;
+                    }
+                });
                 const double om = p.omega ? (double)p.omega[w] : 0.0;
-                const double sg = sigma[w];
                 const double delta = sg * acc;
-                cf[w] = (1.0 + om + delta) / sg;
+                sc[w] = (1.0 + om + delta) / sg;
                 const double c = ws1 * (delta + om);
-                if (c != 0.0) bcp[w] += c;
+                if (c != 0.0) atomicAdd(p.bc + w, c);
                 st_dsum += (unsigned long long)L;
+                ns_loc += 1.0 + om;
             }
             __syncthreads();
             for (int i = a1 + threadIdx.x; i < b1; i += BC_SL_NT) {
@@ -381,26 +440,199 @@ __global__ void __launch_bounds__(BC_SL_NT, 1) slices_lowdeg_kernel(SlicesParams
             }
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < reached; i += BC_SL_NT) {
-            const int w = Q[i];
-            ns_loc += 1.0 + (p.omega ? (double)p.omega[w] : 0.0);
-            st_adj += (unsigned long long)(p.rp[w + 1] - p.rp[w]);
-        }
         st_reach += (threadIdx.x == 0) ? (unsigned long long)reached : 0ull;
+        if (threadIdx.x == 0) {
+            st_adj += (unsigned long long)(p.rp[s + 1] - p.rp[s]);
+            ns_loc += ws1;
+        }
         ns_loc = warp_sum(ns_loc);
         if (lane == 0) sm.red[warp_id()] = ns_loc;
+        // clear the visited bitmap: whole words when most of it was reached
+        if (reached >= p.bm_words) {
+            for (int i = threadIdx.x; i < p.bm_words; i += BC_SL_NT) vis[i] = 0u;
+        } else {
+            for (int i = threadIdx.x; i < reached; i += BC_SL_NT) vis[Q[i] >> 5] = 0u;
+        }
         __syncthreads();
         if (threadIdx.x == 0 && p.omega) {
             double ns = 0.0;
             for (int w = 0; w < BC_SL_NT / 32; ++w) ns += sm.red[w];
             const double om = (double)p.omega[s];
-            if (om != 0.0) bcp[s] += om * (ns - 2.0);
+            if (om != 0.0) atomicAdd(p.bc + s, om * (ns - 2.0));
         }
-        for (int i = threadIdx.x; i < reached; i += BC_SL_NT) {
-            const int w = Q[i];
-            vis[w >> 5] = 0u;
-            sigma[w] = 0.0;
-            cf[w] = 0.0;
+        __syncthreads();
+    }
+    const unsigned long long a = warp_sum_u64(st_reach), b = warp_sum_u64(st_adj), c = warp_sum_u64(st_dag),
+                             d = warp_sum_u64(st_dsum);
+    if (lane == 0) {
+        if (a) atomicAdd(p.stats + 0, a);
+        if (b) atomicAdd(p.stats + 1, b);
+        if (c) atomicAdd(p.stats + 2, c);
+        if (d) atomicAdd(p.stats + 3, d);
+    }
+}
+
+// Shared-memory state variant of the degree-bounded kernel, for n small
+// enough that 2 bits per vertex fit in shared memory (the 512x512 grid: 64 KB
+// per CTA).  The 2-bit field of v is 0 while v is unvisited and
+// (depth(v) mod 3) + 1 once discovered.  A neighbour of a level-L vertex lies
+// at L-1, L or L+1 (or is unvisited), so "field == code(L)" identifies the
+// level-L parents in the sigma pull and "field == code(L+1)" the children in
+// the backward step: no level bitmaps to set and retire, discovery is a
+// shared-memory test-and-set, and a forward level takes two barriers, a
+// backward level one.  sigma / coef stay in the one fp64 slot per vertex.
+__device__ __forceinline__ unsigned lowdeg_code(int L) { return (unsigned)(L % 3) + 1u; }
+
+#ifndef BC_SM_NT
+#define BC_SM_NT 640  // threads per CTA of the shared-memory-state kernel: one pass over most grid levels
+#endif
+#ifndef BC_SM_MINB
+#define BC_SM_MINB 2  // two CTAs per SM (64 KB state + 16 KB frontier each)
+#endif
+#ifndef BC_SM_FR
+#define BC_SM_FR 0  // 1: keep the current / next frontier in shared memory (measured slower: the 16 KB come out of L1)
+#endif
+#ifndef BC_SL_FCAP
+#define BC_SL_FCAP 2048  // frontier vertices kept in shared memory per level (larger levels read Q)
+#endif
+
+template <bool ELL>
+__global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(SlicesParams p) {
+    __shared__ SlicesSmem sm;
+    __shared__ int fr[2][BC_SL_FCAP];  // the current / next frontier
+    extern __shared__ unsigned f2[];   // 2 bits per vertex
+    const size_t n = (size_t)p.n;
+    const int nw = (p.n + 15) / 16;
+    double *sc = p.sigma + blockIdx.x * n;  // sigma, then coef (in place)
+    int *Q = p.queue + blockIdx.x * n;
+    int *loff = p.loff + blockIdx.x * (n + 2);
+    const int lane = lane_id();
+    unsigned long long st_reach = 0, st_adj = 0, st_dag = 0, st_dsum = 0;
+    for (int i = threadIdx.x; i < nw; i += BC_SM_NT) f2[i] = 0u;
+
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const int t = atomicAdd(p.next_src, 1);
+            if (t == p.nsrc + (int)gridDim.x - 1) *p.next_src = 0;  // last fetch resets
+            sm.src = t;
+        }
+        __syncthreads();
+        const int si = sm.src;
+        __syncthreads();
+        if (si >= p.nsrc) break;
+        const int s = p.src[si];
+        if (threadIdx.x == 0) {
+            f2[s >> 4] |= lowdeg_code(0) << ((s & 15) * 2);
+            sc[s] = 1.0;
+            Q[0] = s;
+            fr[0][0] = s;
+            loff[0] = 0;
+            loff[1] = 1;
+            sm.tail = 1;
+        }
+        __syncthreads();
+        // forward: (1) discovery by shared-memory test-and-set, barrier,
+        // (2) every new vertex pulls sigma from its level-L neighbours,
+        // barrier.  The level's vertices are read from a shared-memory copy
+        // of the frontier when it fits (BC_SL_FCAP), else from Q.
+        int L = 0, qs = 0, qe = 1, cb = 0;
+        while (qs < qe) {
+            const unsigned cn = lowdeg_code(L + 1), cc = lowdeg_code(L);
+            const bool in_sm = BC_SM_FR && qe - qs <= BC_SL_FCAP;
+            for (int i = qs + threadIdx.x; i < qe; i += BC_SM_NT) {
+                const int v = in_sm ? fr[cb][i - qs] : Q[i];
+                lowdeg_nbrs<ELL>(p, v, [&](const int *w) {
+#pragma unroll
+                    for (int k = 0; k < BC_LD_GRP; ++k) {
+                        if (w[k] < 0) continue;
+                        const int sh = (w[k] & 15) * 2;
+                        if (((f2[w[k] >> 4] >> sh) & 3u) == 0u &&
+                            ((atomicOr(&f2[w[k] >> 4], cn << sh) >> sh) & 3u) == 0u) {
+                            const int pos = atomicAdd(&sm.tail, 1);
+                            Q[pos] = w[k];
+                            if (BC_SM_FR && pos - qe < BC_SL_FCAP) fr[cb ^ 1][pos - qe] = w[k];
+                        }
+                    }
+                });
+            }
+            __syncthreads();
+            const int ne = sm.tail;
+            const bool nx_sm = BC_SM_FR && ne - qe <= BC_SL_FCAP;
+            for (int i = qe + threadIdx.x; i < ne; i += BC_SM_NT) {
+                const int w = nx_sm ? fr[cb ^ 1][i - qe] : Q[i];
+                double sg = 0.0;
+                lowdeg_nbrs<ELL>(p, w, [&](const int *v) {
+                    double x[BC_LD_GRP];
+#pragma unroll
+                    for (int k = 0; k < BC_LD_GRP; ++k) {
+                        const bool par = v[k] >= 0 && ((f2[v[k] >> 4] >> ((v[k] & 15) * 2)) & 3u) == cc;
+                        x[k] = par ? sc[v[k]] : 0.0;
+                        st_dag += par;
+                    }
+#pragma unroll
+                    for (int k = 0; k < BC_LD_GRP; ++k) sg += x[k];
+                });
+                sc[w] = sg;
+            }
+            __syncthreads();
+            qs = qe;
+            qe = ne;
+            cb ^= 1;
+            ++L;
+            if (threadIdx.x == 0) loff[L + 1] = qe;
+        }
+        const int Lmax = L - 1;
+        const int reached = qe;
+        const double ws1 = 1.0 + (p.omega ? (double)p.omega[s] : 0.0);
+        double ns_loc = 0.0;
+        for (L = Lmax; L >= 1; --L) {
+            const int a = loff[L], b = loff[L + 1];
+            const unsigned cch = lowdeg_code(L + 1);
+            for (int i = a + threadIdx.x; i < b; i += BC_SM_NT) {
+                const int w = Q[i];
+                double acc = 0.0;
+                const double sg = sc[w];
+                lowdeg_nbrs<ELL>(p, w, [&](const int *v) {
+                    double x[BC_LD_GRP];
+#pragma unroll
+                    for (int k = 0; k < BC_LD_GRP; ++k) {
+                        const bool ch = v[k] >= 0 && ((f2[v[k] >> 4] >> ((v[k] & 15) * 2)) & 3u) == cch;
+                        x[k] = ch ? sc[v[k]] : 0.0;
+                    }
+#pragma unroll
+                    for (int k = 0; k < BC_LD_GRP; ++k) {
+                        acc += x[k];
+                        st_adj += v[k] >= 0;
+                    }
+                });
+                const double om = p.omega ? (double)p.omega[w] : 0.0;
+                const double delta = sg * acc;
+                sc[w] = (1.0 + om + delta) / sg;
+                const double c = ws1 * (delta + om);
+                if (c != 0.0) atomicAdd(p.bc + w, c);
+                st_dsum += (unsigned long long)L;
+                ns_loc += 1.0 + om;
+            }
+            __syncthreads();
+        }
+        st_reach += (threadIdx.x == 0) ? (unsigned long long)reached : 0ull;
+        if (threadIdx.x == 0) {
+            st_adj += (unsigned long long)(p.rp[s + 1] - p.rp[s]);
+            ns_loc += ws1;
+        }
+        ns_loc = warp_sum(ns_loc);
+        if (lane == 0) sm.red[warp_id()] = ns_loc;
+        if (reached >= nw / 4) {
+            for (int i = threadIdx.x; i < nw; i += BC_SM_NT) f2[i] = 0u;
+        } else {
+            for (int i = threadIdx.x; i < reached; i += BC_SM_NT) f2[Q[i] >> 4] = 0u;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && p.omega) {
+            double ns = 0.0;
+            for (int w = 0; w < BC_SM_NT / 32; ++w) ns += sm.red[w];
+            const double om = (double)p.omega[s];
+            if (om != 0.0) atomicAdd(p.bc + s, om * (ns - 2.0));
         }
         __syncthreads();
     }
@@ -432,4 +664,19 @@ __global__ void fill_int_kernel(int *p, size_t cnt, int v) {
     if (i < cnt) p[i] = v;
 }
 
+}  // namespace bcb
+
+namespace bcb {
+// ell[v] = the (<= 4) neighbours of v, padded with -1
+__global__ void build_ell4_kernel(int n, const int *rp, const int *col, int4 *ell) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const int a = rp[v], d = rp[v + 1] - a;
+    int4 q;
+    q.x = d > 0 ? col[a] : -1;
+    q.y = d > 1 ? col[a + 1] : -1;
+    q.z = d > 2 ? col[a + 2] : -1;
+    q.w = d > 3 ? col[a + 3] : -1;
+    ell[v] = q;
+}
 }  // namespace bcb
