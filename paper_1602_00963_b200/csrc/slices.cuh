@@ -487,31 +487,41 @@ __device__ __forceinline__ unsigned lowdeg_code(int L) { return (unsigned)(L % 3
 #define BC_SM_NT 640  // threads per CTA of the shared-memory-state kernel: one pass over most grid levels
 #endif
 #ifndef BC_SM_MINB
-#define BC_SM_MINB 2  // two CTAs per SM (64 KB state + 16 KB frontier each)
+#define BC_SM_MINB 2  // two CTAs per SM (64 KB state each)
 #endif
-#ifndef BC_SM_FR
-#define BC_SM_FR 0  // 1: keep the current / next frontier in shared memory (measured slower: the 16 KB come out of L1)
-#endif
-#ifndef BC_SL_FCAP
-#define BC_SL_FCAP 2048  // frontier vertices kept in shared memory per level (larger levels read Q)
-#endif
+// A vertex's neighbour "row": the int4 of neighbour ids (ELL) or, for CSR
+// reads, the vertex id in .x.
+template <bool ELL>
+__device__ __forceinline__ int4 lowdeg_row(const SlicesParams &p, int v) {
+    if constexpr (ELL) return p.ell4[v];
+    else return make_int4(v, 0, 0, 0);
+}
+template <bool ELL, typename F>
+__device__ __forceinline__ void lowdeg_row_nbrs(const SlicesParams &p, int4 row, F &&f) {
+    if constexpr (ELL) {
+        int w[BC_LD_GRP] = {row.x, row.y, row.z, row.w};
+        f(w);
+    } else {
+        lowdeg_nbrs<false>(p, row.x, f);
+    }
+}
 
 template <bool ELL>
 __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(SlicesParams p) {
     __shared__ SlicesSmem sm;
-    __shared__ int fr[2][BC_SL_FCAP];  // the current / next frontier
-    extern __shared__ unsigned f2[];   // 2 bits per vertex
+    extern __shared__ unsigned f2[];  // 2 bits per vertex
     const size_t n = (size_t)p.n;
     const int nw = (p.n + 15) / 16;
+    const int tid = threadIdx.x;
     double *sc = p.sigma + blockIdx.x * n;  // sigma, then coef (in place)
     int *Q = p.queue + blockIdx.x * n;
     int *loff = p.loff + blockIdx.x * (n + 2);
     const int lane = lane_id();
     unsigned long long st_reach = 0, st_adj = 0, st_dag = 0, st_dsum = 0;
-    for (int i = threadIdx.x; i < nw; i += BC_SM_NT) f2[i] = 0u;
+    for (int i = tid; i < nw; i += BC_SM_NT) f2[i] = 0u;
 
     for (;;) {
-        if (threadIdx.x == 0) {
+        if (tid == 0) {
             const int t = atomicAdd(p.next_src, 1);
             if (t == p.nsrc + (int)gridDim.x - 1) *p.next_src = 0;  // last fetch resets
             sm.src = t;
@@ -521,47 +531,60 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
         __syncthreads();
         if (si >= p.nsrc) break;
         const int s = p.src[si];
-        if (threadIdx.x == 0) {
+        if (tid == 0) {
             f2[s >> 4] |= lowdeg_code(0) << ((s & 15) * 2);
             sc[s] = 1.0;
             Q[0] = s;
-            fr[0][0] = s;
             loff[0] = 0;
             loff[1] = 1;
             sm.tail = 1;
         }
         __syncthreads();
-        // forward: (1) discovery by shared-memory test-and-set, barrier,
-        // (2) every new vertex pulls sigma from its level-L neighbours,
-        // barrier.  The level's vertices are read from a shared-memory copy
-        // of the frontier when it fits (BC_SL_FCAP), else from Q.
-        int L = 0, qs = 0, qe = 1, cb = 0;
+        // forward: (1) discovery by shared-memory test-and-set, new vertices
+        // appended with one shared atomic per warp, barrier; (2) every new
+        // vertex pulls sigma from its level-L neighbours, barrier.  The thread
+        // that pulls slot qe + tid keeps that vertex's row in registers: it is
+        // its first frontier slot of the next discovery.
+        int L = 0, qs = 0, qe = 1;
+        int4 crow = make_int4(0, 0, 0, 0);
+        bool carry = false;
         while (qs < qe) {
             const unsigned cn = lowdeg_code(L + 1), cc = lowdeg_code(L);
-            const bool in_sm = BC_SM_FR && qe - qs <= BC_SL_FCAP;
-            for (int i = qs + threadIdx.x; i < qe; i += BC_SM_NT) {
-                const int v = in_sm ? fr[cb][i - qs] : Q[i];
-                lowdeg_nbrs<ELL>(p, v, [&](const int *w) {
+            for (int i = qs + tid; i < qe; i += BC_SM_NT) {
+                const int4 row = (carry && i == qs + tid) ? crow : lowdeg_row<ELL>(p, Q[i]);
+                lowdeg_row_nbrs<ELL>(p, row, [&](const int *w) {
 #pragma unroll
                     for (int k = 0; k < BC_LD_GRP; ++k) {
-                        if (w[k] < 0) continue;
-                        const int sh = (w[k] & 15) * 2;
-                        if (((f2[w[k] >> 4] >> sh) & 3u) == 0u &&
-                            ((atomicOr(&f2[w[k] >> 4], cn << sh) >> sh) & 3u) == 0u) {
-                            const int pos = atomicAdd(&sm.tail, 1);
-                            Q[pos] = w[k];
-                            if (BC_SM_FR && pos - qe < BC_SL_FCAP) fr[cb ^ 1][pos - qe] = w[k];
+                        bool won = false;
+                        if (w[k] >= 0) {
+                            const int sh = (w[k] & 15) * 2;
+                            won = ((f2[w[k] >> 4] >> sh) & 3u) == 0u &&
+                                  ((atomicOr(&f2[w[k] >> 4], cn << sh) >> sh) & 3u) == 0u;
+                        }
+                        const unsigned am = __activemask();
+                        const unsigned bal = __ballot_sync(am, won);
+                        if (bal) {
+                            const int leader = __ffs(bal) - 1;
+                            int base = 0;
+                            if (lane == leader) base = atomicAdd(&sm.tail, __popc(bal));
+                            base = __shfl_sync(am, base, leader);
+                            if (won) Q[base + __popc(bal & ((1u << lane) - 1u))] = w[k];
                         }
                     }
                 });
             }
+            carry = false;
             __syncthreads();
             const int ne = sm.tail;
-            const bool nx_sm = BC_SM_FR && ne - qe <= BC_SL_FCAP;
-            for (int i = qe + threadIdx.x; i < ne; i += BC_SM_NT) {
-                const int w = nx_sm ? fr[cb ^ 1][i - qe] : Q[i];
+            for (int i = qe + tid; i < ne; i += BC_SM_NT) {
+                const int w = Q[i];
+                const int4 row = lowdeg_row<ELL>(p, w);
+                if (i == qe + tid) {
+                    crow = row;
+                    carry = true;
+                }
                 double sg = 0.0;
-                lowdeg_nbrs<ELL>(p, w, [&](const int *v) {
+                lowdeg_row_nbrs<ELL>(p, row, [&](const int *v) {
                     double x[BC_LD_GRP];
 #pragma unroll
                     for (int k = 0; k < BC_LD_GRP; ++k) {
@@ -577,22 +600,37 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
             __syncthreads();
             qs = qe;
             qe = ne;
-            cb ^= 1;
             ++L;
-            if (threadIdx.x == 0) loff[L + 1] = qe;
+            if (tid == 0) loff[L + 1] = qe;
         }
         const int Lmax = L - 1;
         const int reached = qe;
         const double ws1 = 1.0 + (p.omega ? (double)p.omega[s] : 0.0);
         double ns_loc = 0.0;
+        // backward, one barrier per level; each thread's first slot of the
+        // next level (vertex, row, sigma) is loaded before the barrier --
+        // level L-1 is not written during level L's step
+        int a = 0, b = 0, wq = -1;
+        int4 rq = make_int4(0, 0, 0, 0);
+        double sq = 0.0;
+        if (Lmax >= 1) {
+            a = loff[Lmax];
+            b = loff[Lmax + 1];
+            if (a + tid < b) {
+                wq = Q[a + tid];
+                rq = lowdeg_row<ELL>(p, wq);
+                sq = sc[wq];
+            }
+        }
         for (L = Lmax; L >= 1; --L) {
-            const int a = loff[L], b = loff[L + 1];
             const unsigned cch = lowdeg_code(L + 1);
-            for (int i = a + threadIdx.x; i < b; i += BC_SM_NT) {
-                const int w = Q[i];
+            for (int i = a + tid; i < b; i += BC_SM_NT) {
+                const bool first = i == a + tid;
+                const int w = first ? wq : Q[i];
+                const int4 row = first ? rq : lowdeg_row<ELL>(p, w);
+                const double sg = first ? sq : sc[w];
                 double acc = 0.0;
-                const double sg = sc[w];
-                lowdeg_nbrs<ELL>(p, w, [&](const int *v) {
+                lowdeg_row_nbrs<ELL>(p, row, [&](const int *v) {
                     double x[BC_LD_GRP];
 #pragma unroll
                     for (int k = 0; k < BC_LD_GRP; ++k) {
@@ -613,22 +651,31 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
                 st_dsum += (unsigned long long)L;
                 ns_loc += 1.0 + om;
             }
+            const int an = loff[L - 1], bn = loff[L];
+            wq = -1;
+            if (L - 1 >= 1 && an + tid < bn) {
+                wq = Q[an + tid];
+                rq = lowdeg_row<ELL>(p, wq);
+                sq = sc[wq];
+            }
             __syncthreads();
+            a = an;
+            b = bn;
         }
-        st_reach += (threadIdx.x == 0) ? (unsigned long long)reached : 0ull;
-        if (threadIdx.x == 0) {
+        st_reach += (tid == 0) ? (unsigned long long)reached : 0ull;
+        if (tid == 0) {
             st_adj += (unsigned long long)(p.rp[s + 1] - p.rp[s]);
             ns_loc += ws1;
         }
         ns_loc = warp_sum(ns_loc);
         if (lane == 0) sm.red[warp_id()] = ns_loc;
         if (reached >= nw / 4) {
-            for (int i = threadIdx.x; i < nw; i += BC_SM_NT) f2[i] = 0u;
+            for (int i = tid; i < nw; i += BC_SM_NT) f2[i] = 0u;
         } else {
-            for (int i = threadIdx.x; i < reached; i += BC_SM_NT) f2[Q[i] >> 4] = 0u;
+            for (int i = tid; i < reached; i += BC_SM_NT) f2[Q[i] >> 4] = 0u;
         }
         __syncthreads();
-        if (threadIdx.x == 0 && p.omega) {
+        if (tid == 0 && p.omega) {
             double ns = 0.0;
             for (int w = 0; w < BC_SM_NT / 32; ++w) ns += sm.red[w];
             const double om = (double)p.omega[s];

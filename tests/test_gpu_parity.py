@@ -129,6 +129,39 @@ def test_config2_grid512_sampled_launch_config():
     assert abs(got.sum() - inv) <= 1e-9 * inv
 
 
+@pytest.mark.parametrize("which", ["ell", "csr", "csr_pruned"])
+def test_slices_lowdeg_kernels_large_and_small_n(which):
+    """The degree-bounded slices kernels: the global-bitmap kernel (n past
+    the shared-memory state, 1.2M vertices) and the shared-memory 2-bit-state
+    kernel (small n), each with int4 (ELL, max degree <= 4) or CSR neighbour
+    reads, pruning on in one case, on sampled sources of long-diameter graphs.
+    The big grid is 40 x 30000 (30038 levels; sigma <= C(30038, 39) < 2^440 --
+    a 1100 x 1100 grid would overflow fp64 sigma, C(2198, 1099) > 2^2000)."""
+    bcb = _bcb()
+    big = gg.grid(40, 30000)
+    if which == "csr":
+        big = gg.disjoint_union(big, gg.hypercube(6))  # max degree 6
+    elif which == "csr_pruned":
+        big = gg.disjoint_union(big, gg.random_tree(3000, seed=5), gg.hypercube(5))
+    small = gg.grid(300, 301)
+    if which != "ell":
+        small = gg.disjoint_union(small, gg.random_tree(500, seed=6), gg.hypercube(5))
+    for h in (big, small):
+        S = gg.sample_sources(h, h.n, seed=4)[:24]
+        with bcb.Graph.from_csr(h) as G:
+            G.set_option(bcb.OPT_MODE, 2)
+            if which == "csr_pruned":
+                G.prune_degree1()
+                _, rm, _, _ = G.pruning()
+                S = S[rm[S] == 0]
+                want = oracle.bc_pruned(h, S)
+            else:
+                want = oracle.bc(h, S)
+            got = G.compute(S)
+            assert G.stats()["lanes"] == 1
+            assert_bc_close(got, want)
+
+
 @pytest.mark.parametrize("hub", [32, 4096])
 def test_small_suite_pruned(hub):
     bcb = _bcb()
