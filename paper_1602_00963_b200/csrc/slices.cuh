@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(BC_SL_NT, BC_SL_MINB) slices_lowdeg_kernel(Sli
 __device__ __forceinline__ unsigned lowdeg_code(int L) { return (unsigned)(L % 3) + 1u; }
 
 #ifndef BC_SM_NT
-#define BC_SM_NT 640  // threads per CTA of the shared-memory-state kernel: one pass over most grid levels
+#define BC_SM_NT 512  // threads per CTA of the shared-memory-state kernel (one pass over most grid levels; 63 registers, no spills)
 #endif
 #ifndef BC_SM_MINB
 #define BC_SM_MINB 2  // two CTAs per SM (64 KB state each)
@@ -540,18 +540,33 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
             sm.tail = 1;
         }
         __syncthreads();
-        // forward: (1) discovery by shared-memory test-and-set, new vertices
-        // appended with one shared atomic per warp, barrier; (2) every new
-        // vertex pulls sigma from its level-L neighbours, barrier.  The thread
-        // that pulls slot qe + tid keeps that vertex's row in registers: it is
-        // its first frontier slot of the next discovery.
+        // forward, one barrier per level: each thread takes a level-L vertex
+        // v, loads its row once, first pulls sigma(v) from v's level-(L-1)
+        // neighbours (complete before the previous barrier), then discovers
+        // v's unvisited neighbours (level L+1) by shared-memory test-and-set,
+        // appending them with one shared atomic per warp.  Concurrently set
+        // codes are code(L+1) != code(L-1), so the parent test is unaffected.
         int L = 0, qs = 0, qe = 1;
-        int4 crow = make_int4(0, 0, 0, 0);
-        bool carry = false;
         while (qs < qe) {
-            const unsigned cn = lowdeg_code(L + 1), cc = lowdeg_code(L);
+            const unsigned cn = lowdeg_code(L + 1), cp = lowdeg_code(L + 2);  // (L + 2) mod 3 == (L - 1) mod 3
             for (int i = qs + tid; i < qe; i += BC_SM_NT) {
-                const int4 row = (carry && i == qs + tid) ? crow : lowdeg_row<ELL>(p, Q[i]);
+                const int v = Q[i];
+                const int4 row = lowdeg_row<ELL>(p, v);
+                if (L >= 1) {
+                    double sg = 0.0;
+                    lowdeg_row_nbrs<ELL>(p, row, [&](const int *u) {
+                        double x[BC_LD_GRP];
+#pragma unroll
+                        for (int k = 0; k < BC_LD_GRP; ++k) {
+                            const bool par = u[k] >= 0 && ((f2[u[k] >> 4] >> ((u[k] & 15) * 2)) & 3u) == cp;
+                            x[k] = par ? sc[u[k]] : 0.0;
+                            st_dag += par;
+                        }
+#pragma unroll
+                        for (int k = 0; k < BC_LD_GRP; ++k) sg += x[k];
+                    });
+                    sc[v] = sg;
+                }
                 lowdeg_row_nbrs<ELL>(p, row, [&](const int *w) {
 #pragma unroll
                     for (int k = 0; k < BC_LD_GRP; ++k) {
@@ -573,33 +588,9 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
                     }
                 });
             }
-            carry = false;
-            __syncthreads();
-            const int ne = sm.tail;
-            for (int i = qe + tid; i < ne; i += BC_SM_NT) {
-                const int w = Q[i];
-                const int4 row = lowdeg_row<ELL>(p, w);
-                if (i == qe + tid) {
-                    crow = row;
-                    carry = true;
-                }
-                double sg = 0.0;
-                lowdeg_row_nbrs<ELL>(p, row, [&](const int *v) {
-                    double x[BC_LD_GRP];
-#pragma unroll
-                    for (int k = 0; k < BC_LD_GRP; ++k) {
-                        const bool par = v[k] >= 0 && ((f2[v[k] >> 4] >> ((v[k] & 15) * 2)) & 3u) == cc;
-                        x[k] = par ? sc[v[k]] : 0.0;
-                        st_dag += par;
-                    }
-#pragma unroll
-                    for (int k = 0; k < BC_LD_GRP; ++k) sg += x[k];
-                });
-                sc[w] = sg;
-            }
             __syncthreads();
             qs = qe;
-            qe = ne;
+            qe = sm.tail;
             ++L;
             if (tid == 0) loff[L + 1] = qe;
         }
