@@ -365,7 +365,8 @@ def main():
             # bytes are the K = 1, fp64 model of both sweeps
             kms = {"slices": agg["fwd_ms"]}
             kbytes = {"slices": kbytes["fwd"] + kbytes["bwd"]}
-            names = {"slices": "slices_lowdeg_kernel (forward + backward sweeps of one source per CTA)"}
+            names = {"slices": "slices_lowdeg_sm_kernel (2-bit shared-memory state; forward + "
+                               "backward sweeps of one source per CTA)"}
         dom = max(kms, key=lambda k: kms[k])
         dom_ms = kms[dom]
         achieved = kbytes[dom] / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
