@@ -135,7 +135,10 @@ typedef enum {
     BC_OPT_HUB_DEGREE = 2, /* vertices with degree > value are processed as split hubs (>= 32) */
     BC_OPT_PROFILE = 3,    /* 1 = record CUDA events around the level kernels (bc_get_stats) */
     BC_OPT_MODE = 4,       /* 0 = auto, 1 = lanes (bit-lane batches), 2 = slices (CTA per source) */
-    BC_OPT_RELABEL = 5,    /* 1 (default) = traverse a degree-descending relabelled copy of the graph */
+    BC_OPT_RELABEL = 5,    /* traverse a relabelled copy of the graph: 0 = caller's ids, 1 (default) =
+                              degree-descending, or breadth-first (Cuthill-McKee, from a far vertex of each
+                              component) when max degree <= 64 and auto mode picks slices;
+                              2 = breadth-first always.  Results are returned in caller ids either way */
     BC_OPT_SOURCE_ORDER = 6, /* batch schedule: 0 = given order, 1 = degree, 2 (default) = anchor clusters */
     BC_OPT_FWD_PUSH = 7,    /* forward levels L <= value expand in push form (default 0), later ones pull */
     BC_OPT_BWD_MODE = 8,    /* backward sweep: 0 = default, 1 = push form, 2 = pull form (successor checking) */

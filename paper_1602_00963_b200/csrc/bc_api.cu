@@ -356,6 +356,9 @@ bc_status build_hubs(bc_graph *g, DevCSR &c, cudaStream_t st) {
     return BC_OK;
 }
 
+// auto mode (BC_OPT_MODE = 0): slices for large sparse (long-diameter-like) graphs
+static bool auto_slices(int64_t n, int64_t nnz) { return n > 65536 && (double)nnz / (double)n < 6.0; }
+
 // The compute CSR: cur() relabelled by descending degree (stable, ties by
 // id), so hub rows are contiguous at the front of every per-vertex array.
 bc_status build_run(bc_graph *g) {
@@ -375,7 +378,45 @@ bc_status build_run(bc_graph *g) {
     CK(dalloc(&keys_out, n));
     CK(dalloc(&vals_in, n));
     relabel_keys_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, c.rp, maxdeg, keys_in, vals_in);
-    if (g->relabel && maxdeg > 0) {
+    // relabel 1 (default): degree order, or breadth-first order for degree-bounded
+    // graphs that auto mode runs as slices (grid: 33 -> 38 GTEPS; R-MAT S20 is
+    // 17 % slower in BFS order, tools/exp43.sh); 2: breadth-first order always
+    const bool bfs_order = g->relabel == 2 || (g->relabel == 1 && maxdeg <= BC_LOWDEG && auto_slices(n, c.nnz));
+    if (bfs_order && n > 0) {
+        // breadth-first (Cuthill-McKee) order from a pseudo-peripheral vertex:
+        // a BFS frontier of a long-diameter graph becomes a few contiguous id
+        // runs, so the slices kernels' per-vertex sigma/coef slots share sectors
+        std::vector<int> hrp(n + 1), hcol((size_t)c.nnz);
+        CU(cudaMemcpyAsync(hrp.data(), c.rp, (size_t)(n + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
+        if (c.nnz) CU(cudaMemcpyAsync(hcol.data(), c.col, (size_t)c.nnz * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        std::vector<int> order, dist(n, -1);
+        order.reserve(n);
+        auto bfs = [&](int s0) {  // appends s0's component to order; returns its last vertex
+            size_t h = order.size();
+            dist[s0] = 0;
+            order.push_back(s0);
+            for (; h < order.size(); ++h) {
+                const int v = order[h];
+                for (int e = hrp[v]; e < hrp[v + 1]; ++e)
+                    if (dist[hcol[e]] < 0) {
+                        dist[hcol[e]] = dist[v] + 1;
+                        order.push_back(hcol[e]);
+                    }
+            }
+            return order.back();
+        };
+        for (int v0 = 0; v0 < n; ++v0) {
+            if (dist[v0] >= 0) continue;
+            const size_t h = order.size();
+            const int far = bfs(v0);  // first pass finds a far vertex, the second orders from it
+            for (size_t i = h; i < order.size(); ++i) dist[order[i]] = -1;
+            order.resize(h);
+            bfs(far);
+        }
+        CU(cudaMemcpyAsync(r.perm, order.data(), (size_t)n * sizeof(int), cudaMemcpyHostToDevice, st));
+        CU(cudaStreamSynchronize(st));
+    } else if (g->relabel && maxdeg > 0) {
         const int end_bit = 32 - __builtin_clz((unsigned)maxdeg);
         size_t tmp_bytes = 0;
         CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in, keys_out, vals_in, r.perm, n, 0, end_bit, st));
@@ -1365,7 +1406,8 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
             g->src_order = (int)value;
             return BC_OK;
         case BC_OPT_RELABEL: {
-            int v = value ? 1 : 0;
+            if (value < 0 || value > 2) return fail(BC_ERR_INVALID, "relabel must be 0, 1 or 2");
+            const int v = (int)value;
             if (v == g->relabel) return BC_OK;
             DeviceGuard dg(g->device);
             g->relabel = v;
@@ -1459,7 +1501,7 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     // batch mode: bit lanes (low diameter) or one source per CTA (long
     // diameter); auto picks slices for large sparse graphs (mean degree < 6)
     int mode = g->mode;
-    if (mode == 0) mode = (g->n > 65536 && (double)run.nnz / (double)g->n < 6.0) ? 2 : 1;
+    if (mode == 0) mode = auto_slices(g->n, run.nnz) ? 2 : 1;
     // level-row width: 4 bytes per lane (the 16- and 32-bit sigma tiers) unless
     // fp64 rows are requested; a batch that needs fp64 widens them (widen_rows)
     const int rb = g->sigma_width == 64 || g->bwd_mode == 2 || g->fwd_push_levels > 0 ? 8 : 4;

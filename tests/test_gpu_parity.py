@@ -55,7 +55,7 @@ SUITE = small_suite()
 
 @pytest.mark.parametrize("words", [1, 2, 4, 8])
 @pytest.mark.parametrize("hub", [32, 4096])
-@pytest.mark.parametrize("relabel", [0, 1])
+@pytest.mark.parametrize("relabel", [0, 1, 2])
 def test_small_suite_all_sources(words, hub, relabel):
     bcb = _bcb()
     for g in SUITE:
@@ -91,13 +91,17 @@ def test_backward_forms_push_and_pull(bwd, words):
         assert_bc_close(G.compute(S), oracle.bc(g, S))
 
 
+@pytest.mark.parametrize("relabel", [1, 2])
 @pytest.mark.parametrize("prune", [False, True])
-def test_small_suite_slices_mode(prune):
-    """Batch mode 'slices' (one source per CTA) on the same suite."""
+def test_small_suite_slices_mode(prune, relabel):
+    """Batch mode 'slices' (one source per CTA) on the same suite, degree and
+    breadth-first relabelling (the latter covers disconnected and isolated
+    vertices: every component is ordered from its own far vertex)."""
     bcb = _bcb()
     for g in SUITE:
         with bcb.Graph.from_csr(g) as G:
             G.set_option(bcb.OPT_MODE, 2)
+            G.set_option(bcb.OPT_RELABEL, relabel)
             if prune:
                 G.prune_degree1()
             assert_bc_close(G.compute(), oracle.bc(g))
