@@ -200,8 +200,10 @@ struct SlicesWS {
     double *sigma = nullptr, *cf = nullptr, *bcp = nullptr;  // cf / bcp: slices_kernel only
     bool full = false;     // cf and bcp allocated
     int4 *ell = nullptr;   // [n] padded neighbours (max degree <= 4)
+    int4 *qrow = nullptr;  // [rows][n] neighbour rows in queue order (BC_SM_QROW)
     void release() {
         dfree(bm);
+        dfree(qrow);
         dfree(ell);
         dfree(queue);
         dfree(loff);
@@ -1065,6 +1067,9 @@ bc_status ensure_slices(bc_graph *g, int rows, bool full) {
     CK(dalloc(&w.loff, (n + 2) * rows));
     CK(dalloc(&w.sigma, cnt));
     CK(dalloc(&w.ell, n));
+#if BC_SM_QROW
+    CK(dalloc(&w.qrow, n * rows));
+#endif
     if (w.bm) CU(cudaMemset(w.bm, 0, 3 * bmw * rows * sizeof(unsigned)));
     CU(cudaMemset(w.sigma, 0, cnt * 8));
     if (full) {
@@ -1135,6 +1140,7 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
     p.bcp = g->sws.bcp;
     p.bc = g->d_bc;
     p.ell4 = ell ? g->sws.ell : nullptr;
+    p.qrow = g->sws.qrow;
     p.stats = g->d_stats;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ev) {

@@ -49,6 +49,7 @@ struct SlicesParams {
     double *bcp;            // private BC rows (slices_kernel)
     double *bc;             // shared BC vector (slices_lowdeg_kernel adds into it)
     const int4 *ell4;       // max degree <= 4: neighbours padded with -1, one 16-byte load per vertex
+    int4 *qrow;             // [gridDim.x][n] ELL rows in queue order (BC_SM_QROW), else null
     unsigned *bm;           // global bitmaps [gridDim.x][2][bm_words] (when not in shared memory)
     int bm_words;
     unsigned long long *stats;  // [4] reached, adjacency, dag edges, depth sum
@@ -489,6 +490,9 @@ __device__ __forceinline__ unsigned lowdeg_code(int L) { return (unsigned)(L % 3
 #ifndef BC_SM_MINB
 #define BC_SM_MINB 2  // two CTAs per SM (64 KB state each)
 #endif
+#ifndef BC_SM_QROW
+#define BC_SM_QROW 0  // discoverer copies the new vertex's ELL row next to its queue slot
+#endif
 // A vertex's neighbour "row": the int4 of neighbour ids (ELL) or, for CSR
 // reads, the vertex id in .x.
 template <bool ELL>
@@ -516,6 +520,8 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
     double *sc = p.sigma + blockIdx.x * n;  // sigma, then coef (in place)
     int *Q = p.queue + blockIdx.x * n;
     int *loff = p.loff + blockIdx.x * (n + 2);
+    constexpr bool QROW = ELL && BC_SM_QROW;
+    int4 *QR = QROW ? p.qrow + blockIdx.x * n : nullptr;
     const int lane = lane_id();
     unsigned long long st_reach = 0, st_adj = 0, st_dag = 0, st_dsum = 0;
     for (int i = tid; i < nw; i += BC_SM_NT) f2[i] = 0u;
@@ -551,7 +557,7 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
             const unsigned cn = lowdeg_code(L + 1), cp = lowdeg_code(L + 2);  // (L + 2) mod 3 == (L - 1) mod 3
             for (int i = qs + tid; i < qe; i += BC_SM_NT) {
                 const int v = Q[i];
-                const int4 row = lowdeg_row<ELL>(p, v);
+                const int4 row = (QROW && L >= 1) ? QR[i] : lowdeg_row<ELL>(p, v);
                 if (L >= 1) {
                     double sg = 0.0;
                     lowdeg_row_nbrs<ELL>(p, row, [&](const int *u) {
@@ -583,7 +589,11 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
                             int base = 0;
                             if (lane == leader) base = atomicAdd(&sm.tail, __popc(bal));
                             base = __shfl_sync(am, base, leader);
-                            if (won) Q[base + __popc(bal & ((1u << lane) - 1u))] = w[k];
+                            if (won) {
+                                const int pos = base + __popc(bal & ((1u << lane) - 1u));
+                                Q[pos] = w[k];
+                                if constexpr (QROW) QR[pos] = p.ell4[w[k]];
+                            }
                         }
                     }
                 });
@@ -609,7 +619,7 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
             b = loff[Lmax + 1];
             if (a + tid < b) {
                 wq = Q[a + tid];
-                rq = lowdeg_row<ELL>(p, wq);
+                rq = QROW ? QR[a + tid] : lowdeg_row<ELL>(p, wq);
                 sq = sc[wq];
             }
         }
@@ -618,7 +628,7 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
             for (int i = a + tid; i < b; i += BC_SM_NT) {
                 const bool first = i == a + tid;
                 const int w = first ? wq : Q[i];
-                const int4 row = first ? rq : lowdeg_row<ELL>(p, w);
+                const int4 row = first ? rq : (QROW ? QR[i] : lowdeg_row<ELL>(p, w));
                 const double sg = first ? sq : sc[w];
                 double acc = 0.0;
                 lowdeg_row_nbrs<ELL>(p, row, [&](const int *v) {
@@ -646,7 +656,7 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
             wq = -1;
             if (L - 1 >= 1 && an + tid < bn) {
                 wq = Q[an + tid];
-                rq = lowdeg_row<ELL>(p, wq);
+                rq = QROW ? QR[an + tid] : lowdeg_row<ELL>(p, wq);
                 sq = sc[wq];
             }
             __syncthreads();
