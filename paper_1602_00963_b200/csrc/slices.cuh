@@ -495,9 +495,31 @@ __device__ __forceinline__ unsigned lowdeg_code(int L) { return (unsigned)(L % 3
 #endif
 // A vertex's neighbour "row": the int4 of neighbour ids (ELL) or, for CSR
 // reads, the vertex id in .x.
+#ifndef BC_SM_L2HINT
+#define BC_SM_L2HINT 0  // ELL rows evict-last and queue slots evict-first in L2
+#endif
+__device__ __forceinline__ int4 ld_row_keep(const int4 *p) {
+#if BC_SM_L2HINT
+    int4 r;
+    asm volatile("{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+                 "ld.global.nc.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], pol;\n\t}"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+#else
+    return *p;
+#endif
+}
+__device__ __forceinline__ void st_slot_stream(int *p, int v) {
+#if BC_SM_L2HINT
+    asm volatile("{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+                 "st.global.L2::cache_hint.b32 [%0], %1, pol;\n\t}" ::"l"(p), "r"(v) : "memory");
+#else
+    *p = v;
+#endif
+}
 template <bool ELL>
 __device__ __forceinline__ int4 lowdeg_row(const SlicesParams &p, int v) {
-    if constexpr (ELL) return p.ell4[v];
+    if constexpr (ELL) return ld_row_keep(p.ell4 + v);
     else return make_int4(v, 0, 0, 0);
 }
 template <bool ELL, typename F>
@@ -591,7 +613,7 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
                             base = __shfl_sync(am, base, leader);
                             if (won) {
                                 const int pos = base + __popc(bal & ((1u << lane) - 1u));
-                                Q[pos] = w[k];
+                                st_slot_stream(Q + pos, w[k]);
                                 if constexpr (QROW) QR[pos] = p.ell4[w[k]];
                             }
                         }
