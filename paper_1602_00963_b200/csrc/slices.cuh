@@ -490,6 +490,9 @@ __device__ __forceinline__ unsigned lowdeg_code(int L) { return (unsigned)(L % 3
 #ifndef BC_SM_MINB
 #define BC_SM_MINB 2  // two CTAs per SM (64 KB state each)
 #endif
+#ifndef BC_SM_AGG
+#define BC_SM_AGG 1  // one tail atomic per warp per neighbour group (test-and-sets issued together)
+#endif
 #ifndef BC_SM_QROW
 #define BC_SM_QROW 0  // discoverer copies the new vertex's ELL row next to its queue slot
 #endif
@@ -596,6 +599,44 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
                     sc[v] = sg;
                 }
                 lowdeg_row_nbrs<ELL>(p, row, [&](const int *w) {
+#if BC_SM_AGG
+                    // all test-and-sets of the group first (independent shared atomics),
+                    // then one tail atomic per warp for the group's winners
+                    bool won[BC_LD_GRP];
+#pragma unroll
+                    for (int k = 0; k < BC_LD_GRP; ++k) {
+                        won[k] = false;
+                        if (w[k] >= 0) {
+                            const int sh = (w[k] & 15) * 2;
+                            won[k] = ((f2[w[k] >> 4] >> sh) & 3u) == 0u &&
+                                     ((atomicOr(&f2[w[k] >> 4], cn << sh) >> sh) & 3u) == 0u;
+                        }
+                    }
+                    const unsigned am = __activemask();
+                    unsigned bal[BC_LD_GRP];
+                    int tot = 0;
+#pragma unroll
+                    for (int k = 0; k < BC_LD_GRP; ++k) {
+                        bal[k] = __ballot_sync(am, won[k]);
+                        tot += __popc(bal[k]);
+                    }
+                    if (tot) {
+                        const int leader = __ffs(am) - 1;
+                        int base = 0;
+                        if (lane == leader) base = atomicAdd(&sm.tail, tot);
+                        base = __shfl_sync(am, base, leader);
+                        const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+                        for (int k = 0; k < BC_LD_GRP; ++k) {
+                            if (won[k]) {
+                                const int pos = base + __popc(bal[k] & lt);
+                                st_slot_stream(Q + pos, w[k]);
+                                if constexpr (QROW) QR[pos] = p.ell4[w[k]];
+                            }
+                            base += __popc(bal[k]);
+                        }
+                    }
+#else
 #pragma unroll
                     for (int k = 0; k < BC_LD_GRP; ++k) {
                         bool won = false;
@@ -618,6 +659,7 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
                             }
                         }
                     }
+#endif
                 });
             }
             __syncthreads();
