@@ -117,8 +117,13 @@ const char *bc_status_string(bc_status s);
 const char *bc_last_error(void); /* thread-local detail of the last failure */
 
 /*
- * bc_sssp -- verification only (not timed): one source on the ORIGINAL
- * (unpruned) graph.  All outputs are HOST arrays of length n (each nullable):
+ * bc_sssp -- verification only (not timed): one source, exact integer sigma
+ * (uint64 rows, W = 1 lane, the caller-id CSR).  On an unpruned handle it
+ * traverses the graph; on a PRUNED handle it traverses the residual graph
+ * (Eq.(5) recursion) and fills the removed vertices as bc_set_capture
+ * describes, so the outputs describe the unpruned graph either way; a
+ * removed source is BC_ERR_INVALID.  All outputs are HOST arrays of length n
+ * (each nullable):
  *   depth           int32, -1 if unreachable                  (Alg.2 d[])
  *   sigma           uint64 shortest-path counts (exact integer path)
  *   sigma_overflow  uint8, 1 where sigma (or a predecessor's) exceeded 2^64-1
@@ -127,6 +132,41 @@ const char *bc_last_error(void); /* thread-local detail of the last failure */
  */
 bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma,
                   uint8_t *sigma_overflow, double *delta);
+
+/*
+ * bc_set_capture -- verification only (not timed): the NEXT bc_compute on
+ * this handle also records the per-source Brandes state of each captured
+ * source, as computed by that call's production kernels -- the same batch,
+ * lane width, sigma-row tier (16/32/64 bits), relabelled CSR, hub split and
+ * concurrent pipelines (lanes mode), or the same one-source-per-CTA kernel
+ * (slices mode, CAP instantiation).  For i < n_cap and every vertex v
+ * (caller ids), with s = sources[i]:
+ *   depth[i*n + v]  int32   d(s, v), -1 if unreachable       (Alg.2 d[])
+ *   sigma[i*n + v]  double  sigma_sv: the integer the tier's rows held,
+ *                           converted (exact below 2^53; fp64 rows round
+ *                           above it, like the oracle's fp64 sigma)     (Alg.1 line 20)
+ *   delta[i*n + v]  double  delta_s(v) (Eq.(2)); 0 at s
+ *                           and at unreached vertices
+ *   tier[i]         int32   bits of the sigma rows the source's batch
+ *                           completed with (16, 32, 64; slices mode: 64);
+ *                           0 for a source without a traversal (isolated,
+ *                           or residual-isolated on a pruned handle)
+ * On a PRUNED handle the outputs describe the UNPRUNED graph (as bc_compute's
+ * scores do, R13): a removed vertex u with neighbour p gets
+ * d(s,u) = d(s,p) + 1, sigma_su = sigma_sp, delta_s(u) = 0, and a kept
+ * vertex v != s gets delta_s(v) = delta'_s(v) + omega(v) (Eq.(5)).
+ *   sources   HOST int32[n_cap], distinct; each must be in the source set of
+ *             the next bc_compute (else that call fails with BC_ERR_INVALID).
+ *   n_cap     0 .. BC_CAPTURE_MAX; 0 cancels a pending capture.
+ *   depth, sigma, delta, tier   HOST arrays ([n_cap*n], [n_cap]), each
+ *             nullable; owned by the caller and written during the next
+ *             bc_compute, which then returns only after they are filled.
+ * The capture applies to one bc_compute call, successful or not.  Device
+ * memory: 36 bytes per captured source per vertex, allocated on first use.
+ */
+#define BC_CAPTURE_MAX 4096
+bc_status bc_set_capture(bc_graph *g, const int32_t *sources, int64_t n_cap, int32_t *depth, double *sigma,
+                         double *delta, int32_t *tier);
 
 /* Tuning options (bc_set_option).  Values are validated. */
 typedef enum {

@@ -127,13 +127,32 @@ class Graph:
         return out
 
     def sssp(self, source: int):
-        """(depth int32, sigma uint64, overflow uint8, delta float64) on the unpruned graph."""
+        """(depth int32, sigma uint64, overflow uint8, delta float64) of the
+        unpruned graph (a pruned handle traverses the residual graph and
+        fills the removed vertices)."""
         d = np.empty(self.n, np.int32)
         s = np.empty(self.n, np.uint64)
         o = np.empty(self.n, np.uint8)
         de = np.empty(self.n, np.float64)
         _check(_L.load().bc_sssp(self._h, int(source), _ptr(d), _ptr(s), _ptr(o), _ptr(de)))
         return d, s, o, de
+
+    def compute_captured(self, sources=None, capture=(), out=None, stream=None):
+        """bc_set_capture + bc_compute: the BC over ``sources`` (as
+        :meth:`compute`) and, for each vertex of ``capture``, the per-source
+        state the production kernels of that call computed:
+        ``(bc, depth int32[c, n], sigma float64[c, n], delta float64[c, n],
+        tier int32[c])``."""
+        cap = np.ascontiguousarray(capture, dtype=np.int32)
+        c = len(cap)
+        depth = np.empty((c, self.n), np.int32)
+        sigma = np.empty((c, self.n), np.float64)
+        delta = np.empty((c, self.n), np.float64)
+        tier = np.empty(max(c, 1), np.int32)
+        _check(_L.load().bc_set_capture(self._h, _ptr(cap) if c else None, c, _ptr(depth), _ptr(sigma),
+                                        _ptr(delta), _ptr(tier)))
+        bc = self.compute(sources, out=out, stream=stream)
+        return bc, depth, sigma, delta, tier[:c]
 
     def set_option(self, option: int, value: int):
         _check(_L.load().bc_set_option(self._h, int(option), int(value)))

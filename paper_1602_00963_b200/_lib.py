@@ -79,6 +79,7 @@ SIGNATURES = {
     "bc_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "bc_last_error": (ctypes.c_char_p, []),
     "bc_sssp": (ctypes.c_int, [_vp, _i32, _vp, _vp, _vp, _vp]),
+    "bc_set_capture": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "bc_set_option": (ctypes.c_int, [_vp, ctypes.c_int, _i64]),
     "bc_get_stats": (ctypes.c_int, [_vp, ctypes.POINTER(bc_stats)]),
     "bc_get_pruning": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, ctypes.POINTER(_i64)]),
@@ -93,7 +94,9 @@ def load(auto_build: bool = True):
     """Load (building first if stale) the CUDA library; raises if unavailable."""
     global _lib
     if _lib is None:
-        if auto_build and needs_build():
+        # an explicitly chosen library (BC_SO, e.g. an experiment build with
+        # its own -D defines) is never rebuilt with the default flags
+        if auto_build and not os.environ.get("BC_SO") and needs_build():
             build()
         if not os.path.exists(SO):
             raise ImportError(f"libbcb200.so not built ({SO}); run __graft_entry__.build()")

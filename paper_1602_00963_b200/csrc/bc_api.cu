@@ -124,6 +124,8 @@ struct LaneWS {
     double *lane_ns = nullptr;
     void *part = nullptr;  // split-slot partial sums [max CTAs][BC_NW][2][K]
     double *A = nullptr;   // push-backward accumulators [n][K], zero between batches
+    int *lane_cap = nullptr;       // [K] capture slot of each lane or -1 (bc_set_capture)
+    uint64_t *capmask = nullptr;   // [8] lanes of the batch that are captured
     uint64_t **d_lv = nullptr;  // device copies of the level mask / row pointers (2-degree derive)
     void **d_rows = nullptr;
     int dptr_cap = 0;
@@ -133,6 +135,8 @@ struct LaneWS {
         dptr_cap = 0;
         dfree(part);
         dfree(A);
+        dfree(lane_cap);
+        dfree(capmask);
         for (auto &q : slev) dfree(q);
         slev.clear();
         dfree(seen);
@@ -265,6 +269,34 @@ struct bc_graph {
     int64_t cl_cap = 0;
     void *cl_tmp = nullptr;
     size_t cl_tmp_bytes = 0;
+    // verification capture (bc_set_capture), consumed by the next bc_compute
+    struct Capture {
+        std::vector<int> src;              // original ids
+        std::vector<uint8_t> trivial;      // per slot: residual-isolated source (no traversal)
+        int32_t *h_depth = nullptr;        // caller's host arrays [ncap][n]
+        double *h_sigma = nullptr, *h_delta = nullptr;
+        int32_t *h_tier = nullptr;         // [ncap]
+        int *d_vslot = nullptr;            // [n] compute ids -> slot or -1
+        int *d_src = nullptr;              // [ncap] original ids
+        int *d_depth = nullptr, *d_tier = nullptr;  // compute ids
+        double *d_sigma = nullptr, *d_delta = nullptr;
+        int *o_depth = nullptr;            // original ids
+        double *o_sigma = nullptr, *o_delta = nullptr;
+        int64_t cap = 0;                   // allocated slots
+        void release() {
+            dfree(d_vslot);
+            dfree(d_src);
+            dfree(d_depth);
+            dfree(d_tier);
+            dfree(d_sigma);
+            dfree(d_delta);
+            dfree(o_depth);
+            dfree(o_sigma);
+            dfree(o_delta);
+            cap = 0;
+            src.clear();
+        }
+    } capt;
     DevCSR &cur() { return pruned ? res : orig; }
 };
 
@@ -664,6 +696,8 @@ bc_status ensure_ws(bc_graph *g, LaneWS &ws, int W, bool verify, int nhub, int r
         if (verify) CK(dalloc(&ws.ovf, n * W));
         CK(dalloc(&ws.lane_w1, K));
         CK(dalloc(&ws.lane_ns, K));
+        CK(dalloc(&ws.lane_cap, K));
+        CK(dalloc(&ws.capmask, 8));
         CK(dalloc((double **)&ws.part, (size_t)g->num_sms * 8 * BC_NW * 2 * K));
         if (!verify) {
             CK(dalloc(&ws.A, n * K));
@@ -723,9 +757,19 @@ bc_status ensure_level(bc_graph *g, LaneWS &ws, int L) {
     return BC_OK;
 }
 
-__global__ void lane_setup_kernel(const int *src, int nl, int K, const uint32_t *omega, double *w1) {
+// per lane: 1 + omega(source) and, with a capture active, the capture slot
+// of the lane's source (capmask pre-zeroed)
+__global__ void lane_setup_kernel(const int *src, int nl, int K, const uint32_t *omega, double *w1,
+                                  const int *cap_vslot, int *lane_cap, unsigned long long *capmask) {
     int l = blockIdx.x * blockDim.x + threadIdx.x;
-    if (l < K) w1[l] = (l < nl && omega && src[l] >= 0) ? 1.0 + (double)omega[src[l]] : 1.0;
+    if (l < K) {
+        w1[l] = (l < nl && omega && src[l] >= 0) ? 1.0 + (double)omega[src[l]] : 1.0;
+        if (cap_vslot) {
+            const int c = (l < nl && src[l] >= 0) ? cap_vslot[src[l]] : -1;
+            lane_cap[l] = c;
+            if (c >= 0) atomicOr(capmask + (l >> 6), 1ull << (l & 63));
+        }
+    }
 }
 
 // occupancy-derived grid for the level kernels
@@ -746,7 +790,12 @@ struct BatchCtx {
     const int *src;         // device, nl entries
     int nl;
     cudaStream_t st;
-    double *dbg_delta;      // lane-0 delta (verification)
+    // verification capture (nullable): slot per source (compute ids of this
+    // CSR), per-source outputs [slot][n]; cap_depth == nullptr: delta only
+    const int *cap_vslot;
+    int *cap_depth;
+    double *cap_sigma, *cap_delta;
+    int *cap_tier;
     bool run_backward;
     bool endpoint;
     std::vector<uint64_t *> *lvl_out;  // verification: level masks used (nullable)
@@ -796,7 +845,8 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
     p.part = ws.part;
     p.ntiles = c.csr->ntiles;
     p.tile_vs = c.csr->tile_vs;
-    p.dbg_delta = nullptr;
+    p.lane_cap = nullptr;
+    p.cap_delta = nullptr;
     p.narrow_ovf = x.d_work_ctr + 2;  // fixed address (d_flags may grow and move with the level count)
     using RT = typename RowOf<SigT>::t;
     // integer rows with a limit (16-bit or 32-bit): re-run the batch wider on overflow
@@ -805,7 +855,9 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
 
     const size_t mbytes = (size_t)n * W * sizeof(uint64_t);
     CK(ensure_level(g, ws, 1));
-    lane_setup_kernel<<<(K + 255) / 256, 256, 0, st>>>(c.src, c.nl, K, c.omega, ws.lane_w1);
+    if (c.cap_vslot) CU(cudaMemsetAsync(ws.capmask, 0, 8 * sizeof(uint64_t), st));
+    lane_setup_kernel<<<(K + 255) / 256, 256, 0, st>>>(c.src, c.nl, K, c.omega, ws.lane_w1, c.cap_vslot, ws.lane_cap,
+                                                       (unsigned long long *)ws.capmask);
     CU(cudaMemsetAsync(ws.seen, 0, mbytes, st));
     if (ws.ovf) CU(cudaMemsetAsync(ws.ovf, 0, mbytes, st));
     CU(cudaMemsetAsync(level_ptr(g, ws, 0), 0, mbytes, st));
@@ -941,6 +993,16 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
         }
         Lb = Lmax + 1;
     }
+    if (c.cap_vslot && c.cap_depth) {
+        // verification capture: depth and sigma of the captured lanes, from
+        // the level masks and sigma rows of this (completed) forward
+        const unsigned vb = (unsigned)(((int64_t)n + 255) / 256);
+        for (int l = 0; l <= Lb; ++l)
+            cap_extract_kernel<W, RT><<<vb, 256, 0, st>>>(n, l, level_ptr(g, ws, l), (const RT *)ws.slev[l], ws.lane_cap,
+                                                          ws.capmask, c.cap_depth, c.cap_sigma);
+        cap_tier_kernel<<<(K + 255) / 256, 256, 0, st>>>(K, ws.lane_cap, 8 * (int)sizeof(RT), c.cap_tier);
+        CU(cudaGetLastError());
+    }
     if constexpr (!std::is_same<SigT, unsigned long long>::value) {
         bool pulled = false;
         if constexpr (std::is_same<SigT, double>::value) {
@@ -952,7 +1014,8 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
             const int gridb = level_grid(g, kb, units, SMEM);
             auto khb = lanes_hub_finalize<W, SigT, true>;
             cudaFuncSetAttribute(khb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-            p.dbg_delta = c.dbg_delta;
+            p.lane_cap = c.cap_vslot ? ws.lane_cap : nullptr;
+            p.cap_delta = c.cap_delta;
             for (int l = Lb; l >= 1; --l) {
                 p.level = l;
                 p.S_cur = ws.slev[l];
@@ -992,7 +1055,8 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
             const int gridp = std::max(1, std::min(g->num_sms * std::max(1, occp), units));
             const unsigned fin_blocks = (unsigned)std::min<int64_t>(((int64_t)n * 32 + BC_NT - 1) / BC_NT,
                                                                     (int64_t)g->num_sms * 8);
-            p.dbg_delta = c.dbg_delta;
+            p.lane_cap = c.cap_vslot ? ws.lane_cap : nullptr;
+            p.cap_delta = c.cap_delta;
             for (int l = Lb; l >= 1; --l) {
                 p.level = l;
                 p.S_cur = ws.slev[l];
@@ -1086,7 +1150,7 @@ bc_status ensure_slices(bc_graph *g, int rows, bool full) {
 
 // One CTA per source (persistent grid), for long-diameter graphs.
 bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStream_t st,
-                     std::vector<cudaEvent_t> *ev) {
+                     std::vector<cudaEvent_t> *ev, bool cap) {
 #ifndef BC_SLICES_SMEM_BM
 #define BC_SLICES_SMEM_BM 0  // shared-memory bitmaps cost occupancy; global (L2-resident) ones measured faster
 #endif
@@ -1107,9 +1171,14 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
     const bool sm2 = lowdeg && BC_SLICES_SM2 && sm2_bytes <= (size_t)BC_SLICES_SM2_MAXB;
     const bool smem_bm = !lowdeg && BC_SLICES_SMEM_BM && g->n <= (int64_t)SLICES_SMEM_BM_WORDS * 32;
     const size_t dsm = sm2 ? sm2_bytes : smem_bm ? 2 * SLICES_SMEM_BM_WORDS * sizeof(unsigned) : 0;
-    auto kern = sm2      ? (ell ? slices_lowdeg_sm_kernel<true> : slices_lowdeg_sm_kernel<false>)
-                : lowdeg ? (ell ? slices_lowdeg_kernel<true> : slices_lowdeg_kernel<false>)
-                         : (smem_bm ? slices_kernel<true> : slices_kernel<false>);
+    // CAP instantiations (verification capture, bc_set_capture) keep the
+    // capture stores out of the timed kernels
+    auto kern = sm2      ? (ell ? (cap ? slices_lowdeg_sm_kernel<true, true> : slices_lowdeg_sm_kernel<true>)
+                                : (cap ? slices_lowdeg_sm_kernel<false, true> : slices_lowdeg_sm_kernel<false>))
+                : lowdeg ? (ell ? (cap ? slices_lowdeg_kernel<true, true> : slices_lowdeg_kernel<true>)
+                                : (cap ? slices_lowdeg_kernel<false, true> : slices_lowdeg_kernel<false>))
+                         : (smem_bm ? (cap ? slices_kernel<true, true> : slices_kernel<true>)
+                                    : (cap ? slices_kernel<false, true> : slices_kernel<false>));
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
     int occ = 1;
     const int nt = sm2 ? BC_SM_NT : lowdeg ? BC_SL_NT : BC_NT;
@@ -1142,6 +1211,12 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
     p.ell4 = ell ? g->sws.ell : nullptr;
     p.qrow = g->sws.qrow;
     p.stats = g->d_stats;
+    if (cap) {
+        p.cap_vslot = g->capt.d_vslot;
+        p.cap_depth = g->capt.d_depth;
+        p.cap_sigma = g->capt.d_sigma;
+        p.cap_delta = g->capt.d_delta;
+    }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ev) {
         cudaEventCreate(&e0);
@@ -1160,6 +1235,84 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
     g->last.kernel_launches += lowdeg ? 1 : 2;
     g->last.batches += 1;
     g->last.lanes = 1;
+    return BC_OK;
+}
+
+// ---- verification capture (bc_set_capture)
+// Checks that every captured source is in this call's source set (trav /
+// triv, original ids), sizes the buffers and maps the sources to slots in
+// the compute CSR's ids.  Runs before the batches are enqueued.
+bc_status capture_prepare(bc_graph *g, const int32_t *sources, int64_t num_sources, const std::vector<int> &trav,
+                          cudaStream_t st) {
+    auto &cp = g->capt;
+    const int64_t n = g->n, nc = (int64_t)cp.src.size();
+    // 1: in the call's source set, 2: and traversed
+    std::vector<uint8_t> in_set((size_t)n, sources ? 0 : 1);
+    if (sources)
+        for (int64_t i = 0; i < num_sources; ++i) in_set[sources[i]] = 1;
+    else if (g->pruned)
+        for (int64_t v = 0; v < n; ++v)
+            if (g->h_removed[v]) in_set[v] = 0;
+    for (int v : trav) in_set[v] = 2;
+    for (int s : cp.src)
+        if (!in_set[s]) return fail(BC_ERR_INVALID, "captured source %d is not in the source set of this call", s);
+    cp.trivial.assign((size_t)nc, 0);
+    for (int64_t c = 0; c < nc; ++c) cp.trivial[c] = in_set[cp.src[c]] != 2;
+    if (cp.cap < nc || !cp.d_vslot) {
+        const int64_t keep_n = nc;
+        std::vector<int> keep = cp.src;
+        cp.release();
+        cp.src = keep;
+        CK(dalloc(&cp.d_vslot, (size_t)n));
+        CK(dalloc(&cp.d_src, (size_t)keep_n));
+        CK(dalloc(&cp.d_tier, (size_t)keep_n));
+        CK(dalloc(&cp.d_depth, (size_t)(keep_n * n)));
+        CK(dalloc(&cp.d_sigma, (size_t)(keep_n * n)));
+        CK(dalloc(&cp.d_delta, (size_t)(keep_n * n)));
+        CK(dalloc(&cp.o_depth, (size_t)(keep_n * n)));
+        CK(dalloc(&cp.o_sigma, (size_t)(keep_n * n)));
+        CK(dalloc(&cp.o_delta, (size_t)(keep_n * n)));
+        cp.cap = keep_n;
+    }
+    std::vector<int> vslot((size_t)n, -1);
+    for (int64_t c = 0; c < nc; ++c) vslot[g->run.h_inv[cp.src[c]]] = (int)c;
+    CU(cudaMemcpyAsync(cp.d_vslot, vslot.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(cp.d_src, cp.src.data(), (size_t)nc * 4, cudaMemcpyHostToDevice, st));
+    CU(cudaMemsetAsync(cp.d_depth, 0xff, (size_t)(nc * n) * 4, st));
+    CU(cudaMemsetAsync(cp.d_sigma, 0, (size_t)(nc * n) * 8, st));
+    CU(cudaMemsetAsync(cp.d_delta, 0, (size_t)(nc * n) * 8, st));
+    CU(cudaMemsetAsync(cp.d_tier, 0, (size_t)nc * 4, st));
+    CU(cudaStreamSynchronize(st));  // vslot is pageable host memory
+    return BC_OK;
+}
+
+// After the batches: compute ids -> original ids, the sources' own entries,
+// the removed vertices of a pruned handle, then the copies to the caller's
+// host arrays (synchronous at the end of bc_compute).
+bc_status capture_finish(bc_graph *g, cudaStream_t st, bool slices) {
+    auto &cp = g->capt;
+    const int64_t n = g->n, nc = (int64_t)cp.src.size();
+    const unsigned blocks = (unsigned)((nc * n + 255) / 256);
+    const int *inv = g->run.inv;
+    cap_unpermute_kernel<int><<<blocks, 256, 0, st>>>(nc, (int)n, inv, cp.d_depth, cp.o_depth);
+    cap_unpermute_kernel<double><<<blocks, 256, 0, st>>>(nc, (int)n, inv, cp.d_sigma, cp.o_sigma);
+    cap_unpermute_kernel<double><<<blocks, 256, 0, st>>>(nc, (int)n, inv, cp.d_delta, cp.o_delta);
+    cap_sources_kernel<double><<<(unsigned)((nc + 255) / 256), 256, 0, st>>>((int)nc, (int)n, cp.d_src, cp.o_depth,
+                                                                          cp.o_sigma);
+    if (g->pruned)
+        cap_prune_fill_kernel<double><<<blocks, 256, 0, st>>>(nc, (int)n, g->orig.rp, g->orig.col, g->removed, g->omega,
+                                                              cp.o_depth, cp.o_sigma, cp.o_delta, nullptr);
+    CU(cudaGetLastError());
+    if (cp.h_depth) CU(cudaMemcpyAsync(cp.h_depth, cp.o_depth, (size_t)(nc * n) * 4, cudaMemcpyDeviceToHost, st));
+    if (cp.h_sigma) CU(cudaMemcpyAsync(cp.h_sigma, cp.o_sigma, (size_t)(nc * n) * 8, cudaMemcpyDeviceToHost, st));
+    if (cp.h_delta) CU(cudaMemcpyAsync(cp.h_delta, cp.o_delta, (size_t)(nc * n) * 8, cudaMemcpyDeviceToHost, st));
+    if (cp.h_tier) {
+        if (slices) {  // one fp64 sigma slot per vertex: the 64-bit tier
+            for (int64_t c = 0; c < nc; ++c) cp.h_tier[c] = cp.trivial[c] ? 0 : 64;
+        } else {
+            CU(cudaMemcpyAsync(cp.h_tier, cp.d_tier, (size_t)nc * 4, cudaMemcpyDeviceToHost, st));
+        }
+    }
     return BC_OK;
 }
 
@@ -1234,6 +1387,7 @@ bc_status bc_destroy(bc_graph *g) {
         g->vctx.release();
         g->sctx.release();
         g->sws.release();
+        g->capt.release();
         dfree(g->d_stats);
         dfree(g->d_work_ctr);
         dfree(g->d_src);
@@ -1361,6 +1515,7 @@ bc_status bc_prune_degree1(bc_graph *g, int64_t *out_removed) {
     dfree(rdeg);
     dfree(tot);
     g->pruned = true;
+    CK(build_layout(g, g->res, st));  // bc_sssp traverses the residual graph in caller ids
     CK(build_run(g));
     if (out_removed) {
         int64_t r = 0;
@@ -1384,6 +1539,7 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
             DeviceGuard dg(g->device);
             g->hub_deg = (int)value;
             CK(build_layout(g, g->orig, g->own_stream));
+            if (g->pruned) CK(build_layout(g, g->res, g->own_stream));
             CK(build_run(g));
             return BC_OK;
         }
@@ -1431,6 +1587,29 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
     return fail(BC_ERR_INVALID, "unknown option %d", option);
 }
 
+bc_status bc_set_capture(bc_graph *g, const int32_t *sources, int64_t n_cap, int32_t *depth, double *sigma,
+                         double *delta, int32_t *tier) {
+    if (!g) return fail(BC_ERR_INVALID, "NULL handle");
+    if (n_cap < 0 || n_cap > BC_CAPTURE_MAX) return fail(BC_ERR_INVALID, "n_cap=%lld out of range [0, %d]", (long long)n_cap, BC_CAPTURE_MAX);
+    g->capt.src.clear();
+    if (n_cap == 0) return BC_OK;
+    if (!sources) return fail(BC_ERR_INVALID, "sources is NULL");
+    std::vector<int> src((size_t)n_cap);
+    for (int64_t i = 0; i < n_cap; ++i) {
+        const int s = sources[i];
+        if (s < 0 || s >= g->n) return fail(BC_ERR_INVALID, "captured source %d out of range", s);
+        for (int64_t j = 0; j < i; ++j)
+            if (src[j] == s) return fail(BC_ERR_INVALID, "duplicate captured source %d", s);
+        src[i] = s;
+    }
+    g->capt.src = src;
+    g->capt.h_depth = depth;
+    g->capt.h_sigma = sigma;
+    g->capt.h_delta = delta;
+    g->capt.h_tier = tier;
+    return BC_OK;
+}
+
 bc_status bc_get_stats(const bc_graph *g, bc_stats *out) {
     if (!g || !out) return fail(BC_ERR_INVALID, "NULL argument");
     *out = g->last;
@@ -1467,6 +1646,16 @@ bc_status bc_get_pruning(const bc_graph *g, uint32_t *omega, uint8_t *removed, i
 
 bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, double *out_bc, void *cuda_stream) {
     if (!g) return fail(BC_ERR_INVALID, "NULL handle");
+    // a capture (bc_set_capture) applies to this call only, success or not
+    const bool capture = !g->capt.src.empty();
+    struct CaptureReset {
+        bc_graph *g;
+        ~CaptureReset() {
+            g->capt.src.clear();
+            g->capt.h_depth = g->capt.h_tier = nullptr;
+            g->capt.h_sigma = g->capt.h_delta = nullptr;
+        }
+    } capture_reset{g};
     if (!out_bc) return fail(BC_ERR_INVALID, "out_bc is NULL");
     if (num_sources < 0 || (num_sources > 0 && !sources)) return fail(BC_ERR_INVALID, "bad source list");
     DeviceGuard dg(g->device);
@@ -1496,6 +1685,7 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     cudaStream_t st = cuda_stream ? (cudaStream_t)cuda_stream : g->own_stream;
     if (!g->run_valid) CK(build_run(g));
     DevCSR &run = g->run;
+    if (capture) CK(capture_prepare(g, sources, num_sources, trav, st));
     // batch schedule: compute ids, ascending = degree descending (sources with
     // similar BFS depth profiles share a batch and sit in adjacent lanes)
     for (auto &v : trav) v = run.h_inv[v];
@@ -1610,7 +1800,8 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     CU(cudaMemsetAsync(g->d_bc, 0, (size_t)n * 8, st));
     CU(cudaMemsetAsync(g->d_stats, 0, 8 * sizeof(unsigned long long), st));
     std::vector<cudaEvent_t> ef;
-    if (mode == 2 && !trav.empty()) CK(run_slices(g, run, g->d_src, (int)trav.size(), st, g->profile ? &ef : nullptr));
+    if (mode == 2 && !trav.empty())
+        CK(run_slices(g, run, g->d_src, (int)trav.size(), st, g->profile ? &ef : nullptr, capture));
     if (mode == 1 && !trav.empty()) {
         NS = std::max(1, std::min(NS, (int)plan.size()));
         for (int i = 0; i < NS; ++i) {
@@ -1658,6 +1849,13 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
                     c.st = xs;
                     c.run_backward = true;
                     c.endpoint = true;
+                    if (capture) {
+                        c.cap_vslot = g->capt.d_vslot;
+                        c.cap_depth = g->capt.d_depth;
+                        c.cap_sigma = g->capt.d_sigma;
+                        c.cap_delta = g->capt.d_delta;
+                        c.cap_tier = g->capt.d_tier;
+                    }
                     x.last.batches += 1;
                     // narrow sigma first (16-bit rows, exact integers); a batch whose sigma
                     // overflows is re-run with fp64 rows from scratch (nothing of it was
@@ -1753,6 +1951,7 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
         CU(cudaMemcpyAsync(out_bc, g->d_bc2, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
     }
     g->last.kernel_launches += 1;
+    if (capture) CK(capture_finish(g, st, mode == 2));
     if (g->profile) cudaEventRecord(t1, st);
     CU(cudaStreamSynchronize(st));
     g->last.reached = (int64_t)hst[0];
@@ -1784,10 +1983,17 @@ bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma, 
                   double *delta) {
     if (!g) return fail(BC_ERR_INVALID, "NULL handle");
     if (source < 0 || source >= g->n) return fail(BC_ERR_INVALID, "source %d out of range", source);
+    if (g->pruned && g->h_removed[source])
+        return fail(BC_ERR_INVALID, "source %d was removed by 1-degree pruning", source);
     DeviceGuard dg(g->device);
     const int n = (int)g->n;
     cudaStream_t st = g->own_stream;
     bc_stats keep = g->last;
+    // the caller-id CSR the handle computes on: the original graph, or on a
+    // pruned handle the residual graph (the removed vertices are filled in
+    // afterwards from their single neighbour, cap_prune_fill_kernel)
+    DevCSR &csr = g->cur();
+    const uint32_t *omega = g->pruned ? g->omega : nullptr;
     CK(ctx_init(g, g->vctx));
     CK(ensure_ws(g, g->vctx.ws, 1, true, std::max(g->orig.nhub, g->run.nhub)));
     g->vctx.st = st;
@@ -1797,7 +2003,7 @@ bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma, 
         CK(dalloc(&g->d_src, 1));
         g->src_cap = 1;
     }
-    int *d_depth = nullptr;
+    int *d_depth = nullptr, *d_vs = nullptr;
     unsigned long long *d_sig = nullptr;
     uint8_t *d_ov = nullptr;
     double *d_delta = nullptr;
@@ -1805,14 +2011,20 @@ bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma, 
     CK(dalloc(&d_sig, n));
     CK(dalloc(&d_ov, n));
     CK(dalloc(&d_delta, n));
+    CK(dalloc(&d_vs, n));
     CU(cudaMemcpyAsync(g->d_src, &source, 4, cudaMemcpyHostToDevice, st));
     CU(cudaMemsetAsync(d_depth, 0xff, (size_t)n * 4, st));
     CU(cudaMemsetAsync(d_delta, 0, (size_t)n * 8, st));
+    CU(cudaMemsetAsync(d_sig, 0, (size_t)n * 8, st));
+    CU(cudaMemsetAsync(d_ov, 0, (size_t)n, st));
+    // delta of lane 0 through the capture path: source -> slot 0
+    CU(cudaMemsetAsync(d_vs, 0xff, (size_t)n * 4, st));
+    CU(cudaMemsetAsync(d_vs + source, 0, 4, st));
     bc_status s = BC_OK;
-    if (g->orig.h_deg[source] > 0) {
+    if (csr.h_deg[source] > 0) {
         BatchCtx c{};
-        c.csr = &g->orig;
-        c.omega = nullptr;
+        c.csr = &csr;
+        c.omega = omega;
         c.src = g->d_src;
         c.nl = 1;
         c.st = st;
@@ -1825,8 +2037,6 @@ bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma, 
         if (s == BC_OK) {
             for (int l = 0; l <= Lmax; ++l)
                 depth_from_mask_kernel<<<(n + 255) / 256, 256, 0, st>>>(lv[l], n, 1, l, d_depth);
-            CU(cudaMemsetAsync(d_sig, 0, (size_t)n * 8, st));
-            CU(cudaMemsetAsync(d_ov, 0, (size_t)n, st));
             for (int l = 0; l <= Lmax; ++l)
                 gather_level_lane0_kernel<unsigned long long><<<(n + 255) / 256, 256, 0, st>>>(
                     n, lv[l], 1, (const unsigned long long *)g->vctx.ws.slev[l], 64, g->vctx.ws.ovf, d_sig, d_ov);
@@ -1840,25 +2050,24 @@ bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma, 
                 BatchCtx c2 = c;
                 c2.run_backward = true;
                 c2.endpoint = false;
-                c2.dbg_delta = d_delta;
+                c2.cap_vslot = d_vs;
+                c2.cap_delta = d_delta;
                 c2.lvl_out = nullptr;
                 c2.levels_out = nullptr;
                 s = run_batch<1, double>(g, g->sctx, c2, nullptr, nullptr);
             }
         }
     } else {
-        CU(cudaMemsetAsync(d_sig, 0, (size_t)n * 8, st));
-        CU(cudaMemsetAsync(d_ov, 0, (size_t)n, st));
         const int zero = 0;
         CU(cudaMemcpyAsync(d_depth + source, &zero, 4, cudaMemcpyHostToDevice, st));
         const unsigned long long one = 1;
         CU(cudaMemcpyAsync(d_sig + source, &one, 8, cudaMemcpyHostToDevice, st));
     }
+    if (s == BC_OK && g->pruned)
+        cap_prune_fill_kernel<unsigned long long><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+            1, n, g->orig.rp, g->orig.col, g->removed, g->omega, d_depth, d_sig, d_delta, d_ov);
     if (s == BC_OK) {
         CU(cudaGetLastError());
-        if (g->orig.h_deg[source] > 0) {
-            // gather above already ran; nothing else
-        }
         if (depth) CU(cudaMemcpyAsync(depth, d_depth, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
         if (sigma) CU(cudaMemcpyAsync(sigma, d_sig, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
         if (sigma_overflow) CU(cudaMemcpyAsync(sigma_overflow, d_ov, (size_t)n, cudaMemcpyDeviceToHost, st));
@@ -1869,6 +2078,7 @@ bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma, 
     dfree(d_sig);
     dfree(d_ov);
     dfree(d_delta);
+    dfree(d_vs);
     g->last = keep;
     return s;
 }

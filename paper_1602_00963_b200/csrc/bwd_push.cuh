@@ -113,7 +113,7 @@ __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double
             arow[32 * j] = 0.0;
             if constexpr (COEF) row[32 * j] = (1.0 + om + delta) / sv[j];
             contrib += p.lane_w1[32 * j + lane] * (delta + om);
-            if (j == 0 && lane == 0 && p.dbg_delta) p.dbg_delta[x] = delta;
+            cap_delta_put(p, 32 * j + lane, x, delta);
         }
     }
     contrib = warp_sum(contrib);
@@ -217,7 +217,7 @@ struct PushKernel {
                     if (owned) {
                         arow[32 * j] = 0.0;
                         contrib += p.lane_w1[32 * j + lane] * (delta + om);
-                        if (j == 0 && lane == 0 && p.dbg_delta) p.dbg_delta[x] = delta;
+                        cap_delta_put(p, 32 * j + lane, x, delta);
                     }
                 }
             }

@@ -226,4 +226,54 @@ __global__ void unpermute_kernel(int n, const int *inv, const double *bc_new, do
     if (v < n) out[v] = bc_new[inv[v]];
 }
 
+// ---- verification capture (bc_set_capture / bc_sssp) --------------------
+// [ncap][n] arrays from compute ids to original ids: out[c][v] = in[c][inv[v]]
+template <typename T>
+__global__ void cap_unpermute_kernel(long long ncap, int n, const int *inv, const T *in, T *out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ncap * n) return;
+    const long long c = i / n;
+    const int v = (int)(i - c * n);
+    out[i] = in[c * n + inv[v]];
+}
+
+// every captured source s (original ids): d(s, s) = 0, sigma_ss = 1 (also
+// for residual-isolated sources, which are not traversed, R10)
+template <typename ST>
+__global__ void cap_sources_kernel(int ncap, int n, const int *src, int *depth, ST *sigma) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncap) return;
+    depth[(size_t)c * n + src[c]] = 0;
+    sigma[(size_t)c * n + src[c]] = ST(1);
+}
+
+// Pruned handle (original ids): turn the residual traversal's per-source
+// state into the unpruned graph's (R13).  A removed vertex u hangs off its
+// single neighbour p, so d(s, u) = d(s, p) + 1, sigma_su = sigma_sp and
+// delta_s(u) = 0 (u lies on no shortest path between other vertices); a
+// kept vertex v != s reached by s has delta_s(v) = delta'_s(v) + omega(v)
+// (Eq.(5): each of v's removed children adds a pair dependency of 1).  A
+// removed u whose neighbour is removed too (a K2) is not reachable from a
+// kept source.  Kept vertices' depth / sigma are only read here, removed
+// ones only written, so one pass suffices.
+template <typename ST>
+__global__ void cap_prune_fill_kernel(long long ncap, int n, const int *rp, const int *col, const uint8_t *removed,
+                                      const uint32_t *omega, int *depth, ST *sigma, double *delta, uint8_t *ovf) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ncap * n) return;
+    const long long c = i / n;
+    const int u = (int)(i - c * n);
+    const size_t base = (size_t)c * n;
+    if (removed[u]) {
+        const int par = col[rp[u]];
+        const int dp = removed[par] ? -1 : depth[base + par];
+        depth[i] = dp >= 0 ? dp + 1 : -1;
+        sigma[i] = dp >= 0 ? sigma[base + par] : ST(0);
+        if (ovf) ovf[i] = dp >= 0 ? ovf[base + par] : 0;
+        if (delta) delta[i] = 0.0;
+    } else if (delta && depth[i] > 0) {
+        delta[i] += (double)omega[u];
+    }
+}
+
 }  // namespace bcb

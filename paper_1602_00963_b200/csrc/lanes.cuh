@@ -180,13 +180,23 @@ struct LanesParams {
     uint64_t *hub_ovf;           // verify: [nhub][W]
     int ntiles;
     const int *tile_vs;          // [ntiles+1] tile t = vertices [tile_vs[t], tile_vs[t+1]), <= TV of them
-    double *dbg_delta;           // backward: delta of lane 0 (verification), nullable
+    const int *lane_cap;         // verification capture (bc_set_capture): [K] slot of a captured lane or -1, nullable
+    double *cap_delta;           // ... backward: delta_s(x) of captured lanes, [slot][n] (compute ids)
     int *narrow_ovf;             // narrow forward: set when some sigma > 65535 (batch is re-run in fp64)
     uint64_t derived[8];         // 2-degree lanes (NEXT-1): tree derived from lanes l-2, l-1 after the forward
     const int *prev_new;         // forward: flag "level L is non-empty"; 0 -> the launch is a no-op
                                  // (levels are launched one ahead of the host's termination test)
     void *part;                  // [gridDim][BC_NW][2][K] SigT: partial sums of slots split across warps
 };
+
+// verification capture of delta_s(x) (bc_set_capture): lane l of the batch,
+// vertex x; a no-op unless a capture is active (p.lane_cap != nullptr)
+__device__ __forceinline__ void cap_delta_put(const LanesParams &p, int l, int x, double delta) {
+    if (p.lane_cap) {
+        const int c = p.lane_cap[l];
+        if (c >= 0) p.cap_delta[(size_t)c * p.n + x] = delta;
+    }
+}
 
 #ifndef BC_R4
 #define BC_R4 1  // item steps in flight per warp at W = 4 (occupancy beats per-warp MLP)
@@ -413,12 +423,13 @@ struct LanesKernel {
                         const double delta = sg.x * acc[2 * pr];
                         cf.x = (1.0 + om + delta) / sg.x;
                         contrib += p.lane_w1[64 * pr + t2] * (delta + om);
-                        if (pr == 0 && lane == 0 && p.dbg_delta) p.dbg_delta[x] = delta;
+                        cap_delta_put(p, 64 * pr + t2, x, delta);
                     }
                     if (b2 & 2u) {
                         const double delta = sg.y * acc[2 * pr + 1];
                         cf.y = (1.0 + om + delta) / sg.y;
                         contrib += p.lane_w1[64 * pr + t2 + 1] * (delta + om);
+                        cap_delta_put(p, 64 * pr + t2 + 1, x, delta);
                     }
                     *cell = cf;
                 }
@@ -1062,6 +1073,37 @@ __global__ void trivial_sources_kernel(const int *src, int ns, const uint32_t *o
         const double om = (double)omega[s];
         bc[s] += om * (om - 1.0);
     }
+}
+
+// ---- verification capture (bc_set_capture) -----------------------------
+// Depth and sigma of the captured lanes at level L, read from the level mask
+// and the level sigma rows the production forward wrote (thread per vertex;
+// only the captured lanes' bits are visited: capmask = OR of their bits).
+template <int W, typename RT>
+__global__ void cap_extract_kernel(int n, int L, const uint64_t *mask, const RT *rows, const int *lane_cap,
+                                   const uint64_t *capmask, int *cap_depth, double *cap_sigma) {
+    constexpr int K = 64 * W;
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        uint64_t m = capmask[j];
+        if (!m) continue;
+        m &= mask[(size_t)v * W + j];
+        while (m) {
+            const int b = __ffsll((long long)m) - 1;
+            m &= m - 1;
+            const int l = 64 * j + b, c = lane_cap[l];
+            cap_depth[(size_t)c * n + v] = L;
+            cap_sigma[(size_t)c * n + v] = (double)rows[(size_t)v * K + l];
+        }
+    }
+}
+
+// the sigma-row tier (16 / 32 / 64 bits) the captured lanes' batch completed with
+__global__ void cap_tier_kernel(int K, const int *lane_cap, int tier, int *cap_tier) {
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l < K && lane_cap[l] >= 0) cap_tier[lane_cap[l]] = tier;
 }
 
 // verification: depth of lane 0 from the level masks

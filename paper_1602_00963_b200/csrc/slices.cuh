@@ -53,7 +53,25 @@ struct SlicesParams {
     unsigned *bm;           // global bitmaps [gridDim.x][2][bm_words] (when not in shared memory)
     int bm_words;
     unsigned long long *stats;  // [4] reached, adjacency, dag edges, depth sum
+    // verification capture (bc_set_capture; CAP instantiations only): slot of
+    // a source (compute ids) or -1, and the captured per-source state [slot][n]
+    const int *cap_vslot;
+    int *cap_depth;
+    double *cap_sigma, *cap_delta;
 };
+
+// capture of w's depth / sigma / delta in source slot cs (backward commit)
+template <bool CAP>
+__device__ __forceinline__ void slices_cap(const SlicesParams &p, int cs, int w, int L, double sg, double delta) {
+    if constexpr (CAP) {
+        if (cs >= 0) {
+            const size_t o = (size_t)cs * p.n + w;
+            p.cap_depth[o] = L;
+            p.cap_sigma[o] = sg;
+            p.cap_delta[o] = delta;
+        }
+    }
+}
 
 struct SlicesSmem {
     int cd[BC_NT + 1];
@@ -61,6 +79,7 @@ struct SlicesSmem {
     int rs[BC_NT];
     int scan[2 * BC_NW + 2];
     int tail;
+    int cnt[3];  // slices_lowdeg_sm_kernel: appends of level L counted in cnt[L % 3] (rotating, see there)
     int src;
     double red[32];
 };
@@ -94,7 +113,7 @@ __device__ __forceinline__ void slices_chunk_items(const SlicesParams &p, Slices
     __syncthreads();
 }
 
-template <bool SMEM_BM>
+template <bool SMEM_BM, bool CAP = false>
 __global__ void __launch_bounds__(BC_NT) slices_kernel(SlicesParams p) {
     __shared__ SlicesSmem sm;
     extern __shared__ unsigned smbm[];  // 2 * SLICES_SMEM_BM_WORDS when SMEM_BM
@@ -127,6 +146,7 @@ __global__ void __launch_bounds__(BC_NT) slices_kernel(SlicesParams p) {
         __syncthreads();
         if (si >= p.nsrc) break;
         const int s = p.src[si];
+        const int cs = CAP ? p.cap_vslot[s] : -1;
         if (threadIdx.x == 0) {
             vis[s >> 5] |= 1u << (s & 31);
             sigma[s] = 1.0;
@@ -213,6 +233,7 @@ __global__ void __launch_bounds__(BC_NT) slices_kernel(SlicesParams p) {
                 const double sg = sigma[w];
                 const double delta = sg * cf[w];
                 cf[w] = (1.0 + om + delta) / sg;
+                slices_cap<CAP>(p, cs, w, L, sg, delta);
                 const double c = ws1 * (delta + om);
                 if (c != 0.0) bcp[w] += c;
                 st_dsum += (unsigned long long)L;
@@ -305,7 +326,7 @@ __device__ __forceinline__ void lowdeg_nbrs(const SlicesParams &p, int v, F &&f)
     }
 }
 
-template <bool ELL>
+template <bool ELL, bool CAP = false>
 __global__ void __launch_bounds__(BC_SL_NT, BC_SL_MINB) slices_lowdeg_kernel(SlicesParams p) {
     __shared__ SlicesSmem sm;
     const size_t n = (size_t)p.n;
@@ -329,6 +350,7 @@ __global__ void __launch_bounds__(BC_SL_NT, BC_SL_MINB) slices_lowdeg_kernel(Sli
         __syncthreads();
         if (si >= p.nsrc) break;
         const int s = p.src[si];
+        const int cs = CAP ? p.cap_vslot[s] : -1;
         if (threadIdx.x == 0) {
             atomicOr(&vis[s >> 5], 1u << (s & 31));
             atomicOr(&lb0[s >> 5], 1u << (s & 31));
@@ -429,6 +451,7 @@ __global__ void __launch_bounds__(BC_SL_NT, BC_SL_MINB) slices_lowdeg_kernel(Sli
                 const double om = p.omega ? (double)p.omega[w] : 0.0;
                 const double delta = sg * acc;
                 sc[w] = (1.0 + om + delta) / sg;
+                slices_cap<CAP>(p, cs, w, L, sg, delta);
                 const double c = ws1 * (delta + om);
                 if (c != 0.0) atomicAdd(p.bc + w, c);
                 st_dsum += (unsigned long long)L;
@@ -535,7 +558,7 @@ __device__ __forceinline__ void lowdeg_row_nbrs(const SlicesParams &p, int4 row,
     }
 }
 
-template <bool ELL>
+template <bool ELL, bool CAP = false>
 __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(SlicesParams p) {
     __shared__ SlicesSmem sm;
     extern __shared__ unsigned f2[];  // 2 bits per vertex
@@ -562,13 +585,14 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
         __syncthreads();
         if (si >= p.nsrc) break;
         const int s = p.src[si];
+        const int cs = CAP ? p.cap_vslot[s] : -1;
         if (tid == 0) {
             f2[s >> 4] |= lowdeg_code(0) << ((s & 15) * 2);
             sc[s] = 1.0;
             Q[0] = s;
             loff[0] = 0;
             loff[1] = 1;
-            sm.tail = 1;
+            sm.cnt[0] = sm.cnt[1] = sm.cnt[2] = 0;
         }
         __syncthreads();
         // forward, one barrier per level: each thread takes a level-L vertex
@@ -577,9 +601,17 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
         // v's unvisited neighbours (level L+1) by shared-memory test-and-set,
         // appending them with one shared atomic per warp.  Concurrently set
         // codes are code(L+1) != code(L-1), so the parent test is unaffected.
-        int L = 0, qs = 0, qe = 1;
+        // Level L appends to Q[qe + cnt[L % 3]): a fast warp may start level
+        // L+1's appends (into cnt[(L+1) % 3]) while a slow one still reads
+        // cnt[L % 3] after the barrier, so the counters rotate; cnt[(L+1) % 3]
+        // was last read right after the barrier that ended level L-2, and the
+        // barrier ending level L-1 separates those reads from its reset here.
+        int L = 0, qs = 0, qe = 1, r3 = 0;
         while (qs < qe) {
             const unsigned cn = lowdeg_code(L + 1), cp = lowdeg_code(L + 2);  // (L + 2) mod 3 == (L - 1) mod 3
+            int *cnt = &sm.cnt[r3];
+            const int r3n = r3 == 2 ? 0 : r3 + 1;
+            if (tid == 0) sm.cnt[r3n] = 0;
             for (int i = qs + tid; i < qe; i += BC_SM_NT) {
                 const int v = Q[i];
                 const int4 row = (QROW && L >= 1) ? QR[i] : lowdeg_row<ELL>(p, v);
@@ -623,7 +655,7 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
                     if (tot) {
                         const int leader = __ffs(am) - 1;
                         int base = 0;
-                        if (lane == leader) base = atomicAdd(&sm.tail, tot);
+                        if (lane == leader) base = qe + atomicAdd(cnt, tot);
                         base = __shfl_sync(am, base, leader);
                         const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
@@ -650,7 +682,7 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
                         if (bal) {
                             const int leader = __ffs(bal) - 1;
                             int base = 0;
-                            if (lane == leader) base = atomicAdd(&sm.tail, __popc(bal));
+                            if (lane == leader) base = qe + atomicAdd(cnt, __popc(bal));
                             base = __shfl_sync(am, base, leader);
                             if (won) {
                                 const int pos = base + __popc(bal & ((1u << lane) - 1u));
@@ -664,7 +696,8 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
             }
             __syncthreads();
             qs = qe;
-            qe = sm.tail;
+            qe += *cnt;
+            r3 = r3n;
             ++L;
             if (tid == 0) loff[L + 1] = qe;
         }
@@ -711,6 +744,7 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
                 const double om = p.omega ? (double)p.omega[w] : 0.0;
                 const double delta = sg * acc;
                 sc[w] = (1.0 + om + delta) / sg;
+                slices_cap<CAP>(p, cs, w, L, sg, delta);
                 const double c = ws1 * (delta + om);
                 if (c != 0.0) atomicAdd(p.bc + w, c);
                 st_dsum += (unsigned long long)L;
