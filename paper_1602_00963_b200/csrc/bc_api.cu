@@ -10,6 +10,8 @@
 #include <vector>
 #include <algorithm>
 #include <thread>
+#include <chrono>
+#include <cstdlib>
 
 #include "bc.h"
 #include "util.cuh"
@@ -24,6 +26,19 @@ using namespace bcb;
 namespace {
 
 thread_local std::string g_err;
+
+// BC_TRACE=1 (environment): host-side phase times of bc_compute on stderr
+// (diagnosis of launch/sync-bound small graphs; no effect otherwise)
+bool trace_on() {
+    static const bool on = [] {
+        const char *e = std::getenv("BC_TRACE");
+        return e && *e && *e != '0';
+    }();
+    return on;
+}
+double now_us() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 
 bc_status fail(bc_status s, const char *fmt, ...) {
     char buf[1024];
@@ -177,6 +192,8 @@ struct LaneCtx {
     double *own_bc = nullptr;               // private partial BC (pipelines > 0)
     bc_stats last{};                        // host counters of the current call
     std::vector<cudaEvent_t> ef, eb, epush; // profile intervals
+    double sync_us = 0;                     // BC_TRACE: host time blocked in the per-level test
+    int syncs = 0;
     bool ready = false;
     void release() {
         ws.release();
@@ -940,7 +957,12 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
         CU(cudaEventRecord(x.ev_ring[L % FLAG_RING], st));
         if (L >= 2) {
             const int *hp = x.h_flag + 2 * ((L - 1) % FLAG_RING);
+            const double t0 = trace_on() ? now_us() : 0.0;
             CU(cudaEventSynchronize(x.ev_ring[(L - 1) % FLAG_RING]));
+            if (trace_on()) {
+                x.sync_us += now_us() - t0;
+                x.syncs += 1;
+            }
             if (NARROW && hp[1]) narrow_bad = true;  // sigma overflowed 16 bits: the batch is re-run in fp64
             if (narrow_bad || hp[0] == 0) {
                 Lmax = L - 1;
@@ -1646,6 +1668,8 @@ bc_status bc_get_pruning(const bc_graph *g, uint32_t *omega, uint8_t *removed, i
 
 bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, double *out_bc, void *cuda_stream) {
     if (!g) return fail(BC_ERR_INVALID, "NULL handle");
+    const double tr0 = trace_on() ? now_us() : 0.0;
+    double tr_plan = 0, tr_join = 0;
     // a capture (bc_set_capture) applies to this call only, success or not
     const bool capture = !g->capt.src.empty();
     struct CaptureReset {
@@ -1799,6 +1823,7 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     }
     CU(cudaMemsetAsync(g->d_bc, 0, (size_t)n * 8, st));
     CU(cudaMemsetAsync(g->d_stats, 0, 8 * sizeof(unsigned long long), st));
+    if (trace_on()) tr_plan = now_us();
     std::vector<cudaEvent_t> ef;
     if (mode == 2 && !trav.empty())
         CK(run_slices(g, run, g->d_src, (int)trav.size(), st, g->profile ? &ef : nullptr, capture));
@@ -1915,6 +1940,7 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
             for (auto &t : th) t.join();
         }
         if (start) cudaEventDestroy(start);
+        if (trace_on()) tr_join = now_us();
         for (int i = 0; i < NS; ++i)
             if (sts[i] != BC_OK) return fail(sts[i], "%s", msgs[i].c_str());
         for (int i = 0; i < NS; ++i) {
@@ -1954,6 +1980,21 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     if (capture) CK(capture_finish(g, st, mode == 2));
     if (g->profile) cudaEventRecord(t1, st);
     CU(cudaStreamSynchronize(st));
+    if (trace_on()) {
+        const double t = now_us();
+        double su = 0;
+        int sc = 0;
+        for (auto &x : g->ctx) {
+            su += x.sync_us;
+            sc += x.syncs;
+            x.sync_us = 0;
+            x.syncs = 0;
+        }
+        fprintf(stderr, "[bc_trace] n=%lld sources=%lld mode=%d batches=%lld: setup %.0f us, pipelines %.0f us "
+                        "(per-level waits %d, %.0f us summed over threads), finish %.0f us, total %.0f us\n",
+                (long long)n, (long long)trav.size(), mode, (long long)g->last.batches, tr_plan - tr0,
+                tr_join > 0 ? tr_join - tr_plan : 0.0, sc, su, t - (tr_join > 0 ? tr_join : tr_plan), t - tr0);
+    }
     g->last.reached = (int64_t)hst[0];
     g->last.adj_reached = (int64_t)hst[1];
     g->last.dag_edges = (int64_t)hst[2];

@@ -64,6 +64,9 @@ __device__ __forceinline__ double rcp_f64(double x) {
 #ifndef BC_PUSH_MINB8
 #define BC_PUSH_MINB8 3  // ... W = 8: 16 coef values per thread
 #endif
+#ifndef BC_PUSH_COMPACT
+#define BC_PUSH_COMPACT 0  // 1: backward push over the slot's compacted lanes (measured slower overall, profiles/exp_r2_push.txt)
+#endif
 
 template <int W>
 struct PushSmem {
@@ -73,6 +76,7 @@ struct PushSmem {
     uint64_t u[TV * W];
     alignas(16) uint64_t hc[BC_NW * 32 * W];  // per warp: contributing-lane words of the step's items
     int4 hsv[BC_NW * 32];         // per warp: (slot, y, group mask, -) of the step's items
+    uint16_t lst[BC_NW * 64 * W]; // per warp: the current slot's level-L lanes in lane order (compacted push)
     int scan[2 * BC_NW + 2];
     int unit;
 };
@@ -228,7 +232,182 @@ struct PushKernel {
         }
     }
 
+    // ---- compacted backward push (BC_PUSH_COMPACT).  At a slot change the
+    // warp lists the slot's level-L lanes u = lvl[L][x] in lane order (a warp
+    // scan over 2W-lane chunks) and thread t takes the u-ranks t, t+32, ...:
+    // nr = ceil(|u| / 32) rounds.  coef is formed for those lanes only, and
+    // a hit (x, y, c) costs nr rounds of one red each (a lane of u outside
+    // c skips its red) instead of 2W lane groups of mostly idle threads.  The
+    // lanes of one round are increasing, so a red instruction touches the
+    // same L2 sectors of A[y] as the group form.
+    // lp[r / 2] holds the lane of round r in its 16-bit half r % 2 (0xffff:
+    // no lane of u has rank lane + 32 r).
+    __device__ __forceinline__ int compact_slot(int hs, uint32_t (&lp)[NG / 2], int &tot) {
+        constexpr int CH = 2 * W;  // lanes per thread chunk (<= 16)
+        const int l0 = lane * CH;
+        const uint64_t uw = sm.u[hs * W + (l0 >> 6)];
+        uint32_t bits = (uint32_t)(uw >> (l0 & 63)) & ((1u << CH) - 1u);
+        const int cnt = __popc(bits);
+        const int incl = warp_incl_scan(cnt);
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        uint16_t *lst = sm.lst + wid * K;
+        int pos = incl - cnt;
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            lst[pos++] = (uint16_t)(l0 + b);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < NG / 2; ++q) {
+            const int k0 = lane + 64 * q, k1 = k0 + 32;
+            const uint32_t a = k0 < total ? lst[k0] : 0xffffu, b = k1 < total ? lst[k1] : 0xffffu;
+            lp[q] = a | (b << 16);
+        }
+        __syncwarp();  // the list is rewritten at the next slot change
+        tot = total;
+        return (total + 31) >> 5;
+    }
+    __device__ __forceinline__ static int lane_at(const uint32_t (&lp)[NG / 2], int r) {
+        return (int)((lp[r >> 1] >> ((r & 1) * 16)) & 0xffffu);
+    }
+
+    // coef of the compacted lanes of slot hs (x at level L), Eq.(5) as in
+    // slot_coef; an owned slot is also finalised (BC, A[x] := 0)
+    __device__ __forceinline__ void slot_coef_c(int hs, bool owned, int nr, const uint32_t (&lp)[NG / 2],
+                                                double (&cf)[NG]) {
+        const int x = sm.vert[hs];
+        const RT *row = reinterpret_cast<const RT *>(p.S_cur) + (size_t)x * K;
+        double *arow = A + (size_t)x * K;
+        const double om = p.omega ? (double)p.omega[x] : 0.0;
+        double contrib = 0.0;
+#pragma unroll
+        for (int h = 0; h < NG; h += NG / 2) {
+            double sv[NG / 2], av[NG / 2];
+#pragma unroll
+            for (int q = 0; q < NG / 2; ++q) {
+                const int l = lane_at(lp, h + q);
+                sv[q] = 1.0;
+                av[q] = 0.0;
+                if (h + q < nr && l < K) {
+                    sv[q] = (double)row[l];
+                    av[q] = arow[l];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < NG / 2; ++q) {
+                const int r = h + q, l = lane_at(lp, r);
+                cf[r] = 0.0;
+                if (r < nr && l < K) {
+                    const double delta = sv[q] * av[q];
+                    cf[r] = (1.0 + om + delta) * rcp_f64(sv[q]);
+                    if (owned) {
+                        arow[l] = 0.0;
+                        contrib += p.lane_w1[l] * (delta + om);
+                        cap_delta_put(p, l, x, delta);
+                    }
+                }
+            }
+        }
+        if (owned) {  // warp-uniform
+            contrib = warp_sum(contrib);
+            if (lane == 0 && contrib != 0.0) p.bc[x] += contrib;
+        }
+    }
+
+    __device__ void warp_push_compact(int nslots, int ws, int we, bool hub_mode) {
+        const uint64_t *mpar = p.mask_nxt_ro;  // lvl[L-1] (parents)
+        bool has_derived = false;
+#pragma unroll
+        for (int j = 0; j < W; ++j) has_derived |= p.derived[j] != 0;
+        const uint64_t pol = policy_evict_first();
+        int cur = -1, nr = 0, tot = 0;
+        uint32_t lp[NG / 2];
+        double cf[NG];
+#pragma unroll
+        for (int j = 0; j < NG; ++j) cf[j] = 0.0;
+#pragma unroll
+        for (int q = 0; q < NG / 2; ++q) lp[q] = 0xffffffffu;
+        st_items += (lane == 0) ? (unsigned long long)(we - ws) : 0ull;
+        for (int e0 = ws; e0 < we; e0 += 32 * R) {
+            int sl[R], vv[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                const int e = e0 + k * 32 + lane;
+                sl[k] = -1;
+                vv[k] = 0;
+                if (e < we) {
+                    const int s = slot_of(sm.cd, nslots, e);
+                    sl[k] = s;
+                    vv[k] = ld_stream(p.col + sm.rs[s] + (e - sm.cd[s]), pol);
+                }
+            }
+            uint64_t cc[R][W];
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+#pragma unroll
+                for (int j = 0; j < W; ++j) cc[k][j] = 0;
+                if (sl[k] >= 0) {
+                    load_mask<W>(mpar + (size_t)vv[k] * W, cc[k]);
+#pragma unroll
+                    for (int j = 0; j < W; ++j) cc[k][j] &= sm.u[sl[k] * W + j];
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                bool h = false;
+#pragma unroll
+                for (int j = 0; j < W; ++j) h |= cc[k][j] != 0;
+                unsigned hm = __ballot_sync(0xffffffffu, h);
+                st_hits += (lane == 0) ? __popc(hm) : 0;
+                if (hm == 0) continue;
+                int4 *hsv = sm.hsv + wid * 32;
+                hsv[lane] = make_int4(sl[k], vv[k], 0, 0);
+#pragma unroll
+                for (int j = 0; j < W; ++j) sm.hc[(wid * 32 + lane) * W + j] = cc[k][j];
+                __syncwarp();
+                while (hm) {
+                    const int src = __ffs(hm) - 1;
+                    hm &= hm - 1;
+                    const int2 rec = *reinterpret_cast<const int2 *>(hsv + src);
+                    const int hs = rec.x, y = rec.y;
+                    if (hs != cur) {  // warp-uniform: compact the new slot's lanes, form their coef
+                        cur = hs;
+                        nr = compact_slot(hs, lp, tot);
+                        slot_coef_c(hs, !hub_mode && sm.cd[hs] >= ws && sm.cd[hs + 1] <= we, nr, lp, cf);
+                    }
+                    const uint32_t *c32 = reinterpret_cast<const uint32_t *>(sm.hc + (wid * 32 + src) * W);
+                    if (has_derived && lane == 0) {  // only with BC_OPT_TWO_DEGREE: derived lanes' DAG edges
+#pragma unroll
+                        for (int j = 0; j < W; ++j) st_dag += __popcll(sm.hc[(wid * 32 + src) * W + j] & p.derived[j]);
+                    }
+                    double *arow = A + (size_t)y * K;
+#pragma unroll
+                    for (int r = 0; r < NG; ++r) {
+                        if (r < nr) {  // uniform
+                            const int l = lane_at(lp, r);
+                            const uint32_t on = l < K ? (c32[l >> 5] >> (l & 31)) & 1u : 0u;
+#ifdef BC_EXP_NORED  // experiment build only: traversal cost without the reds (wrong results)
+                            red_add_f64_if(arow + (l & (K - 1)), cf[r], on & (cf[r] == -1.0));
+#elif defined(BC_PUSH_DENSE)  // experiment: full rounds red 0.0 for the slot's lanes outside c (no branch)
+                            if ((r + 1) * 32 <= tot) red_add_f64(arow + l, on ? cf[r] : 0.0);
+                            else red_add_f64_if(arow + (l & (K - 1)), cf[r], on);
+#else
+                            red_add_f64_if(arow + (l & (K - 1)), cf[r], on);
+#endif
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+    }
+
     __device__ void warp_push(int nslots, int ws, int we, bool hub_mode) {
+        if constexpr (!FWD && BC_PUSH_COMPACT) {
+            warp_push_compact(nslots, ws, we, hub_mode);
+            return;
+        }
         const uint64_t *mpar = FWD ? p.seen : p.mask_nxt_ro;  // fwd: seen[y]; bwd: lvl[L-1] (parents)
         bool has_derived = false;
 #pragma unroll

@@ -128,8 +128,9 @@ def test_capture_sigma_tiers(layers, tiers):
     bcb = _bcb()
     g = gg.disjoint_union(layered(10, layers), gg.rmat(9, 8, seed=3))
     S = g.non_isolated()
-    caps = [0, 5, 10 * (layers // 2), 10 * layers + 7, 10 * layers + 100]
-    caps = [c for c in caps if c in set(S.tolist())]
+    # layered sources fill the first batches (given order, 64 lanes); the last
+    # R-MAT sources share a batch with no layered vertex
+    caps = [0, 5, 10 * (layers // 2), int(S[-1]), int(S[-7])]
     with bcb.Graph.from_csr(g) as G:
         G.set_option(bcb.OPT_MODE, 1)
         G.set_option(bcb.OPT_LANE_WORDS, 1)
@@ -181,7 +182,8 @@ def test_sssp_pruned_handle_fills_removed_vertices():
                 zero = m & (de == 0)
                 assert np.all(gde[zero] == 0)
                 nz = m & ~zero
-                assert np.max(np.abs(gde[nz] - de[nz]) / de[nz]) <= 1e-9
+                if nz.any():
+                    assert np.max(np.abs(gde[nz] - de[nz]) / de[nz]) <= 1e-9
             rem = np.nonzero(rm)[0]
             if len(rem):
                 with pytest.raises(bcb.BCError):

@@ -27,9 +27,11 @@ ap.add_argument("--sigma", type=int, default=0)
 ap.add_argument("--streams", type=int, default=0)
 ap.add_argument("--two-degree", type=int, default=0)
 ap.add_argument("--sort", default="none", choices=["none", "deg", "degasc"])
+ap.add_argument("--no-profile", action="store_true")
+ap.add_argument("--all", action="store_true", help="all non-isolated sources")
 a = ap.parse_args()
 g = gg.grid(a.grid, a.grid) if a.grid else gg.rmat(a.scale, a.ef, seed=1)
-S = gg.sample_sources(g, a.sources, seed=2)
+S = g.non_isolated() if a.all else gg.sample_sources(g, a.sources, seed=2)
 G = bcb.Graph.from_csr(g)
 if a.prune:
     G.prune_degree1()
@@ -48,7 +50,7 @@ if a.sort != "none":
     S = S[np.argsort(-d if a.sort == "deg" else d, kind="stable")]
 if a.hub:
     G.set_option(bcb.OPT_HUB_DEGREE, a.hub)
-G.set_option(bcb.OPT_PROFILE, 1)
+G.set_option(bcb.OPT_PROFILE, 0 if a.no_profile else 1)
 for r in range(a.repeat):
     t = time.perf_counter()
     bc = G.compute(S)
