@@ -199,18 +199,33 @@ def run_reference(args, cfg):
 
 
 def algorithmic_bytes(st, K):
-    """SURVEY §8(d-iii) model split per kernel.  A = sum of
-    reached adjacency, D = DAG lane-edges, N = reached lane-vertices, sb =
-    bytes per stored sigma value (2 for 16-bit rows, 8 for fp64 rows):
-      fwd  level kernel (pull)      A(4/K + 1/8) + sb D + sb N   col ids shared by K lanes,
-                                     1 mask bit per lane, sigma per DAG edge, sigma row write
-      bwd  push + finalize kernels  A(4/K + 1/8) + 8 D + (sb + 16) N   coef value per DAG edge
-                                     (red), sigma and accumulator read, accumulator re-zeroed"""
+    """Algorithmic bytes per kernel class for the roofline.
+    A = sum of reached adjacency, D = DAG lane-edges, N = reached
+    lane-vertices over the run; K lanes share each column read.
+
+    "survey": SURVEY.md §8(d-iii) exactly, B_alg = A(8/k + 2 b_d) + 16 D + 24 n
+      with b_d = 1/8 (one mask bit per lane), split per sweep as
+        fwd  A(4/K + 1/8) + 8 D + 16 N   (sigma per DAG edge; depth 4 + sigma 8 + BC 4 per vertex)
+        bwd  A(4/K + 1/8) + 8 D +  8 N   (coef per DAG edge; coef written once)
+    "rows": what this build's rows actually move, sb = bytes per stored
+      sigma value (2 for 16-bit rows, 4 for 32-bit, 8 for fp64):
+        fwd  A(4/K + 1/8) + sb D + sb N
+        bwd  A(4/K + 1/8) + 8 D + (sb + 16) N  (sigma and accumulator read, accumulator re-zeroed)"""
     A, D, N = st["adj_reached"], st["dag_edges"], st["reached"]
     nb, b = st["narrow_batches"], max(1, st["batches"])
-    sb = (2.0 * nb + 8.0 * (b - nb)) / b
+    mid = st.get("mid_batches", 0)
+    sb = (2.0 * nb + 4.0 * mid + 8.0 * max(0, b - nb - mid)) / b
     scan = A * (4.0 / K + 1.0 / 8.0)
-    return {"fwd": scan + sb * D + sb * N, "bwd": scan + 8.0 * D + (sb + 16.0) * N}
+    return {"survey": {"fwd": scan + 8.0 * D + 16.0 * N, "bwd": scan + 8.0 * D + 8.0 * N},
+            "rows": {"fwd": scan + sb * D + sb * N, "bwd": scan + 8.0 * D + (sb + 16.0) * N}}
+
+
+def slices_bytes(st):
+    """Slices mode (one source per CTA, both sweeps in one kernel): SURVEY.md
+    §8(d-iii) unbatched, k = 1 and an int32 depth (b_d = 4):
+    B_alg = A (8 + 8) + 16 D + 24 n over the run."""
+    A, D, N = st["adj_reached"], st["dag_edges"], st["reached"]
+    return A * 16.0 + 16.0 * D + 24.0 * N
 
 
 def main():
@@ -286,8 +301,10 @@ def main():
     e1 = torch.cuda.Event(enable_timing=True)
     agg = {"fwd_ms": 0.0, "bwd_ms": 0.0, "bwd_push_ms": 0.0, "bwd_fin_ms": 0.0, "fwd_launches": 0,
            "bwd_launches": 0, "kernel_launches": 0, "reached": 0, "adj_reached": 0, "dag_edges": 0,
-           "num_sources": 0, "levels_total": 0, "batches": 0, "narrow_batches": 0, "narrow_fallbacks": 0}
-    kbytes = {"fwd": 0.0, "bwd": 0.0}
+           "num_sources": 0, "levels_total": 0, "batches": 0, "narrow_batches": 0, "narrow_fallbacks": 0,
+           "mid_batches": 0}
+    kbytes = {"survey": {"fwd": 0.0, "bwd": 0.0}, "rows": {"fwd": 0.0, "bwd": 0.0}}
+    sbytes = 0.0
     lanes = 0
     e0.record(stream)
     for i in range(args.steps):
@@ -295,7 +312,7 @@ def main():
         st = G.stats()
         lanes = st["lanes"]
         for k in ("kernel_launches", "reached", "adj_reached", "dag_edges", "num_sources", "levels_total",
-                  "batches", "narrow_batches", "narrow_fallbacks"):
+                  "batches", "narrow_batches", "narrow_fallbacks", "mid_batches"):
             agg[k] += st[k]
     e1.record(stream)
     torch.cuda.synchronize()
@@ -349,43 +366,75 @@ def main():
         prof_ms += st["total_ms"]
         for k in ("fwd_ms", "bwd_ms", "bwd_push_ms", "bwd_fin_ms", "fwd_launches", "bwd_launches"):
             agg[k] += st[k]
-        for kk, vb in algorithmic_bytes(st, st["lanes"]).items():
-            kbytes[kk] += vb
+        for model, d in algorithmic_bytes(st, st["lanes"]).items():
+            for kk, vb in d.items():
+                kbytes[model][kk] += vb
+        sbytes += slices_bytes(st)
     G.set_option(bcb.OPT_PROFILE, 0)
     G.set_option(bcb.OPT_STREAMS, 0)
 
     if rank == 0:
         pk, pk_kind = peaks()
-        kms = {"fwd": agg["fwd_ms"], "bwd": agg["bwd_ms"]}
-        names = {"fwd": "lanes_level_kernel<fwd> (pull; + hub finalize)",
-                 "bwd": "lanes_push_kernel<bwd> (+ finalize kernels)"}
-        if agg["bwd_ms"] == 0.0 and agg["fwd_ms"] > 0.0:
-            # slices mode (one source per CTA): both sweeps run
-            # inside one persistent kernel, timed as "fwd"; its algorithmic
-            # bytes are the K = 1, fp64 model of both sweeps
-            kms = {"slices": agg["fwd_ms"]}
-            kbytes = {"slices": kbytes["fwd"] + kbytes["bwd"]}
-            names = {"slices": "slices_lowdeg_sm_kernel (2-bit shared-memory state; forward + "
-                               "backward sweeps of one source per CTA)"}
-        dom = max(kms, key=lambda k: kms[k])
-        dom_ms = kms[dom]
-        achieved = kbytes[dom] / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
-        traffic = None
+        peak = pk["hbm_gbs"]
         try:
-            tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-            traffic = tr.get(cfg, {}).get(dom, {}).get("dram_bytes_per_launch")
+            tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(cfg, {})
         except Exception:
-            pass
-        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "kernel": names[dom],
+            tr = {}
+        slices = agg["bwd_ms"] == 0.0 and agg["fwd_ms"] > 0.0
+        if not slices:
+            kms = {"fwd": agg["fwd_ms"], "bwd": agg["bwd_ms"]}
+            names = {"fwd": "lanes_level_kernel<fwd> (pull; + hub finalize)",
+                     "bwd": "lanes_push_kernel<bwd> (+ finalize kernels)"}
+            dom = max(kms, key=lambda k: kms[k])
+            dom_ms = kms[dom]
+            gbs = lambda b, t: b / (t / 1e3) / 1e9 if t > 0 else 0.0  # noqa: E731
+            achieved = gbs(kbytes["survey"][dom], dom_ms)
+            rows_ach = gbs(kbytes["rows"][dom], dom_ms)
+            timing = (f"CUDA events around every launch on its stream, {prof_steps} of the timed steps re-run with one "
+                      "batch pipeline (serialised kernels; the timed region overlaps up to 8 pipelines)")
+            model = ("SURVEY.md §8(d-iii): per batch A(4/K + 1/8) + 8 D + 8 N for the backward, "
+                     "A(4/K + 1/8) + 8 D + 16 N for the forward (A reached adjacency, D DAG lane-edges, N reached "
+                     "lane-vertices; bench stats)")
+            kern = {k: {"ms": kms[k], "alg_gb": kbytes["survey"][k] / 1e9, "gbs": gbs(kbytes["survey"][k], kms[k]),
+                        "rows_model_gb": kbytes["rows"][k] / 1e9, "rows_model_gbs": gbs(kbytes["rows"][k], kms[k])}
+                    for k in kms}
+            extra = {"rows_model": {"achieved": rows_ach, "frac": rows_ach / peak,
+                                    "formula": "bytes this build's rows move (16-bit sigma rows): backward "
+                                               "A(4/K + 1/8) + 8 D + (sb + 16) N, forward A(4/K + 1/8) + sb D + sb N"}}
+            limiter = "issue / L2 red sectors (backward), dependent-load latency (forward); DESIGN.md §5"
+        else:
+            dom, dom_ms = "slices", agg["fwd_ms"]
+            names = {"slices": "slices_lowdeg_sm_kernel (2-bit shared-memory state; forward + backward sweeps of "
+                               "one source per CTA)"}
+            achieved = sbytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
+            timing = (f"CUDA events around the one persistent slices launch of each step, {prof_steps} of the timed "
+                      "steps re-run (the same launch as in the timed region)")
+            model = "SURVEY.md §8(d-iii) unbatched, k = 1, int32 depth: A (8 + 8) + 16 D + 24 n per run"
+            kern = {"slices": {"ms": dom_ms, "alg_gb": sbytes / 1e9, "gbs": achieved}}
+            extra = {}
+            limiter = ("latency: each level's dependent L2 load chain (queue -> row -> sigma) and the barrier that "
+                       "ends it (DESIGN.md §4.2); DRAM traffic is below the algorithmic bytes")
+        td = tr.get(dom, {})
+        traffic = td.get("dram_bytes_per_launch")
+        if traffic is not None and td.get("time_s"):
+            extra["dram_frac_ncu"] = td["dram_bytes"] / td["time_s"] / 1e9 / peak
+        sect = {k: td[k] for k in ("ld_sectors_per_request", "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.pct",
+                                   "lts__t_sector_hit_rate.pct", "lts__t_sectors_srcunit_tex_op_red.sum",
+                                   "smsp__inst_executed_op_global_red.sum") if k in td}
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": names[dom], "model": model, "limiter": limiter,
                 "peak_kind": pk_kind, "kernel_share_of_step": dom_ms / prof_ms if prof_ms > 0 else None,
-                "timing": f"CUDA events around every launch on its stream, {prof_steps} of the timed steps re-run "
-                          "with one batch pipeline (serialised kernels; the timed region overlaps up to 8 pipelines)",
-                "kernels": {k: {"ms": kms[k], "alg_gb": kbytes[k] / 1e9,
-                                "gbs": kbytes[k] / (kms[k] / 1e3) / 1e9 if kms[k] else 0.0} for k in kms}}
+                "timing": timing, "kernels": kern, "sector_efficiency": sect or None,
+                "ncu_source": td and tr.get("source"), **extra}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(g, S)
+        if slices:
+            l2_note = ("no flush: per step 296 CTAs sweep 296 sources at a time, each writing 20 B per reached vertex "
+                       "(sigma/coef slot, queue, BC) -- 5.2 MB per source, far beyond L2 across a step")
+        else:
+            l2_note = ("inputs exceed L2 (per step: CSR 4*2m B streamed per level, sigma rows 2*K*n B per level, "
+                       "accumulators 8*K*n B); no flush")
         line = {
             "metric": METRIC, "value": value, "unit": "TEPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -394,7 +443,7 @@ def main():
                        "sources_per_gpu_per_step": per_gpu, "lanes_per_batch": lanes, "pruning": prune,
                        "teps_sources": "|S+| (pruned: each source counts 1 + omega(s))" if prune else "|S|",
                        "parallelism": f"source-sharded x{world} + NCCL BC all-reduce" if world > 1 else "1 GPU",
-                       "l2": "inputs exceed L2 (per step: CSR 4*2m B streamed per level, sigma rows 2*K*n B per level, accumulators 8*K*n B); no flush"},
+                       "l2": l2_note},
             "teps_paper_convention": 2 * value,
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
             "gpu_launches": agg["kernel_launches"],

@@ -1705,6 +1705,8 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
             else if (g->pruned && g->h_omega[s] > 0) triv.push_back(s);
         }
     }
+    double tr_m[4] = {0, 0, 0, 0};  // BC_TRACE marks: sources resolved, W / pipelines chosen, plan + clustering
+    if (trace_on()) tr_m[0] = now_us();
     const bool dev_out = is_device_ptr(out_bc);
     cudaStream_t st = cuda_stream ? (cudaStream_t)cuda_stream : g->own_stream;
     if (!g->run_valid) CK(build_run(g));
@@ -1762,6 +1764,7 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
         }
         (void)cudaGetLastError();
     }
+    if (trace_on()) tr_m[1] = now_us();
     const int64_t need = (int64_t)(trav.size() + triv.size());
     if (g->src_cap < need) {
         dfree(g->d_src);
@@ -1821,6 +1824,7 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
         }
         CU(cudaMemcpyAsync(g->d_src + nlanes, triv.data(), triv.size() * 4, cudaMemcpyHostToDevice, st));
     }
+    if (trace_on()) tr_m[2] = now_us();
     CU(cudaMemsetAsync(g->d_bc, 0, (size_t)n * 8, st));
     CU(cudaMemsetAsync(g->d_stats, 0, 8 * sizeof(unsigned long long), st));
     if (trace_on()) tr_plan = now_us();
@@ -1990,9 +1994,11 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
             x.sync_us = 0;
             x.syncs = 0;
         }
-        fprintf(stderr, "[bc_trace] n=%lld sources=%lld mode=%d batches=%lld: setup %.0f us, pipelines %.0f us "
+        fprintf(stderr, "[bc_trace] n=%lld sources=%lld mode=%d batches=%lld: setup %.0f us (resolve %.0f, sizing %.0f, "
+                        "plan %.0f, memset %.0f), pipelines %.0f us "
                         "(per-level waits %d, %.0f us summed over threads), finish %.0f us, total %.0f us\n",
-                (long long)n, (long long)trav.size(), mode, (long long)g->last.batches, tr_plan - tr0,
+                (long long)n, (long long)trav.size(), mode, (long long)g->last.batches, tr_plan - tr0, tr_m[0] - tr0,
+                tr_m[1] - tr_m[0], tr_m[2] - tr_m[1], tr_plan - tr_m[2],
                 tr_join > 0 ? tr_join - tr_plan : 0.0, sc, su, t - (tr_join > 0 ? tr_join : tr_plan), t - tr0);
     }
     g->last.reached = (int64_t)hst[0];

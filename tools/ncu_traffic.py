@@ -37,6 +37,22 @@ def cls(name):
     return (None, False)
 
 
+# sector efficiency (SURVEY §8(d-ii) graded number 2), summed over the class's launches
+SUMS = ["l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+        "lts__t_sectors_srcunit_tex_op_red.sum", "smsp__inst_executed_op_global_red.sum", "smsp__inst_executed.sum"]
+PCT = "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.pct"  # needs --metrics (not in --set full)
+HIT = "lts__t_sector_hit_rate.pct"
+
+
+def num(r, name):
+    if name not in h:
+        return None
+    try:
+        return float(r[h.index(name)].replace(",", ""))
+    except ValueError:
+        return None
+
+
 agg = {}
 for r in rows[2:]:
     c, main = cls(r[ki])
@@ -46,9 +62,24 @@ for r in rows[2:]:
     a["all_launches"] += 1
     a["launches"] += int(main)
     a["dram_bytes"] += float(r[ri]) * unit[u[ri]] + float(r[wi]) * unit[u[wi]]
-    a["time_s"] += float(r[ti]) * tunit[u[ti]]
+    t = float(r[ti]) * tunit[u[ti]]
+    a["time_s"] += t
+    for m in SUMS:
+        v = num(r, m)
+        if v is not None:
+            a[m] = a.get(m, 0.0) + v
+    for m in (PCT, HIT):  # time-weighted means
+        v = num(r, m)
+        if v is not None:
+            a[m + ":tw"] = a.get(m + ":tw", 0.0) + v * t
 for a in agg.values():
     a["dram_bytes_per_launch"] = a["dram_bytes"] / max(1, a["launches"])
+    for m in (PCT, HIT):
+        if m + ":tw" in a:
+            a[m] = a.pop(m + ":tw") / max(a["time_s"], 1e-30)
+    s_, q_ = a.get(SUMS[0]), a.get(SUMS[1])
+    if s_ and q_:
+        a["ld_sectors_per_request"] = s_ / q_
 path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
 try:
     data = json.load(open(path))
