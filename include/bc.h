@@ -189,9 +189,15 @@ typedef enum {
     BC_OPT_STREAMS = 10,    /* lanes mode: concurrent batch pipelines, 0 = auto (8 for n <= 2^18, else 3;
                                fewer if HBM is short), or 1..8.
                                Batches are independent (BC is additive over sources) */
-    BC_OPT_TWO_DEGREE = 11  /* lanes mode: 1 = 2-degree heuristic: a degree-2 source
+    BC_OPT_TWO_DEGREE = 11, /* lanes mode: 1 = 2-degree heuristic: a degree-2 source
                                whose two neighbours are also sources gets its shortest-path tree derived
                                from theirs (Lemma 1, Eq.(6)) instead of a traversal; default 0 */
+    BC_OPT_DEVICE_LOOP = 12 /* lanes mode: 1 (default) = device-driven batches when eligible -- each batch
+                               (every level, the sigma-tier fallbacks) is one CUDA graph launch with the
+                               termination test on the device; 0 = host-driven level loop
+                               (one host wait per level); 2 = device-driven with 4-byte rows forced (the
+                               fp64 tier then re-runs on the host-driven path; testing).  Eligible: default
+                               sweep options, no profiling, graph depth bound <= 32 levels (bc_graph_create) */
 } bc_option;
 
 bc_status bc_set_option(bc_graph *g, int option, int64_t value);

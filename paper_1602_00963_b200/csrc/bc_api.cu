@@ -19,6 +19,7 @@
 #include "graph_kernels.cuh"
 #include "slices.cuh"
 #include "bwd_push.cuh"
+#include "batch_ctl.cuh"
 #include <cub/device/device_radix_sort.cuh>
 
 using namespace bcb;
@@ -59,6 +60,8 @@ bc_status fail(bc_status s, const char *fmt, ...) {
                         #call, cudaGetErrorString(e_), __FILE__, __LINE__);                           \
         }                                                                                             \
     } while (0)
+
+#define CU_V(call) (void)(call)  // error surfaces through the enclosing cudaGetLastError / capture status
 
 #define CK(expr)                              \
     do {                                      \
@@ -169,8 +172,14 @@ struct LaneWS {
 
 constexpr int LCH = 8;           // levels per mask chunk
 constexpr int FLAG_RING = 4;     // pinned per-level flag slots (termination test one level behind)
-constexpr int TILE_ITEMS = 8192; // non-hub adjacency items per level-kernel tile (soft cap)
+constexpr int TILE_ITEMS = 8192; // non-hub adjacency items per level-kernel tile (soft cap) on large graphs
+#ifndef BC_TILE_MIN
+#define BC_TILE_MIN 256          // ... and the smallest cap (small graphs, see build_layout)
+#endif
 constexpr int MAX_STREAMS = 8;   // concurrent batch pipelines (BC_OPT_STREAMS)
+#ifndef BC_DEVLOOP_MAX_LEVELS
+#define BC_DEVLOOP_MAX_LEVELS 32  // device-driven batches only for graphs whose depth bound is at most this
+#endif
 
 // One batch pipeline: a workspace, a stream and the per-stream control state.
 // bc_compute runs up to MAX_STREAMS of them concurrently (one host thread
@@ -194,8 +203,33 @@ struct LaneCtx {
     std::vector<cudaEvent_t> ef, eb, epush; // profile intervals
     double sync_us = 0;                     // BC_TRACE: host time blocked in the per-level test
     int syncs = 0;
+    // device-driven batches (graph mode, enqueue_device_batch): per-batch
+    // inputs and control live in device memory, so one instantiated CUDA
+    // graph runs every batch of the pipeline
+    int *gb_src = nullptr;            // [512] sources of the current batch (-1 past its end)
+    int *gb_ctl = nullptr;            // [8]: 0 lanes, 1 batch counter, 2 16-bit overflow, 3 32-bit overflow,
+                                      //      4 depth-bound violation, 5 scratch
+    uint64_t *gb_active = nullptr;    // [8] lanes in use
+    int2 *gb_table = nullptr;         // (offset into d_src, lanes) per batch of the pipeline
+    int gb_table_cap = 0;
+    unsigned long long *gb_cnt = nullptr;       // [8]: levels, 16-bit / 32-bit / fp64 batches, host re-runs
+    int *gb_redo = nullptr;           // batch indices left for the host fp64 path (4-byte rows only)
+    unsigned long long *gb_stats_bak = nullptr;  // [8] counters at batch start (restored per tier)
+    cudaGraphExec_t gexec = nullptr;
+    std::vector<uintptr_t> gkey;
+    size_t gnodes = 0;                // nodes of the graph (kernels and copies) launched per batch
     bool ready = false;
     void release() {
+        if (gexec) cudaGraphExecDestroy(gexec), gexec = nullptr;
+        gkey.clear();
+        dfree(gb_src);
+        dfree(gb_ctl);
+        dfree(gb_active);
+        dfree(gb_table);
+        gb_table_cap = 0;
+        dfree(gb_cnt);
+        dfree(gb_redo);
+        dfree(gb_stats_bak);
         ws.release();
         dfree(d_stats);
         dfree(d_work_ctr);
@@ -270,6 +304,18 @@ struct bc_graph {
     };
     std::vector<TdBatch> td_plan;
     std::vector<int> td_lanes;
+    int depth_bound = -1;      // every BFS depth of the graph is <= this (bc_graph_create); -1 unknown
+    int device_loop = 1;       // BC_OPT_DEVICE_LOOP: device-driven batches (CUDA graph per pipeline) when eligible
+    struct Sizing {            // last call's lane width / row width / pipelines (skips cudaMemGetInfo when unchanged)
+        int64_t key[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+        int W = 0, NS = 0, rb = 0;
+        bool devloop = false;
+    } sizing;
+    unsigned long long *h_pin = nullptr;   // pinned: [0, 8) counters, [8 + 8 i, 16 + 8 i) pipeline i device-loop counters
+    cudaEvent_t stats_ev = nullptr;        // the call's counters are in h_pin once this completes
+    bool stats_pending = false;            // asynchronous call: g->last is completed by bc_get_stats
+    bool devloop_used[MAX_STREAMS] = {};
+    bool dl_violation = false;             // a device-driven BFS went past depth_bound (impossible by construction)
     int streams_opt = 0;       // 0 = auto: 8 pipelines for n <= 2^18 (launch/sync-bound batches), else 3       // BC_OPT_STREAMS (S20: 1 / 2 / 3 pipelines = 332 / 319 / 316 ms per 8192 sources)
     SlicesWS sws;    // slices-mode workspace
     unsigned long long *d_stats = nullptr;  // [16] slices mode / trivial sources counters
@@ -351,9 +397,15 @@ bc_status build_layout(bc_graph *g, DevCSR &c, cudaStream_t st) {
     int cnt = 0;
     int64_t items = 0;
     const int64_t n = g->n;
+    // Items per tile: at most TILE_ITEMS, and small enough that a level's
+    // adjacency makes ~8 tiles per SM -- on a small graph (S12: 97k items) a
+    // level's tiles are few, and a warp's serial walk over its share of a
+    // large tile is the level's critical path.
+    int64_t cap = TILE_ITEMS;
+    while (cap > BC_TILE_MIN && c.nnz / cap < 8LL * g->num_sms) cap >>= 1;
     for (int64_t v = 0; v < n; ++v) {
         const int d = c.h_deg[v] > g->hub_deg ? 0 : c.h_deg[v];
-        if (cnt == TV || (cnt > 0 && items + d > TILE_ITEMS)) {
+        if (cnt == TV || (cnt > 0 && items + d > cap)) {
             vs.push_back((int)v);
             cnt = 0;
             items = 0;
@@ -1141,6 +1193,233 @@ bc_status run_batch_w(bc_graph *g, LaneCtx &x, int W, const BatchCtx &c, std::ve
     }
 }
 
+
+// ---------------------------------------------------------------------
+// Device-driven batch (graph mode).  One batch of K lanes -- the forward
+// levels, the sigma-tier fallbacks and the backward levels -- enqueued with
+// no host round trip: Lcap forward and backward level slots are unrolled
+// (Lcap = the graph's depth bound, so every BFS fits), a slot is a no-op
+// when its level is empty, and each sigma tier (16-bit rows, then 32-bit,
+// then fp64 when the rows are 8 bytes wide) is a no-op unless the previous
+// tier overflowed (batch_ctl.cuh).  The sequence is captured once per
+// pipeline into a CUDA graph and launched once per batch; the batch's
+// sources come from the pipeline's device table, so the graph does not
+// change between batches or calls.
+struct DevBatchCfg {
+    const DevCSR *csr;
+    const uint32_t *omega;  // nullable
+    int lcap;               // forward levels 1..lcap are expanded; level lcap+1 must be empty
+    bool fp64_inline;       // 8-byte rows: the fp64 tier runs in the graph
+    bool capture;           // verification capture (bc_set_capture) rides along
+};
+
+template <int W, typename SigT>
+void enqueue_tier(bc_graph *g, LaneCtx &x, const DevBatchCfg &cfg, const int *need, int *ovf_self) {
+    constexpr int K = 64 * W;
+    using RT = typename RowOf<SigT>::t;
+    constexpr bool INTROW = !std::is_same<SigT, double>::value;
+    const int n = (int)g->n;
+    cudaStream_t st = x.st;
+    LaneWS &ws = x.ws;
+    const DevCSR &csr = *cfg.csr;
+    const int *halt = INTROW ? ovf_self : nullptr;
+    LanesParams p{};
+    p.n = n;
+    p.rp = csr.rp;
+    p.col = csr.col;
+    p.omega = cfg.omega;
+    p.seen = ws.seen;
+    p.ovf = nullptr;
+    p.bc = x.d_bc;
+    p.lane_w1 = ws.lane_w1;
+    p.lane_ns = cfg.omega ? ws.lane_ns : nullptr;
+    p.stats = x.d_stats;
+    p.work_ctr = x.d_work_ctr;
+    p.active_dev = x.gb_active;
+    p.need = need;
+    p.halt = halt;
+    p.hub_deg = g->hub_deg;
+    p.nhub = csr.nhub;
+    p.hub_ids = csr.hub_ids;
+    p.hub_seg_off = csr.hub_seg_off;
+    p.nseg = csr.nseg;
+    p.seg_len = g->hub_deg;
+    p.hub_acc = ws.hub_acc;
+    p.part = ws.part;
+    p.ntiles = csr.ntiles;
+    p.tile_vs = csr.tile_vs;
+    p.narrow_ovf = INTROW ? ovf_self : x.gb_ctl + 5;
+    p.lane_cap = cfg.capture ? ws.lane_cap : nullptr;
+    p.cap_delta = cfg.capture ? g->capt.d_delta : nullptr;
+    const size_t nmask = (size_t)n * W;
+    const unsigned zb = (unsigned)std::min<size_t>((nmask + 255) / 256, (size_t)g->num_sms * 8);
+    // tier start: state cleared, counters restored
+    gb_reset_kernel<<<std::max(zb, (unsigned)((cfg.lcap + 3 + 255) / 256)), 256, 0, st>>>(
+        ws.seen, level_ptr(g, ws, 0), level_ptr(g, ws, 1), nmask, (uint64_t *)ws.hub_acc, (size_t)csr.nhub * K,
+        x.d_flags, cfg.lcap + 3, x.d_stats, x.gb_stats_bak, need, nullptr);
+    if (cfg.capture) CU_V(cudaMemsetAsync(ws.capmask, 0, 8 * sizeof(uint64_t), st));
+    lane_setup_kernel<<<(K + 255) / 256, 256, 0, st>>>(x.gb_src, K, K, cfg.omega, ws.lane_w1,
+                                                       cfg.capture ? g->capt.d_vslot : nullptr, ws.lane_cap,
+                                                       (unsigned long long *)ws.capmask);
+    p.any_new = x.d_flags + 1;
+    lanes_init_kernel<W, SigT><<<K, BC_NT, 0, st>>>(p, x.gb_src, level_ptr(g, ws, 0), level_ptr(g, ws, 1));
+    const unsigned mb = (unsigned)(((int64_t)n + 255) / 256);
+    lanes_materialize_kernel<W, RT><<<mb, 256, 0, st>>>(n, level_ptr(g, ws, 0), (RT *)ws.slev[0], need, halt);
+    lanes_materialize_kernel<W, RT><<<mb, 256, 0, st>>>(n, level_ptr(g, ws, 1), (RT *)ws.slev[1], need, halt);
+    // forward slots
+    auto kf = lanes_level_kernel<W, SigT>;
+    constexpr size_t SMEM = sizeof(LanesSmem<W, SigT>);
+    const int units = p.nseg + p.ntiles;
+    const int grid = level_grid(g, kf, units, SMEM);
+    cudaFuncSetAttribute(lanes_hub_finalize<W, SigT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    const int hub_grid = (csr.nhub * 32 + BC_NT - 1) / BC_NT;
+    for (int L = 1; L <= cfg.lcap; ++L) {
+        gb_zero_level_kernel<<<zb, 256, 0, st>>>(level_ptr(g, ws, L + 1), nmask, x.d_flags + L + 1, need);
+        p.level = L;
+        p.S_cur = ws.slev[L];
+        p.S_nxt = ws.slev[L + 1];
+        p.mask_cur = level_ptr(g, ws, L);
+        p.mask_nxt = level_ptr(g, ws, L + 1);
+        p.mask_nxt_ro = nullptr;
+        p.any_new = x.d_flags + L + 1;
+        p.prev_new = x.d_flags + L;
+        kf<<<grid, BC_NT, SMEM, st>>>(p);
+        if (p.nhub > 0) lanes_hub_finalize<W, SigT><<<hub_grid, BC_NT, SMEM, st>>>(p);
+    }
+    if (cfg.capture) {
+        const unsigned vb = (unsigned)(((int64_t)n + 255) / 256);
+        for (int l = 0; l <= cfg.lcap; ++l)
+            cap_extract_kernel<W, RT><<<vb, 256, 0, st>>>(n, l, level_ptr(g, ws, l), (const RT *)ws.slev[l],
+                                                          ws.lane_cap, ws.capmask, g->capt.d_depth, g->capt.d_sigma,
+                                                          need, halt, l == 0 ? nullptr : x.d_flags + l);
+        cap_tier_kernel<<<(K + 255) / 256, 256, 0, st>>>(K, ws.lane_cap, 8 * (int)sizeof(RT), g->capt.d_tier, need,
+                                                         halt);
+    }
+    // backward slots (push form, fused finalize; level 1 by the finalize scan)
+    auto kpush = lanes_push_kernel<W, false, RT>;
+    cudaFuncSetAttribute(kpush, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int occp = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occp, kpush, BC_NT, 0);
+    const int gridp = std::max(1, std::min(g->num_sms * std::max(1, occp), units));
+    const unsigned fin_blocks = (unsigned)std::min<int64_t>(((int64_t)n * 32 + BC_NT - 1) / BC_NT, (int64_t)g->num_sms * 8);
+    for (int l = cfg.lcap; l >= 1; --l) {
+        p.level = l;
+        p.S_cur = ws.slev[l];
+        p.S_nxt = nullptr;
+        p.mask_cur = level_ptr(g, ws, l);
+        p.mask_nxt_ro = level_ptr(g, ws, l - 1);
+        p.mask_nxt = nullptr;
+        p.any_new = x.gb_ctl + 5;  // unused
+        p.prev_new = x.d_flags + l;  // level l non-empty
+        if (l >= 2) kpush<<<gridp, BC_NT, 0, st>>>(p, ws.A);
+        if (l == 1)
+            lanes_bwd_finalize_kernel<W, false, RT><<<fin_blocks, BC_NT, 0, st>>>(p, ws.A);
+        else if (p.nhub > 0)
+            lanes_bwd_hub_fin_kernel<W, RT><<<(p.nhub * 32 + BC_NT - 1) / BC_NT, BC_NT, 0, st>>>(p, ws.A);
+    }
+    if (cfg.omega)
+        lanes_endpoint_kernel<<<(K + 255) / 256, 256, 0, st>>>(x.gb_src, K, cfg.omega, ws.lane_ns, x.d_bc, need, halt);
+}
+
+template <int W>
+bc_status enqueue_device_batch(bc_graph *g, LaneCtx &x, const DevBatchCfg &cfg) {
+    constexpr int K = 64 * W;
+    cudaStream_t st = x.st;
+    gb_begin_kernel<<<1, 512, 0, st>>>(x.gb_table, x.gb_ctl, g->d_src, K, x.gb_src, x.gb_active, x.d_stats,
+                                       x.gb_stats_bak);
+    enqueue_tier<W, unsigned>(g, x, cfg, nullptr, x.gb_ctl + 2);
+    enqueue_tier<W, long long>(g, x, cfg, x.gb_ctl + 2, x.gb_ctl + 3);
+    if (cfg.fp64_inline) enqueue_tier<W, double>(g, x, cfg, x.gb_ctl + 3, nullptr);
+    gb_end_kernel<<<1, 32, 0, st>>>(x.gb_ctl, x.d_flags, cfg.lcap, x.gb_cnt, x.gb_redo, cfg.fp64_inline ? 1 : 0,
+                                    x.d_stats, x.gb_stats_bak);
+    CU(cudaGetLastError());
+    return BC_OK;
+}
+
+bc_status enqueue_device_batch_w(bc_graph *g, LaneCtx &x, int W, const DevBatchCfg &cfg) {
+    switch (W) {
+        case 1: return enqueue_device_batch<1>(g, x, cfg);
+        case 2: return enqueue_device_batch<2>(g, x, cfg);
+        case 4: return enqueue_device_batch<4>(g, x, cfg);
+        case 8: return enqueue_device_batch<8>(g, x, cfg);
+        default: return fail(BC_ERR_INTERNAL, "bad lane words %d", W);
+    }
+}
+
+// The pipeline's graph: rebuilt only when something it bakes in changed
+// (the buffers, the CSR, the lane width, the depth bound, the tier set).
+bc_status device_batch_graph(bc_graph *g, LaneCtx &x, int W, const DevBatchCfg &cfg) {
+    std::vector<uintptr_t> key = {(uintptr_t)W,
+                                  (uintptr_t)cfg.lcap,
+                                  (uintptr_t)cfg.fp64_inline,
+                                  (uintptr_t)cfg.capture,
+                                  (uintptr_t)cfg.omega,
+                                  (uintptr_t)cfg.csr->rp,
+                                  (uintptr_t)cfg.csr->col,
+                                  (uintptr_t)cfg.csr->tile_vs,
+                                  (uintptr_t)cfg.csr->hub_ids,
+                                  (uintptr_t)g->hub_deg,
+                                  (uintptr_t)x.ws.seen,
+                                  (uintptr_t)x.ws.A,
+                                  (uintptr_t)x.ws.hub_acc,
+                                  (uintptr_t)x.ws.part,
+                                  (uintptr_t)x.d_flags,
+                                  (uintptr_t)x.d_bc,
+                                  (uintptr_t)x.gb_table,
+                                  (uintptr_t)g->d_src,
+                                  (uintptr_t)g->capt.d_vslot,
+                                  (uintptr_t)g->capt.d_depth};
+    for (int l = 0; l <= cfg.lcap + 1; ++l) {
+        key.push_back((uintptr_t)x.ws.slev[l]);
+        key.push_back((uintptr_t)level_ptr(g, x.ws, l));
+    }
+    if (x.gexec && key == x.gkey) return BC_OK;
+    if (x.gexec) cudaGraphExecDestroy(x.gexec), x.gexec = nullptr;
+    x.gkey.clear();
+    CU(cudaStreamBeginCapture(x.st, cudaStreamCaptureModeThreadLocal));
+    bc_status s = enqueue_device_batch_w(g, x, W, cfg);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(x.st, &graph);
+    if (s != BC_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return s;
+    }
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        return fail(BC_ERR_CUDA, "graph capture of the device-driven batch failed: %s", cudaGetErrorString(e));
+    }
+    cudaGraphGetNodes(graph, nullptr, &x.gnodes);
+    const cudaError_t ei = cudaGraphInstantiate(&x.gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) {
+        (void)cudaGetLastError();
+        x.gexec = nullptr;
+        return fail(BC_ERR_CUDA, "graph instantiation failed: %s", cudaGetErrorString(ei));
+    }
+    x.gkey = key;
+    return BC_OK;
+}
+
+bc_status ensure_device_batch(bc_graph *g, LaneCtx &x, int nbatches) {
+    if (!x.gb_src) {
+        CK(dalloc(&x.gb_src, 512));
+        CK(dalloc(&x.gb_ctl, 8));
+        CK(dalloc(&x.gb_active, 8));
+        CK(dalloc(&x.gb_cnt, 8));
+        CK(dalloc(&x.gb_stats_bak, 8));
+        CU(cudaMemset(x.gb_ctl, 0, 8 * sizeof(int)));
+    }
+    if (x.gb_table_cap < nbatches) {
+        dfree(x.gb_table);
+        dfree(x.gb_redo);
+        const int cap = std::max(nbatches, 2 * x.gb_table_cap);
+        CK(dalloc(&x.gb_table, cap));
+        CK(dalloc(&x.gb_redo, cap));
+        x.gb_table_cap = cap;
+    }
+    return BC_OK;
+}
+
 bc_status ensure_slices(bc_graph *g, int rows, bool full) {
     if (g->sws.rows >= rows && (g->sws.full || !full)) return BC_OK;
     g->sws.release();
@@ -1258,6 +1537,32 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
     g->last.batches += 1;
     g->last.lanes = 1;
     return BC_OK;
+}
+
+// The call's counters from pinned memory (copied at the end of bc_compute):
+// the kernels' A_s / D_s / n_s / item counters and, for device-driven
+// pipelines, the level and sigma-tier counters of batch_ctl.cuh.
+void finalize_stats(bc_graph *g) {
+    const unsigned long long *h = g->h_pin;
+    g->last.reached = (int64_t)h[0];
+    g->last.adj_reached = (int64_t)h[1];
+    g->last.dag_edges = (int64_t)h[2];
+    g->last.dist_sum = (int64_t)h[3];
+    g->last.fwd_items = (int64_t)h[4];
+    g->last.fwd_hits = (int64_t)h[5];
+    g->last.bwd_items = (int64_t)h[6];
+    g->last.bwd_hits = (int64_t)h[7];
+    for (int i = 0; i < MAX_STREAMS; ++i) {
+        if (!g->devloop_used[i]) continue;
+        const unsigned long long *c = h + 8 + 8 * i;
+        g->last.levels_total += (int64_t)c[0];
+        g->last.fwd_launches += (int64_t)c[0];
+        g->last.bwd_launches += (int64_t)c[0];
+        g->last.narrow_batches += (int64_t)c[1];
+        g->last.mid_batches += (int64_t)c[2];
+        g->last.narrow_fallbacks += (int64_t)(c[2] + c[3]);
+        if (c[5]) g->dl_violation = true;
+    }
 }
 
 // ---- verification capture (bc_set_capture)
@@ -1421,10 +1726,52 @@ bc_status bc_destroy(bc_graph *g) {
         dfree(g->cl_vout);
         if (g->cl_tmp) cudaFree(g->cl_tmp);
         dfree(g->d_tmp);
+        if (g->h_pin) cudaFreeHost(g->h_pin);
+        if (g->stats_ev) cudaEventDestroy(g->stats_ev);
         if (g->own_stream) cudaStreamDestroy(g->own_stream);
     }
     delete g;
     return BC_OK;
+}
+
+// An upper bound on every BFS depth of the graph, for the device-driven
+// batches' level slots: in a component with root r, d(s, t) <= d(s, r) +
+// d(r, t) <= 2 ecc(r).  Roots are taken in descending degree order (a hub
+// is central in a power-law graph, keeping the bound tight).  Host BFS over
+// the caller's CSR, O(n + m), once per graph; a pruned graph's residual
+// distances between kept vertices are the original ones, so the bound holds
+// for it too.
+static int depth_bound(int64_t n, const int64_t *rp, const int32_t *col, const std::vector<int> &deg) {
+    int maxdeg = 0;
+    for (int d : deg) maxdeg = std::max(maxdeg, d);
+    std::vector<int64_t> start((size_t)maxdeg + 2, 0);  // counting sort, degree descending
+    for (int d : deg) start[(size_t)(maxdeg - d) + 1]++;
+    for (size_t i = 1; i < start.size(); ++i) start[i] += start[i - 1];
+    std::vector<int> order((size_t)n);
+    for (int64_t v = 0; v < n; ++v) order[(size_t)start[(size_t)(maxdeg - deg[v])]++] = (int)v;
+    std::vector<int> dist((size_t)n, -1), q((size_t)n);
+    int bound = 0;
+    for (int r : order) {
+        if (dist[r] >= 0) continue;
+        size_t h = 0, t = 0;
+        q[t++] = r;
+        dist[r] = 0;
+        int ecc = 0;
+        while (h < t) {
+            const int v = q[h++];
+            ecc = dist[v];
+            for (int64_t e = rp[v]; e < rp[v + 1]; ++e) {
+                const int w = col[e];
+                if (w < 0 || w >= n) return -1;  // malformed CSR (unvalidated): no bound, host-driven loop
+                if (dist[w] < 0) {
+                    dist[w] = dist[v] + 1;
+                    q[t++] = w;
+                }
+            }
+        }
+        bound = std::max(bound, 2 * ecc);
+    }
+    return bound;
 }
 
 static bc_status create_impl(bc_graph *g, int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
@@ -1462,6 +1809,9 @@ static bc_status create_impl(bc_graph *g, int64_t n, const int64_t *row_ptr, con
     }
     g->orig.h_deg.resize(n);
     for (int64_t v = 0; v < n; ++v) g->orig.h_deg[v] = (int)(row_ptr[v + 1] - row_ptr[v]);
+    g->depth_bound = depth_bound(n, row_ptr, col_idx, g->orig.h_deg);
+    CU(cudaMallocHost((void **)&g->h_pin, (8 + 8 * MAX_STREAMS) * sizeof(unsigned long long)));
+    CU(cudaEventCreateWithFlags(&g->stats_ev, cudaEventDisableTiming));
     CK(build_layout(g, g->orig, st));
     CK(build_run(g));
     return BC_OK;
@@ -1605,6 +1955,10 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
             if (value < 0 || value > 2) return fail(BC_ERR_INVALID, "mode must be 0, 1 or 2");
             g->mode = (int)value;
             return BC_OK;
+        case BC_OPT_DEVICE_LOOP:
+            if (value < 0 || value > 2) return fail(BC_ERR_INVALID, "device loop must be 0, 1 or 2");
+            g->device_loop = (int)value;
+            return BC_OK;
     }
     return fail(BC_ERR_INVALID, "unknown option %d", option);
 }
@@ -1632,9 +1986,17 @@ bc_status bc_set_capture(bc_graph *g, const int32_t *sources, int64_t n_cap, int
     return BC_OK;
 }
 
-bc_status bc_get_stats(const bc_graph *g, bc_stats *out) {
-    if (!g || !out) return fail(BC_ERR_INVALID, "NULL argument");
+bc_status bc_get_stats(const bc_graph *cg, bc_stats *out) {
+    if (!cg || !out) return fail(BC_ERR_INVALID, "NULL argument");
+    bc_graph *g = const_cast<bc_graph *>(cg);
+    if (g->stats_pending) {  // asynchronous bc_compute: its counters land when its stream gets there
+        DeviceGuard dg(g->device);
+        CU(cudaEventSynchronize(g->stats_ev));
+        finalize_stats(g);
+        g->stats_pending = false;
+    }
     *out = g->last;
+    if (g->dl_violation) return fail(BC_ERR_INTERNAL, "a BFS exceeded the graph's depth bound (%d levels)", g->depth_bound);
     return BC_OK;
 }
 
@@ -1718,52 +2080,90 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     for (auto &v : triv) v = run.h_inv[v];
     if (g->src_order >= 1) std::stable_sort(trav.begin(), trav.end());
     g->last = bc_stats{};
+    g->stats_pending = false;
+    g->dl_violation = false;
     g->last.num_sources = (int64_t)trav.size();
     g->last.num_trivial = (int64_t)triv.size();
     // batch mode: bit lanes (low diameter) or one source per CTA (long
     // diameter); auto picks slices for large sparse graphs (mean degree < 6)
     int mode = g->mode;
     if (mode == 0) mode = auto_slices(g->n, run.nnz) ? 2 : 1;
-    // level-row width: 4 bytes per lane (the 16- and 32-bit sigma tiers) unless
-    // fp64 rows are requested; a batch that needs fp64 widens them (widen_rows)
-    const int rb = g->sigma_width == 64 || g->bwd_mode == 2 || g->fwd_push_levels > 0 ? 8 : 4;
-    int W = g->lane_words_opt;
-    if (W == 0) {
-        W = trav.size() > 128 ? 4 : (trav.size() > 64 ? 2 : 1);
-        // K = 512 halves the items per source again but doubles the lanes a
-        // thread carries: faster only where per-batch overhead dominates
-        // (S16: 74 -> 60 ms per 16384 sources; S20: 319 -> 362 ms)
-        if (trav.size() > 256 && g->n <= (1 << 18)) W = 8;
-        // level rows cost n*64*W*row_bytes per BFS level, the accumulators
-        // n*512*W: keep ~9 levels plus the accumulators within 60 % of the
-        // free HBM (S23 at 4-byte rows -> W = 4; R-MAT depth <= ~9)
-        size_t free_b = 0, total_b = 0;
-        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-            for (auto &x : g->ctx)
-                free_b += (size_t)x.ws.slev.size() * (size_t)g->n * 64 * (size_t)x.ws.W * (size_t)x.ws.row_bytes +
-                          (x.ws.A ? (size_t)g->n * 512 * (size_t)x.ws.W : 0);  // reusable
-            while (W > 1 && (double)g->n * 64.0 * W * (9.0 * rb + 8.0) > 0.6 * (double)free_b) W >>= 1;
+    // ---- lane width W (K = 64 W lanes per batch), level-row width rb, batch
+    // pipelines NS and the device-driven batch (graph mode).
+    // Rows cost n*64*W*rb bytes per BFS level, the accumulators n*512*W, the
+    // level masks n*8*W per level; each pipeline holds its own.  Host-driven
+    // batches allocate levels on demand (~11 at R-MAT depths) with 4-byte rows
+    // (the 16- and 32-bit sigma tiers; a batch needing fp64 widens them).
+    // Device-driven batches preallocate levels 0 .. depth_bound + 1 and use
+    // 8-byte rows when they fit (the fp64 tier then runs in the graph too).
+    // Measured (prof_batch): S12 1/4/8 pipelines 21.5/6.2/4.0 ms, S16
+    // 352/114/110 ms, S20 332/316 (3)/332 (4) ms (host-driven).
+    const int lcap = g->depth_bound;
+    const bool dl_opts = g->device_loop && mode == 1 && !g->two_degree && g->bwd_mode != 2 &&
+                         g->fwd_push_levels == 0 && !g->profile && g->sigma_width != 64 && g->hub_deg <= 65536 &&
+                         lcap >= 1 && lcap <= BC_DEVLOOP_MAX_LEVELS;
+    const int64_t skey[8] = {(int64_t)trav.size(), mode, dl_opts, g->lane_words_opt, g->streams_opt,
+                             g->sigma_width + 1000 * g->bwd_mode + 100000 * g->fwd_push_levels, lcap, g->n};
+    int W, NS, rb;
+    bool devloop;
+    if (std::equal(skey, skey + 8, g->sizing.key)) {
+        W = g->sizing.W;
+        NS = g->sizing.NS;
+        rb = g->sizing.rb;
+        devloop = g->sizing.devloop;
+    } else {
+        rb = g->sigma_width == 64 || g->bwd_mode == 2 || g->fwd_push_levels > 0 ? 8 : 4;
+        W = g->lane_words_opt;
+        if (W == 0) {
+            W = trav.size() > 128 ? 4 : (trav.size() > 64 ? 2 : 1);
+            // K = 512 halves the items per source again but doubles the lanes a
+            // thread carries: faster only where per-batch overhead dominates
+            // (S16: 74 -> 60 ms per 16384 sources; S20: 319 -> 362 ms)
+            if (trav.size() > 256 && g->n <= (1 << 18)) W = 8;
         }
-        (void)cudaGetLastError();
+        const int ns_auto = g->n <= (1 << 18) ? 8 : 3;
+        NS = mode == 1 ? (g->streams_opt > 0 ? g->streams_opt : ns_auto) : 1;
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+            (void)cudaGetLastError();
+            free_b = 0;
+        }
+        for (auto &x : g->ctx)  // reusable
+            free_b += (size_t)x.ws.slev.size() * (size_t)g->n * 64 * (size_t)x.ws.W * (size_t)x.ws.row_bytes +
+                      (x.ws.A ? (size_t)g->n * 512 * (size_t)x.ws.W : 0);
+        const double budget = 0.6 * (double)free_b;
+        auto bytes = [&](int w, int r, int levels) {
+            return (double)g->n * 64.0 * w * (levels * (double)r + 8.0) + (double)g->n * 8.0 * w * ((levels + 7) / 8 * 8);
+        };
+        devloop = false;
+        if (dl_opts) {
+            // device-driven: keep the lane width; 8-byte rows if NS pipelines fit, else 4-byte rows
+            const int lv = lcap + 2;
+            for (int r : {8, 4}) {
+                if (r == 8 && g->device_loop == 2) continue;  // 4-byte rows forced (tests the host fp64 re-run)
+                int ns = NS;
+                while (ns > 1 && ns * bytes(W, r, lv) > budget) --ns;
+                if (bytes(W, r, lv) <= budget) {
+                    devloop = true;
+                    rb = r;
+                    NS = ns;
+                    break;
+                }
+            }
+        }
+        if (!devloop) {
+            if (g->lane_words_opt == 0)  // keep ~9 levels plus the accumulators within budget (S23: W = 4)
+                while (W > 1 && bytes(W, rb, 9) > budget) W >>= 1;
+            while (NS > 1 && NS * bytes(W, rb, 11) > budget) --NS;
+        }
+        std::copy(skey, skey + 8, g->sizing.key);
+        g->sizing.W = W;
+        g->sizing.NS = NS;
+        g->sizing.rb = rb;
+        g->sizing.devloop = devloop;
     }
     const int K = 64 * W;
     g->last.lanes = K;
-    // concurrent batch pipelines: bounded by the option, the batch count and
-    // memory (each holds ~10 levels of rows plus the accumulators)
-    // measured (tools/small_probe.py, prof_batch): S12 1/4/8 pipelines 21.5/6.2/4.0 ms,
-    // S16 352/114/110 ms, S20 332/316 (3)/332 (4) ms
-    const int ns_auto = g->n <= (1 << 18) ? 8 : 3;
-    int NS = mode == 1 ? (g->streams_opt > 0 ? g->streams_opt : ns_auto) : 1;
-    if (NS > 1) {
-        size_t free_b = 0, total_b = 0;
-        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-            for (auto &x : g->ctx)
-                free_b += (size_t)x.ws.slev.size() * (size_t)g->n * 64 * (size_t)x.ws.W * (size_t)x.ws.row_bytes +
-                          (x.ws.A ? (size_t)g->n * 512 * (size_t)x.ws.W : 0);
-            while (NS > 1 && (double)NS * g->n * 64.0 * W * (11.0 * rb + 8.0) > 0.6 * (double)free_b) --NS;
-        }
-        (void)cudaGetLastError();
-    }
     if (trace_on()) tr_m[1] = now_us();
     const int64_t need = (int64_t)(trav.size() + triv.size());
     if (g->src_cap < need) {
@@ -1831,7 +2231,105 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     std::vector<cudaEvent_t> ef;
     if (mode == 2 && !trav.empty())
         CK(run_slices(g, run, g->d_src, (int)trav.size(), st, g->profile ? &ef : nullptr, capture));
-    if (mode == 1 && !trav.empty()) {
+    for (auto &u : g->devloop_used) u = false;
+    if (mode == 1 && !trav.empty() && devloop && !plan.empty() && !plan[0].layout) {
+        // ---- device-driven batches: one CUDA graph launch per batch, no host
+        // round trip inside a batch (enqueue_device_batch)
+        NS = std::max(1, std::min(NS, (int)plan.size()));
+        cudaEvent_t start = nullptr;
+        CU(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+        CU(cudaEventRecord(start, st));
+        DevBatchCfg cfg{};
+        cfg.csr = &run;
+        cfg.omega = g->pruned ? run.omega : nullptr;
+        cfg.lcap = lcap;
+        cfg.fp64_inline = rb >= 8;
+        cfg.capture = capture;
+        bc_status r = BC_OK;
+        for (int i = 0; i < NS && r == BC_OK; ++i) {
+            LaneCtx &x = g->ctx[i];
+            auto body = [&]() -> bc_status {
+                CK(ctx_init(g, x));
+                CK(ensure_ws(g, x.ws, W, false, std::max(run.nhub, g->orig.nhub), rb));
+                CK(ensure_level(g, x.ws, lcap + 1));
+                CK(ensure_flags(g, x, lcap + 3));
+                std::vector<int2> tab;
+                for (size_t bi = (size_t)i; bi < plan.size(); bi += (size_t)NS)
+                    tab.push_back(make_int2((int)plan[bi].off, plan[bi].nl));
+                CK(ensure_device_batch(g, x, (int)tab.size()));
+                x.last = bc_stats{};
+                x.st = x.own;
+                cudaStream_t xs = x.st;
+                CU(cudaStreamWaitEvent(xs, start, 0));
+                CU(cudaMemcpyAsync(x.gb_table, tab.data(), tab.size() * sizeof(int2), cudaMemcpyHostToDevice, xs));
+                CU(cudaMemsetAsync(x.gb_ctl, 0, 8 * sizeof(int), xs));
+                CU(cudaMemsetAsync(x.gb_cnt, 0, 8 * sizeof(unsigned long long), xs));
+                CU(cudaMemsetAsync(x.d_stats, 0, 8 * sizeof(unsigned long long), xs));
+                if (i == 0) {
+                    x.d_bc = g->d_bc;
+                } else {
+                    if (!x.own_bc) CK(dalloc(&x.own_bc, (size_t)n));
+                    x.d_bc = x.own_bc;
+                    CU(cudaMemsetAsync(x.d_bc, 0, (size_t)n * 8, xs));
+                }
+                CK(device_batch_graph(g, x, W, cfg));
+                for (size_t b = 0; b < tab.size(); ++b) CU(cudaGraphLaunch(x.gexec, xs));
+                x.last.batches = (int64_t)tab.size();
+                g->devloop_used[i] = true;
+                return BC_OK;
+            };
+            r = body();
+        }
+        cudaEventDestroy(start);
+        if (r != BC_OK) return r;
+        if (!cfg.fp64_inline) {
+            // 4-byte rows: batches whose 32-bit sigma overflowed (sigma >= 2^32,
+            // never on R-MAT) re-run on the host-driven fp64 path
+            for (int i = 0; i < NS; ++i) CU(cudaMemcpyAsync(g->h_pin + 8 + 8 * i, g->ctx[i].gb_cnt, 64, cudaMemcpyDeviceToHost, g->ctx[i].st));
+            for (int i = 0; i < NS; ++i) CU(cudaStreamSynchronize(g->ctx[i].st));
+            for (int i = 0; i < NS; ++i) {
+                LaneCtx &x = g->ctx[i];
+                const int nredo = (int)g->h_pin[8 + 8 * i + 4];
+                if (!nredo) continue;
+                std::vector<int> redo(nredo);
+                CU(cudaMemcpy(redo.data(), x.gb_redo, (size_t)nredo * 4, cudaMemcpyDeviceToHost));
+                for (int b : redo) {
+                    const Plan &pb = plan[(size_t)i + (size_t)b * NS];
+                    BatchCtx c{};
+                    c.csr = &run;
+                    c.omega = g->pruned ? run.omega : nullptr;
+                    c.src = g->d_src + pb.off;
+                    c.nl = pb.nl;
+                    c.st = x.st;
+                    c.run_backward = true;
+                    c.endpoint = true;
+                    if (capture) {
+                        c.cap_vslot = g->capt.d_vslot;
+                        c.cap_depth = g->capt.d_depth;
+                        c.cap_sigma = g->capt.d_sigma;
+                        c.cap_delta = g->capt.d_delta;
+                        c.cap_tier = g->capt.d_tier;
+                    }
+                    CK(widen_rows(g, x.ws));
+                    CK(run_batch_w<double>(g, x, W, c, nullptr, nullptr));
+                }
+            }
+        }
+        for (int i = 0; i < NS; ++i) {
+            LaneCtx &x = g->ctx[i];
+            CU(cudaEventRecord(x.done, x.st));
+            CU(cudaStreamWaitEvent(st, x.done, 0));
+            if (i > 0) {
+                add_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((int)n, x.d_bc, g->d_bc);
+                g->last.kernel_launches += 1;
+            }
+            add_stats_kernel<<<1, 32, 0, st>>>(x.d_stats, g->d_stats);
+            CU(cudaMemcpyAsync(g->h_pin + 8 + 8 * i, x.gb_cnt, 64, cudaMemcpyDeviceToHost, st));
+            g->last.batches += x.last.batches;
+            g->last.levels_total += x.last.levels_total;  // host fp64 re-runs
+            g->last.kernel_launches += x.last.kernel_launches + (int64_t)x.gnodes * x.last.batches;
+        }
+    } else if (mode == 1 && !trav.empty()) {
         NS = std::max(1, std::min(NS, (int)plan.size()));
         for (int i = 0; i < NS; ++i) {
             CK(ctx_init(g, g->ctx[i]));
@@ -1971,8 +2469,7 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
         g->last.kernel_launches += 1;
     }
     CU(cudaGetLastError());
-    unsigned long long hst[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    CU(cudaMemcpyAsync(hst, g->d_stats, sizeof(hst), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(g->h_pin, g->d_stats, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     if (dev_out) {
         unpermute_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((int)n, run.inv, g->d_bc, out_bc);
     } else {
@@ -1983,6 +2480,19 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     g->last.kernel_launches += 1;
     if (capture) CK(capture_finish(g, st, mode == 2));
     if (g->profile) cudaEventRecord(t1, st);
+    bool any_dl = false;
+    for (bool u : g->devloop_used) any_dl |= u;
+    // Stream-ordered and asynchronous when every batch ran device-driven and
+    // the output is on the device: the call returns once the work is
+    // enqueued (the counters land in pinned memory; bc_get_stats waits for
+    // them).  Otherwise the call has already waited (host-driven level loop,
+    // host output, capture, profiling) and completes here.
+    const bool sync = !dev_out || capture || g->profile || trace_on() || !any_dl || mode != 1;
+    if (!sync) {
+        CU(cudaEventRecord(g->stats_ev, st));
+        g->stats_pending = true;
+        return BC_OK;
+    }
     CU(cudaStreamSynchronize(st));
     if (trace_on()) {
         const double t = now_us();
@@ -1994,21 +2504,16 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
             x.sync_us = 0;
             x.syncs = 0;
         }
-        fprintf(stderr, "[bc_trace] n=%lld sources=%lld mode=%d batches=%lld: setup %.0f us (resolve %.0f, sizing %.0f, "
-                        "plan %.0f, memset %.0f), pipelines %.0f us "
+        fprintf(stderr, "[bc_trace] n=%lld sources=%lld mode=%d device-loop=%d batches=%lld: setup %.0f us (resolve %.0f, "
+                        "sizing %.0f, plan %.0f, memset %.0f), pipelines %.0f us "
                         "(per-level waits %d, %.0f us summed over threads), finish %.0f us, total %.0f us\n",
-                (long long)n, (long long)trav.size(), mode, (long long)g->last.batches, tr_plan - tr0, tr_m[0] - tr0,
-                tr_m[1] - tr_m[0], tr_m[2] - tr_m[1], tr_plan - tr_m[2],
+                (long long)n, (long long)trav.size(), mode, (int)any_dl, (long long)g->last.batches, tr_plan - tr0,
+                tr_m[0] - tr0, tr_m[1] - tr_m[0], tr_m[2] - tr_m[1], tr_plan - tr_m[2],
                 tr_join > 0 ? tr_join - tr_plan : 0.0, sc, su, t - (tr_join > 0 ? tr_join : tr_plan), t - tr0);
     }
-    g->last.reached = (int64_t)hst[0];
-    g->last.adj_reached = (int64_t)hst[1];
-    g->last.dag_edges = (int64_t)hst[2];
-    g->last.dist_sum = (int64_t)hst[3];
-    g->last.fwd_items = (int64_t)hst[4];
-    g->last.fwd_hits = (int64_t)hst[5];
-    g->last.bwd_items = (int64_t)hst[6];
-    g->last.bwd_hits = (int64_t)hst[7];
+    finalize_stats(g);
+    if (g->dl_violation)
+        return fail(BC_ERR_INTERNAL, "a BFS exceeded the graph's depth bound (%d levels)", g->depth_bound);
     if (g->profile) {
         g->last.fwd_ms = sum_events(ef);
         for (auto &x : g->ctx) {

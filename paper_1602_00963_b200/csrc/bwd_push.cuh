@@ -128,6 +128,7 @@ __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double
 // finalises the ones at level L (most vertices are not at any given level)
 template <int W, bool COEF, typename RT = double>
 __global__ void __launch_bounds__(BC_NT) lanes_bwd_finalize_kernel(LanesParams p, double *__restrict__ A) {
+    if ((p.prev_new && *p.prev_new == 0) || gated_off(p)) return;
     const int lane = lane_id();
     const int nwarps = (int)((gridDim.x * (size_t)BC_NT) >> 5);
     RT *__restrict__ S = reinterpret_cast<RT *>(p.S_cur);
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(BC_NT) lanes_bwd_finalize_kernel(LanesParams p
 // adjacency segments ran on several CTAs; warp per hub)
 template <int W, typename RT = double>
 __global__ void __launch_bounds__(BC_NT) lanes_bwd_hub_fin_kernel(LanesParams p, double *__restrict__ A) {
+    if ((p.prev_new && *p.prev_new == 0) || gated_off(p)) return;
     const int h = (int)(((size_t)blockIdx.x * BC_NT + threadIdx.x) >> 5);
     if (h >= p.nhub) return;
     const int x = p.hub_ids[h];
@@ -626,7 +628,9 @@ struct PushKernel {
 
 template <int W, bool FWD, typename RT = double>
 __global__ void __launch_bounds__(BC_NT, (W == 8 ? BC_PUSH_MINB8 : BC_PUSH_MINB)) lanes_push_kernel(LanesParams p, double *A) {
-    if (FWD && p.prev_new && *p.prev_new == 0) return;
+    // forward: speculative launch past the last level; backward (device-driven
+    // batch): level L empty.  Either: tier not in use
+    if ((p.prev_new && *p.prev_new == 0) || gated_off(p)) return;
     __shared__ PushSmem<W> sm;
     PushKernel<W, FWD, RT> k(p, A, sm);
     const int total = p.nseg + p.ntiles;

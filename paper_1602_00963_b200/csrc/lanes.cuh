@@ -187,7 +187,18 @@ struct LanesParams {
     const int *prev_new;         // forward: flag "level L is non-empty"; 0 -> the launch is a no-op
                                  // (levels are launched one ahead of the host's termination test)
     void *part;                  // [gridDim][BC_NW][2][K] SigT: partial sums of slots split across warps
+    // device-driven batches (bc_api.cu graph mode; all nullable): the
+    // batch's lanes in use come from device memory, and a launch is a
+    // no-op unless *need != 0 and *halt == 0 (sigma-tier fallback)
+    const uint64_t *active_dev;  // [8]
+    const int *need;
+    const int *halt;
 };
+
+__device__ __forceinline__ bool gated_off(const int *need, const int *halt) {
+    return (need && *need == 0) || (halt && *halt != 0);
+}
+__device__ __forceinline__ bool gated_off(const LanesParams &p) { return gated_off(p.need, p.halt); }
 
 // verification capture of delta_s(x) (bc_set_capture): lane l of the batch,
 // vertex x; a no-op unless a capture is active (p.lane_cap != nullptr)
@@ -215,6 +226,7 @@ struct LanesSmem {
     int2 hsv[BC_NW * 32];                     // per warp: (slot, v) of the step's items
     uint32_t povf[BC_NW * 2 * 32];
     double ns[64 * W];  // per-lane n_s partial sums of this CTA (pruned graphs)
+    uint64_t act[8];    // lanes in use (from p.active_dev or p.active)
     unsigned long long st[6];  // CTA statistics (flushed from 32-bit thread counters per work unit)
     int scan[2 * BC_NW + 2];
     int unit;
@@ -289,6 +301,7 @@ struct LanesKernel {
         if (!BWD && p.lane_ns)
             for (int l = threadIdx.x; l < K; l += BC_NT) sm.ns[l] = 0.0;
         if (threadIdx.x < 6) sm.st[threadIdx.x] = 0;
+        if (threadIdx.x < W) sm.act[threadIdx.x] = p.active_dev ? p.active_dev[threadIdx.x] : p.active[threadIdx.x];
         __syncthreads();
     }
 
@@ -644,7 +657,7 @@ struct LanesKernel {
             if (deg > 0 && deg <= p.hub_deg) {
 #pragma unroll
                 for (int j = 0; j < W; ++j) {
-                    u[j] = BWD ? p.mask_cur[(size_t)x * W + j] : p.active[j] & ~p.seen[(size_t)x * W + j];
+                    u[j] = BWD ? p.mask_cur[(size_t)x * W + j] : sm.act[j] & ~p.seen[(size_t)x * W + j];
                     act |= (u[j] != 0);
                 }
             }
@@ -717,7 +730,7 @@ struct LanesKernel {
         bool any = false;
 #pragma unroll
         for (int j = 0; j < W; ++j) {
-            u[j] = BWD ? p.mask_cur[(size_t)x * W + j] : p.active[j] & ~p.seen[(size_t)x * W + j];
+            u[j] = BWD ? p.mask_cur[(size_t)x * W + j] : sm.act[j] & ~p.seen[(size_t)x * W + j];
             any |= (u[j] != 0);
         }
         if (!any) return;  // uniform
@@ -795,6 +808,7 @@ template <int W, typename SigT, bool BWD = false>
 __global__ void __launch_bounds__(BC_NT, (W == 8 ? BC_MINB8 : (W == 4 ? BC_MINB4 : BC_MINB))) lanes_level_kernel(LanesParams p) {
     extern __shared__ __align__(16) unsigned char smraw[];
     if (p.prev_new && *p.prev_new == 0) return;  // speculative launch past the last level
+    if (gated_off(p)) return;                     // device-driven batch: tier not in use
     LanesSmem<W, SigT> &sm = *reinterpret_cast<LanesSmem<W, SigT> *>(smraw);
     LanesKernel<W, SigT, BWD> k(p, sm);
     const int total = p.nseg + p.ntiles;
@@ -821,6 +835,7 @@ __global__ void __launch_bounds__(BC_NT) lanes_hub_finalize(LanesParams p) {
     using KK = LanesKernel<W, SigT, BWD>;
     constexpr int K = KK::K, LPT = KK::LPT;
     if (p.prev_new && *p.prev_new == 0) return;
+    if (gated_off(p)) return;
     extern __shared__ __align__(16) unsigned char smraw[];
     LanesSmem<W, SigT> &sm = *reinterpret_cast<LanesSmem<W, SigT> *>(smraw);
     KK k(p, sm);
@@ -846,7 +861,7 @@ __global__ void __launch_bounds__(BC_NT) lanes_hub_finalize(LanesParams p) {
             }
             uint64_t um[W];
 #pragma unroll
-            for (int j = 0; j < W; ++j) um[j] = p.active[j] & ~p.seen[(size_t)x * W + j];
+            for (int j = 0; j < W; ++j) um[j] = sm.act[j] & ~p.seen[(size_t)x * W + j];
             const uint32_t ub = pick2<W>(um, k.t2);
             k.commit_fwd(x, p.rp[x + 1] - p.rp[x], ub, acc, aovf);
         }
@@ -862,9 +877,10 @@ __global__ void __launch_bounds__(BC_NT) lanes_init_kernel(LanesParams p, const 
     constexpr int K = 64 * W;
     __shared__ double red_d[BC_NW];
     __shared__ unsigned long long red_u[BC_NW];
+    if (gated_off(p)) return;
     const int l = blockIdx.x;
     const int s = src[l];
-    if (s < 0) return;  // unused lane of a 2-degree batch layout
+    if (s < 0) return;  // unused lane (2-degree batch layout, or past the end of a device-driven batch)
     const int word = l >> 6;
     const uint64_t bit = 1ull << (l & 63);
     const int rs = p.rp[s], re = p.rp[s + 1];
@@ -1017,7 +1033,9 @@ __global__ void derive_ns_kernel(int K, DeriveParams q, double *lane_ns) {
 // Rows of levels 0 and 1: sigma = 1 in the lanes of the level mask, 0 elsewhere
 // (warp per vertex; vertices outside the level skip).
 template <int W, typename SigT>
-__global__ void lanes_materialize_kernel(int n, const uint64_t *mask, SigT *S) {
+__global__ void lanes_materialize_kernel(int n, const uint64_t *mask, SigT *S, const int *need = nullptr,
+                                         const int *halt = nullptr) {
+    if (gated_off(need, halt)) return;
     // thread per vertex finds the vertices of the level, then the warp
     // writes each of their rows (most vertices are at neither level)
     constexpr int K = 64 * W, LPT = 2 * W;
@@ -1056,7 +1074,8 @@ __global__ void gather_level_lane0_kernel(int n, const uint64_t *mask, int W, co
 
 // Endpoint term of the attributed 1-degree form (R13): BC[s] += omega(s)(n_s - 2).
 __global__ void lanes_endpoint_kernel(const int *src, int nlanes, const uint32_t *omega, const double *lane_ns,
-                                      double *bc) {
+                                      double *bc, const int *need = nullptr, const int *halt = nullptr) {
+    if (gated_off(need, halt)) return;
     const int l = blockIdx.x * blockDim.x + threadIdx.x;
     if (l < nlanes && src[l] >= 0) {
         const int s = src[l];
@@ -1081,8 +1100,10 @@ __global__ void trivial_sources_kernel(const int *src, int ns, const uint32_t *o
 // only the captured lanes' bits are visited: capmask = OR of their bits).
 template <int W, typename RT>
 __global__ void cap_extract_kernel(int n, int L, const uint64_t *mask, const RT *rows, const int *lane_cap,
-                                   const uint64_t *capmask, int *cap_depth, double *cap_sigma) {
+                                   const uint64_t *capmask, int *cap_depth, double *cap_sigma,
+                                   const int *need = nullptr, const int *halt = nullptr, const int *nonempty = nullptr) {
     constexpr int K = 64 * W;
+    if (gated_off(need, halt) || (nonempty && *nonempty == 0)) return;
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
 #pragma unroll
@@ -1101,7 +1122,9 @@ __global__ void cap_extract_kernel(int n, int L, const uint64_t *mask, const RT 
 }
 
 // the sigma-row tier (16 / 32 / 64 bits) the captured lanes' batch completed with
-__global__ void cap_tier_kernel(int K, const int *lane_cap, int tier, int *cap_tier) {
+__global__ void cap_tier_kernel(int K, const int *lane_cap, int tier, int *cap_tier, const int *need = nullptr,
+                                const int *halt = nullptr) {
+    if (gated_off(need, halt)) return;
     const int l = blockIdx.x * blockDim.x + threadIdx.x;
     if (l < K && lane_cap[l] >= 0) cap_tier[lane_cap[l]] = tier;
 }

@@ -490,3 +490,78 @@ def test_concurrent_pipelines_agree():
             G.set_option(bcb.OPT_LANE_WORDS, 1)  # many batches
             assert_bc_close(G.compute(S), want)
             assert G.stats()["batches"] == (len(S) + 63) // 64
+
+
+@pytest.mark.parametrize("loop", [0, 1, 2])
+def test_device_loop_and_host_loop_agree(loop):
+    """BC_OPT_DEVICE_LOOP: device-driven batches (one CUDA graph launch per
+    batch, 8-byte rows with the fp64 tier in the graph, or 4-byte rows with
+    the host fp64 re-run) and the host-driven level loop give the oracle's
+    BC on the small suite, pruned and unpruned, with split hubs."""
+    bcb = _bcb()
+    for g in SUITE:
+        for prune in (False, True):
+            with bcb.Graph.from_csr(g) as G:
+                G.set_option(bcb.OPT_MODE, 1)
+                G.set_option(bcb.OPT_DEVICE_LOOP, loop)
+                G.set_option(bcb.OPT_HUB_DEGREE, 32)
+                if prune:
+                    G.prune_degree1()
+                assert_bc_close(G.compute(), oracle.bc(g))
+
+
+@pytest.mark.parametrize("loop", [1, 2])
+@pytest.mark.parametrize("layers", [8, 12])
+def test_device_loop_sigma_tiers(loop, layers):
+    """sigma beyond 16 bits (layers = 8) and beyond 32 bits (layers = 12) in
+    device-driven batches: the 32-bit tier runs inside the graph, the fp64
+    tier too with 8-byte rows (loop 1) or on the host path with 4-byte rows
+    (loop 2); BC and the per-source counters match the oracle."""
+    bcb = _bcb()
+    g = gg.disjoint_union(layered(10, layers), gg.rmat(9, 8, seed=3))
+    want, stats = oracle.bc(g, stats=True)
+    S = g.non_isolated()
+    with bcb.Graph.from_csr(g) as G:
+        G.set_option(bcb.OPT_MODE, 1)
+        G.set_option(bcb.OPT_LANE_WORDS, 1)
+        G.set_option(bcb.OPT_SOURCE_ORDER, 0)
+        G.set_option(bcb.OPT_DEVICE_LOOP, loop)
+        got = G.compute(S)
+        st = G.stats()
+    assert_bc_close(got, want)
+    assert st["reached"] == int(stats[S, 0].sum())
+    assert st["adj_reached"] == int(stats[S, 1].sum())
+    assert st["dag_edges"] == int(stats[S, 2].sum())
+    assert st["narrow_fallbacks"] >= 1
+    assert st["narrow_batches"] + st["narrow_fallbacks"] == st["batches"]
+    if layers == 8:
+        assert st["mid_batches"] == st["narrow_fallbacks"]
+    else:
+        assert st["mid_batches"] < st["narrow_fallbacks"]
+
+
+def test_device_loop_is_stream_ordered():
+    """With a device output on a stream, bc_compute (device-driven) returns
+    once enqueued; work queued behind it on the stream sees the result, and
+    a second call on the same handle is ordered after the first."""
+    import torch
+
+    bcb = _bcb()
+    g = gg.rmat(12, 16, seed=1)
+    S1, S2 = g.non_isolated()[:1500], g.non_isolated()[1500:]
+    w1, w2 = oracle.bc(g, S1), oracle.bc(g, S2)
+    with bcb.Graph.from_csr(g) as G:
+        s = torch.cuda.Stream()
+        a = torch.empty(g.n, dtype=torch.float64, device="cuda")
+        b = torch.empty(g.n, dtype=torch.float64, device="cuda")
+        with torch.cuda.stream(s):
+            G.compute(S1, out=a, stream=s)
+            a2 = a * 2.0  # queued behind the call on the same stream
+            G.compute(S2, out=b, stream=s)
+            tot = a + b
+        s.synchronize()
+        st = G.stats()
+        assert st["batches"] >= 1
+        assert_bc_close(a2.cpu().numpy() / 2.0, w1)
+        assert_bc_close(b.cpu().numpy(), w2)
+        assert_bc_close(tot.cpu().numpy(), w1 + w2)
