@@ -192,12 +192,19 @@ typedef enum {
     BC_OPT_TWO_DEGREE = 11, /* lanes mode: 1 = 2-degree heuristic: a degree-2 source
                                whose two neighbours are also sources gets its shortest-path tree derived
                                from theirs (Lemma 1, Eq.(6)) instead of a traversal; default 0 */
-    BC_OPT_DEVICE_LOOP = 12 /* lanes mode: 1 (default) = device-driven batches when eligible -- each batch
+    BC_OPT_DEVICE_LOOP = 12, /* lanes mode: 1 (default) = device-driven batches when eligible -- each batch
                                (every level, the sigma-tier fallbacks) is one CUDA graph launch with the
                                termination test on the device; 0 = host-driven level loop
                                (one host wait per level); 2 = device-driven with 4-byte rows forced (the
                                fp64 tier then re-runs on the host-driven path; testing).  Eligible: default
                                sweep options, no profiling, graph depth bound <= 32 levels (bc_graph_create) */
+    BC_OPT_SLICES_KERNEL = 13 /* slices mode kernel (NEXT-2 ablation): 0 = auto; 1 = general (frontier
+                               degrees block-scanned into CD + binary search; push sigma
+                               with fp64 atomics); 2 = general with prefix-sum reuse (the forward's CD
+                               prefixes kept and reused by the backward); 3 = degree-
+                               bounded, thread per frontier vertex, pull, global bitmaps; 4 = the same with
+                               a 2-bit per-vertex state in shared memory (n <= 1179648).  3/4 need max
+                               degree <= 64, else bc_compute fails with BC_ERR_INVALID */
 } bc_option;
 
 bc_status bc_set_option(bc_graph *g, int option, int64_t value);

@@ -21,7 +21,8 @@ from . import _lib as _L
 
 __all__ = ["Graph", "BCError", "build", "BC_CREATE_VALIDATE", "OPT_LANE_WORDS", "OPT_HUB_DEGREE",
            "OPT_PROFILE", "OPT_MODE", "OPT_RELABEL", "OPT_SOURCE_ORDER", "OPT_FWD_PUSH",
-           "OPT_BWD_MODE", "OPT_SIGMA_WIDTH", "OPT_STREAMS", "OPT_TWO_DEGREE", "OPT_DEVICE_LOOP"]
+           "OPT_BWD_MODE", "OPT_SIGMA_WIDTH", "OPT_STREAMS", "OPT_TWO_DEGREE", "OPT_DEVICE_LOOP",
+           "OPT_SLICES_KERNEL"]
 
 BC_CREATE_VALIDATE = 0x1
 OPT_LANE_WORDS, OPT_HUB_DEGREE, OPT_PROFILE, OPT_MODE, OPT_RELABEL, OPT_SOURCE_ORDER, OPT_FWD_PUSH = 1, 2, 3, 4, 5, 6, 7
@@ -30,6 +31,7 @@ OPT_SIGMA_WIDTH = 9
 OPT_STREAMS = 10
 OPT_TWO_DEGREE = 11
 OPT_DEVICE_LOOP = 12
+OPT_SLICES_KERNEL = 13
 build = _L.build
 
 

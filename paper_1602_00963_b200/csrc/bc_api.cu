@@ -176,6 +176,9 @@ constexpr int TILE_ITEMS = 8192; // non-hub adjacency items per level-kernel til
 #ifndef BC_TILE_MIN
 #define BC_TILE_MIN 256          // ... and the smallest cap (small graphs, see build_layout)
 #endif
+#ifndef BC_TILE_PER_SM
+#define BC_TILE_PER_SM 1         // tiles are halved until a level's adjacency makes this many per SM
+#endif
 constexpr int MAX_STREAMS = 8;   // concurrent batch pipelines (BC_OPT_STREAMS)
 #ifndef BC_DEVLOOP_MAX_LEVELS
 #define BC_DEVLOOP_MAX_LEVELS 32  // device-driven batches only for graphs whose depth bound is at most this
@@ -256,7 +259,9 @@ struct SlicesWS {
     bool full = false;     // cf and bcp allocated
     int4 *ell = nullptr;   // [n] padded neighbours (max degree <= 4)
     int4 *qrow = nullptr;  // [rows][n] neighbour rows in queue order (BC_SM_QROW)
+    int *cdq = nullptr;    // [rows][n] the forward's chunk degree prefixes (prefix-sum reuse variant)
     void release() {
+        dfree(cdq);
         dfree(bm);
         dfree(qrow);
         dfree(ell);
@@ -305,6 +310,7 @@ struct bc_graph {
     std::vector<TdBatch> td_plan;
     std::vector<int> td_lanes;
     int depth_bound = -1;      // every BFS depth of the graph is <= this (bc_graph_create); -1 unknown
+    int slices_kernel = 0;     // BC_OPT_SLICES_KERNEL: 0 auto, 1 general, 2 general + prefix reuse, 3/4 degree-bounded
     int device_loop = 1;       // BC_OPT_DEVICE_LOOP: device-driven batches (CUDA graph per pipeline) when eligible
     struct Sizing {            // last call's lane width / row width / pipelines (skips cudaMemGetInfo when unchanged)
         int64_t key[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
@@ -398,11 +404,11 @@ bc_status build_layout(bc_graph *g, DevCSR &c, cudaStream_t st) {
     int64_t items = 0;
     const int64_t n = g->n;
     // Items per tile: at most TILE_ITEMS, and small enough that a level's
-    // adjacency makes ~8 tiles per SM -- on a small graph (S12: 97k items) a
+    // adjacency makes BC_TILE_PER_SM tiles per SM -- on a small graph (S12: 97k items) a
     // level's tiles are few, and a warp's serial walk over its share of a
     // large tile is the level's critical path.
     int64_t cap = TILE_ITEMS;
-    while (cap > BC_TILE_MIN && c.nnz / cap < 8LL * g->num_sms) cap >>= 1;
+    while (cap > BC_TILE_MIN && c.nnz / cap < (int64_t)BC_TILE_PER_SM * g->num_sms) cap >>= 1;
     for (int64_t v = 0; v < n; ++v) {
         const int d = c.h_deg[v] > g->hub_deg ? 0 : c.h_deg[v];
         if (cnt == TV || (cnt > 0 && items + d > cap)) {
@@ -1420,8 +1426,8 @@ bc_status ensure_device_batch(bc_graph *g, LaneCtx &x, int nbatches) {
     return BC_OK;
 }
 
-bc_status ensure_slices(bc_graph *g, int rows, bool full) {
-    if (g->sws.rows >= rows && (g->sws.full || !full)) return BC_OK;
+bc_status ensure_slices(bc_graph *g, int rows, bool full, bool reuse) {
+    if (g->sws.rows >= rows && (g->sws.full || !full) && (g->sws.cdq || !reuse)) return BC_OK;
     g->sws.release();
     const size_t n = (size_t)g->n;
     SlicesWS &w = g->sws;
@@ -1443,6 +1449,7 @@ bc_status ensure_slices(bc_graph *g, int rows, bool full) {
         CU(cudaMemset(w.cf, 0, cnt * 8));
         CU(cudaMemset(w.bcp, 0, cnt * 8));
     }
+    if (reuse) CK(dalloc(&w.cdq, cnt));
     CU(cudaDeviceSynchronize());
     w.rows = rows;
     w.full = full;
@@ -1466,10 +1473,21 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
 #endif
     int maxdeg = 0;
     for (int d : run.h_deg) maxdeg = std::max(maxdeg, d);
-    const bool lowdeg = maxdeg <= BC_LOWDEG;  // vertex-per-thread pull variant, no fp atomics
-    const bool ell = BC_SLICES_ELL && maxdeg <= 4;  // neighbours as one int4 load
     const size_t sm2_bytes = (size_t)((g->n + 15) / 16) * sizeof(unsigned);
-    const bool sm2 = lowdeg && BC_SLICES_SM2 && sm2_bytes <= (size_t)BC_SLICES_SM2_MAXB;
+    // kernel: auto = the shared-memory 2-bit state kernel when the graph is
+    // degree-bounded and the state fits, else the global-bitmap degree-bounded
+    // kernel, else the general one (CD scan + binary search mapping);
+    // BC_OPT_SLICES_KERNEL forces one (NEXT-2 ablation)
+    const int sk = g->slices_kernel;
+    const bool can_low = maxdeg <= BC_LOWDEG;
+    const bool can_sm2 = can_low && sm2_bytes <= (size_t)BC_SLICES_SM2_MAXB;
+    if ((sk == 3 && !can_low) || (sk == 4 && !can_sm2))
+        return fail(BC_ERR_INVALID, "slices kernel %d needs max degree <= %d%s", sk, BC_LOWDEG,
+                    sk == 4 ? " and n <= 1179648" : "");
+    const bool lowdeg = sk == 0 ? can_low : (sk == 3 || sk == 4);  // vertex-per-thread pull variant, no fp atomics
+    const bool reuse = sk == 2;                                    // general kernel with prefix-sum reuse
+    const bool ell = BC_SLICES_ELL && maxdeg <= 4;  // neighbours as one int4 load
+    const bool sm2 = lowdeg && (sk == 4 || (sk == 0 && BC_SLICES_SM2 && can_sm2));
     const bool smem_bm = !lowdeg && BC_SLICES_SMEM_BM && g->n <= (int64_t)SLICES_SMEM_BM_WORDS * 32;
     const size_t dsm = sm2 ? sm2_bytes : smem_bm ? 2 * SLICES_SMEM_BM_WORDS * sizeof(unsigned) : 0;
     // CAP instantiations (verification capture, bc_set_capture) keep the
@@ -1478,6 +1496,7 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
                                 : (cap ? slices_lowdeg_sm_kernel<false, true> : slices_lowdeg_sm_kernel<false>))
                 : lowdeg ? (ell ? (cap ? slices_lowdeg_kernel<true, true> : slices_lowdeg_kernel<true>)
                                 : (cap ? slices_lowdeg_kernel<false, true> : slices_lowdeg_kernel<false>))
+                : reuse  ? (cap ? slices_kernel<false, true, true> : slices_kernel<false, false, true>)
                          : (smem_bm ? (cap ? slices_kernel<true, true> : slices_kernel<true>)
                                     : (cap ? slices_kernel<false, true> : slices_kernel<false>));
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
@@ -1488,7 +1507,7 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
     if (lowdeg) occ = std::min(occ, BC_SL_OCC);  // experiment builds: cap the sources in flight per SM
 #endif
     const int rows = std::max(1, std::min(ns, g->num_sms * std::max(1, occ)));
-    CK(ensure_slices(g, rows, !lowdeg));
+    CK(ensure_slices(g, rows, !lowdeg, reuse));
     if (ell) {
         build_ell4_kernel<<<(unsigned)((g->n + 255) / 256), 256, 0, st>>>((int)g->n, run.rp, run.col, g->sws.ell);
         g->last.kernel_launches += 1;
@@ -1511,6 +1530,7 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
     p.bc = g->d_bc;
     p.ell4 = ell ? g->sws.ell : nullptr;
     p.qrow = g->sws.qrow;
+    p.cdq = g->sws.cdq;
     p.stats = g->d_stats;
     if (cap) {
         p.cap_vslot = g->capt.d_vslot;
@@ -1954,6 +1974,10 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
         case BC_OPT_MODE:
             if (value < 0 || value > 2) return fail(BC_ERR_INVALID, "mode must be 0, 1 or 2");
             g->mode = (int)value;
+            return BC_OK;
+        case BC_OPT_SLICES_KERNEL:
+            if (value < 0 || value > 4) return fail(BC_ERR_INVALID, "slices kernel must be 0..4");
+            g->slices_kernel = (int)value;
             return BC_OK;
         case BC_OPT_DEVICE_LOOP:
             if (value < 0 || value > 2) return fail(BC_ERR_INVALID, "device loop must be 0, 1 or 2");

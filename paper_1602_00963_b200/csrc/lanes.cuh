@@ -84,6 +84,39 @@ __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// ---- Blackwell bulk copies (TMA engine, cp.async.bulk) with mbarrier completion
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *mb, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+// one arrival that also announces `bytes` of transaction (the bulk copy's completion)
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *mb, uint32_t bytes) {
+    uint64_t state;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
+                 : "=l"(state) : "r"(smem_u32(mb)), "r"(bytes) : "memory");
+    (void)state;
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t *mb, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok) : "r"(smem_u32(mb)), "r"(parity) : "memory");
+    } while (!ok);
+}
+// global -> shared bulk copy of `bytes` (multiple of 16, 16-byte aligned), completing on mb
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *mb) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(mb)) : "memory");
+}
+// order earlier generic-proxy accesses of shared memory before later async-proxy (bulk copy) writes
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+#ifndef BC_FWD_BULK
+#define BC_FWD_BULK 0  // 1: 16-bit forward hit rows gathered by bulk copies into a per-warp shared ring (slower: profiles/exp_r2_fwd_bulk.txt)
+#endif
 // 16-byte async copy with zero fill when !valid, L2 cache policy
 __device__ __forceinline__ void cp_async16z(void *smem_dst, const void *gsrc, bool valid, uint64_t pol) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -230,6 +263,12 @@ struct LanesSmem {
     unsigned long long st[6];  // CTA statistics (flushed from 32-bit thread counters per work unit)
     int scan[2 * BC_NW + 2];
     int unit;
+    // 16-bit forward with BC_FWD_BULK: per warp a ring of RING sigma rows
+    // (K x 16 bit) filled by bulk copies, one mbarrier per slot
+    static constexpr bool BULK = BC_FWD_BULK && std::is_same<SigT, unsigned>::value;
+    static constexpr int RING = BULK ? (W >= 8 ? 2 : (W == 4 ? 4 : 8)) : 1;
+    alignas(128) uint32_t ring[BULK ? BC_NW * RING * 32 * W : 4];
+    alignas(8) uint64_t mbar[BC_NW * RING];
 };
 
 // Lane -> thread mapping of the level kernel ("pair-strided"): thread t of
@@ -293,6 +332,7 @@ struct LanesKernel {
     // per-thread statistics of the current work unit (bounded by its items, so
     // 32 bits suffice except the adjacency sum); flushed by flush_stats()
     unsigned st_reach = 0, st_dag = 0, st_dsum = 0, st_items = 0, st_hits = 0;
+    unsigned ring_issued = 0, ring_used = 0;  // BC_FWD_BULK: bulk copies issued / consumed by this warp (uniform)
     unsigned long long st_adj = 0;
     int any_new_loc = 0;
 
@@ -302,6 +342,10 @@ struct LanesKernel {
             for (int l = threadIdx.x; l < K; l += BC_NT) sm.ns[l] = 0.0;
         if (threadIdx.x < 6) sm.st[threadIdx.x] = 0;
         if (threadIdx.x < W) sm.act[threadIdx.x] = p.active_dev ? p.active_dev[threadIdx.x] : p.active[threadIdx.x];
+        if constexpr (Smem::BULK && !BWD) {
+            if (threadIdx.x < BC_NW * Smem::RING) mbar_init(sm.mbar + threadIdx.x, 1);
+            mbar_init_fence();
+        }
         __syncthreads();
     }
 
@@ -546,6 +590,59 @@ struct LanesKernel {
                 }
                 const uint32_t *hcw = sm.hc + wid * 32 * 2 * W + (lane >> 4) * W;
                 const int sh = t2 & 31;
+                if constexpr (Smem::BULK && !BWD) {
+                    // 16-bit forward, Blackwell bulk copies: lane 0 streams the
+                    // hit rows (K x 16 bit, zero outside level L, so whole rows
+                    // are added -- lanes outside c only collect what the commit
+                    // discards) into the warp's shared ring, up to RING hits
+                    // ahead; the warp adds a row once its mbarrier completes
+                    constexpr int RG = Smem::RING;
+                    constexpr uint32_t RB = (uint32_t)K * 2u;
+                    uint32_t *ringw = sm.ring + (size_t)wid * RG * 32 * W;
+                    uint64_t *mbw = sm.mbar + wid * RG;
+                    unsigned hi = hm;
+                    auto issue = [&]() {
+                        const int s = __ffs(hi) - 1;
+                        hi &= hi - 1;
+                        if (lane == 0) {
+                            const int slot = (int)(ring_issued & (RG - 1));
+                            fence_proxy_async_smem();  // the slot's previous row was read by generic loads
+                            mbar_arrive_expect_tx(mbw + slot, RB);
+                            bulk_g2s(ringw + slot * 32 * W, Scur() + (size_t)sm.hsv[wid * 32 + s].y * K, RB, mbw + slot);
+                        }
+                        ++ring_issued;
+                    };
+#pragma unroll 1
+                    for (int q = 0; q < RG && hi; ++q) issue();
+                    while (hm) {
+                        const int src = __ffs(hm) - 1;
+                        hm &= hm - 1;
+                        const int hs = sm.hsv[wid * 32 + src].x;
+                        if (hs != cur) {
+                            while (cur < hs) {
+                                flush(cur, first, ws, we, hub_mode, acc, aovf);
+                                ++cur;
+#pragma unroll
+                                for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
+                                aovf = 0;
+                            }
+                        }
+                        const int slot = (int)(ring_used & (RG - 1));
+                        mbar_wait_parity(mbw + slot, (ring_used / RG) & 1u);
+                        const uint32_t *row = ringw + slot * 32 * W + lane;
+#pragma unroll
+                        for (int pr = 0; pr < W; ++pr) {
+                            const uint32_t t = row[32 * pr];
+                            acc[2 * pr] += t & 0xffffu;
+                            acc[2 * pr + 1] += t >> 16;
+                        }
+                        ++ring_used;
+                        __syncwarp();
+                        if (hi) issue();
+                    }
+                    __syncwarp();
+                    continue;
+                }
                 while (hm) {
                     const int src = __ffs(hm) - 1;
                     hm &= hm - 1;

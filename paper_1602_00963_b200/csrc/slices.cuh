@@ -51,6 +51,8 @@ struct SlicesParams {
     const int4 *ell4;       // max degree <= 4: neighbours padded with -1, one 16-byte load per vertex
     int4 *qrow;             // [gridDim.x][n] ELL rows in queue order (BC_SM_QROW), else null
     unsigned *bm;           // global bitmaps [gridDim.x][2][bm_words] (when not in shared memory)
+    int *cdq;               // slices_kernel<REUSE>: [gridDim.x][n] inclusive frontier-degree prefix of each
+                            // queue position within its chunk (the forward's scan, reused backward)
     int bm_words;
     unsigned long long *stats;  // [4] reached, adjacency, dag edges, depth sum
     // verification capture (bc_set_capture; CAP instantiations only): slot of
@@ -86,19 +88,36 @@ struct SlicesSmem {
 
 // Process the items of frontier chunk Q[c0, c1) (<= BC_NT vertices); calls
 // f(v, w) for every item.
-template <typename F>
+// REUSE (prefix-sum reuse): the forward (STORE) writes
+// each queue position's inclusive degree prefix within its chunk to cdq; the
+// backward (LOAD) walks the same chunks of the same level (both cut Q from
+// the level start in steps of BC_NT) and reads the prefixes back instead of
+// re-scanning.
+template <int CDMODE = 0, typename F>  // 0: scan, 1: scan and store to cdq, 2: load from cdq
 __device__ __forceinline__ void slices_chunk_items(const SlicesParams &p, SlicesSmem &sm, const int *Q, int c0,
-                                                   int c1, F &&f) {
+                                                   int c1, F &&f, int *cdq = nullptr) {
     const int i = threadIdx.x;
     int deg = 0, v = -1, rs = 0;
-    if (c0 + i < c1) {
-        v = Q[c0 + i];
-        rs = p.rp[v];
-        deg = p.rp[v + 1] - rs;
-    }
     int ex, d1, tot, d2;
-    block_excl_scan2(deg, 0, ex, d1, tot, d2, sm.scan);
     const int nv = c1 - c0;
+    if constexpr (CDMODE == 2) {
+        if (i < nv) {
+            v = Q[c0 + i];
+            rs = p.rp[v];
+            ex = i > 0 ? cdq[c0 + i - 1] : 0;
+        }
+        tot = cdq[c1 - 1];
+    } else {
+        if (c0 + i < c1) {
+            v = Q[c0 + i];
+            rs = p.rp[v];
+            deg = p.rp[v + 1] - rs;
+        }
+        block_excl_scan2(deg, 0, ex, d1, tot, d2, sm.scan);
+        if constexpr (CDMODE == 1) {
+            if (i < nv) cdq[c0 + i] = ex + deg;
+        }
+    }
     if (i < nv) {
         sm.cd[i] = ex;
         sm.vs[i] = v;
@@ -113,7 +132,7 @@ __device__ __forceinline__ void slices_chunk_items(const SlicesParams &p, Slices
     __syncthreads();
 }
 
-template <bool SMEM_BM, bool CAP = false>
+template <bool SMEM_BM, bool CAP = false, bool REUSE = false>
 __global__ void __launch_bounds__(BC_NT) slices_kernel(SlicesParams p) {
     __shared__ SlicesSmem sm;
     extern __shared__ unsigned smbm[];  // 2 * SLICES_SMEM_BM_WORDS when SMEM_BM
@@ -123,6 +142,7 @@ __global__ void __launch_bounds__(BC_NT) slices_kernel(SlicesParams p) {
     int *Q = p.queue + blockIdx.x * n;
     int *loff = p.loff + blockIdx.x * (n + 2);
     double *bcp = p.bcp + blockIdx.x * n;
+    int *cdq = REUSE ? p.cdq + blockIdx.x * n : nullptr;
     unsigned *vis = SMEM_BM ? smbm : p.bm + (size_t)blockIdx.x * 3 * p.bm_words;
     unsigned *lvb = vis + (SMEM_BM ? SLICES_SMEM_BM_WORDS : p.bm_words);
     const int bmw = p.bm_words;
@@ -161,7 +181,7 @@ __global__ void __launch_bounds__(BC_NT) slices_kernel(SlicesParams p) {
         while (qs < qe) {
             for (int c0 = qs; c0 < qe; c0 += BC_NT) {
                 const int c1 = min(qe, c0 + BC_NT);
-                slices_chunk_items(p, sm, Q, c0, c1, [&](int v, int w) {
+                slices_chunk_items<REUSE ? 1 : 0>(p, sm, Q, c0, c1, [&](int v, int w) {
                     // visited bit clear => w is discovered now, at level L+1; the
                     // level bit is published before the visited bit, so a thread
                     // that finds w visited also sees whether it is at L+1
@@ -187,7 +207,7 @@ __global__ void __launch_bounds__(BC_NT) slices_kernel(SlicesParams p) {
                         atomicAdd(&sigma[w], sigma[v]);
                         ++st_dag;
                     }
-                });
+                }, cdq);
             }
             __syncthreads();
             qs = qe;
@@ -217,9 +237,9 @@ __global__ void __launch_bounds__(BC_NT) slices_kernel(SlicesParams p) {
                 __syncthreads();
                 for (int c0 = a; c0 < b; c0 += BC_NT) {
                     const int c1 = min(b, c0 + BC_NT);
-                    slices_chunk_items(p, sm, Q, c0, c1, [&](int w, int v) {
+                    slices_chunk_items<REUSE ? 2 : 0>(p, sm, Q, c0, c1, [&](int w, int v) {
                         if (lvb[v >> 5] & (1u << (v & 31))) atomicAdd(&cf[w], cf[v]);
-                    });
+                    }, cdq);
                 }
                 __syncthreads();
                 for (int i = a1 + threadIdx.x; i < b1; i += BC_NT) {

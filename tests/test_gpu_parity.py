@@ -565,3 +565,25 @@ def test_device_loop_is_stream_ordered():
         assert_bc_close(a2.cpu().numpy() / 2.0, w1)
         assert_bc_close(b.cpu().numpy(), w2)
         assert_bc_close(tot.cpu().numpy(), w1 + w2)
+
+
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4])
+def test_slices_kernel_variants(kernel):
+    """BC_OPT_SLICES_KERNEL (NEXT-2 ablation): the general kernel with and
+    without the prefix-sum reuse and both degree-bounded kernels agree with
+    the oracle; the degree-bounded ones refuse graphs of larger degree."""
+    bcb = _bcb()
+    for g in SUITE + [gg.grid(40, 300), gg.disjoint_union(gg.grid(30, 31), gg.random_tree(200, seed=8))]:
+        for prune in (False, True):
+            with bcb.Graph.from_csr(g) as G:
+                G.set_option(bcb.OPT_MODE, 2)
+                G.set_option(bcb.OPT_SLICES_KERNEL, kernel)
+                maxdeg = int(g.degrees.max()) if g.n else 0
+                if prune:
+                    G.prune_degree1()
+                    maxdeg = int(np.diff(G.pruning()[2]).max())
+                if kernel >= 3 and maxdeg > 64:
+                    with pytest.raises(bcb.BCError):
+                        G.compute()
+                    continue
+                assert_bc_close(G.compute(), oracle.bc(g))
