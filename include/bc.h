@@ -203,8 +203,10 @@ typedef enum {
                                with fp64 atomics); 2 = general with prefix-sum reuse (the forward's CD
                                prefixes kept and reused by the backward); 3 = degree-
                                bounded, thread per frontier vertex, pull, global bitmaps; 4 = the same with
-                               a 2-bit per-vertex state in shared memory (n <= 1179648).  3/4 need max
-                               degree <= 64, else bc_compute fails with BC_ERR_INVALID */
+                               a 2-bit per-vertex state in shared memory (n <= 1179648); 5 / 6 = 4 / 8
+                               sources per CTA swept in lockstep as lanes of one traversal (2-bit depth
+                               code per lane, one union frontier per level).  3-6 need max degree <= 64,
+                               else bc_compute fails with BC_ERR_INVALID */
 } bc_option;
 
 bc_status bc_set_option(bc_graph *g, int option, int64_t value);

@@ -18,6 +18,7 @@
 #include "lanes.cuh"
 #include "graph_kernels.cuh"
 #include "slices.cuh"
+#include "slices_multi.cuh"
 #include "bwd_push.cuh"
 #include "batch_ctl.cuh"
 #include <cub/device/device_radix_sort.cuh>
@@ -260,7 +261,21 @@ struct SlicesWS {
     int4 *ell = nullptr;   // [n] padded neighbours (max degree <= 4)
     int4 *qrow = nullptr;  // [rows][n] neighbour rows in queue order (BC_SM_QROW)
     int *cdq = nullptr;    // [rows][n] the forward's chunk degree prefixes (prefix-sum reuse variant)
+    // slices_multi_kernel (KS sources per CTA)
+    int mrows = 0, mks = 0;
+    uint32_t *mst2 = nullptr;
+    int *mapl = nullptr, *mq = nullptr, *mloff = nullptr;
+    double *msg = nullptr;
+    void release_multi() {
+        dfree(mst2);
+        dfree(mapl);
+        dfree(mq);
+        dfree(mloff);
+        dfree(msg);
+        mrows = mks = 0;
+    }
     void release() {
+        release_multi();
         dfree(cdq);
         dfree(bm);
         dfree(qrow);
@@ -1456,6 +1471,82 @@ bc_status ensure_slices(bc_graph *g, int rows, bool full, bool reuse) {
     return BC_OK;
 }
 
+bc_status ensure_multi(bc_graph *g, int rows, int ks) {
+    SlicesWS &w = g->sws;
+    if (w.mrows >= rows && w.mks == ks) return BC_OK;
+    w.release_multi();
+    const size_t n = (size_t)g->n;
+    CK(dalloc(&w.mst2, n * rows));
+    CK(dalloc(&w.mapl, n * rows));
+    CK(dalloc(&w.mq, n * ks * rows));
+    CK(dalloc(&w.mloff, (n + 2) * rows));
+    CK(dalloc(&w.msg, n * ks * rows));
+    CU(cudaMemset(w.mst2, 0, n * rows * 4));
+    CU(cudaMemset(w.mapl, 0xff, n * rows * 4));
+    CU(cudaDeviceSynchronize());
+    w.mrows = rows;
+    w.mks = ks;
+    return BC_OK;
+}
+
+template <int KS>
+bc_status run_slices_multi(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStream_t st,
+                           std::vector<cudaEvent_t> *ev, bool cap, bool ell) {
+    auto kern = ell ? (cap ? slices_multi_kernel<KS, true, true> : slices_multi_kernel<KS, true>)
+                    : (cap ? slices_multi_kernel<KS, false, true> : slices_multi_kernel<KS, false>);
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BC_SMU_NT, 0);
+    const int groups = (ns + KS - 1) / KS;
+    const int rows = std::max(1, std::min(groups, g->num_sms * std::max(1, occ)));
+    CK(ensure_multi(g, rows, KS));
+    if (ell) {
+        if (!g->sws.ell) CK(dalloc(&g->sws.ell, (size_t)g->n));
+        build_ell4_kernel<<<(unsigned)((g->n + 255) / 256), 256, 0, st>>>((int)g->n, run.rp, run.col, g->sws.ell);
+        g->last.kernel_launches += 1;
+    }
+    SlicesParams p{};
+    p.n = (int)g->n;
+    p.rp = run.rp;
+    p.col = run.col;
+    p.omega = g->pruned ? run.omega : nullptr;
+    p.src = d_src;
+    p.nsrc = ns;
+    p.next_src = g->d_work_ctr + 1;
+    p.bc = g->d_bc;
+    p.ell4 = ell ? g->sws.ell : nullptr;
+    p.stats = g->d_stats;
+    if (cap) {
+        p.cap_vslot = g->capt.d_vslot;
+        p.cap_depth = g->capt.d_depth;
+        p.cap_sigma = g->capt.d_sigma;
+        p.cap_delta = g->capt.d_delta;
+    }
+    MultiParams mp{};
+    mp.st2 = g->sws.mst2;
+    mp.apl = g->sws.mapl;
+    mp.sg = g->sws.msg;
+    mp.q = g->sws.mq;
+    mp.qcap = (long long)g->n * KS;
+    mp.loff = g->sws.mloff;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ev) {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+    }
+    kern<<<rows, BC_SMU_NT, 0, st>>>(p, mp);
+    if (ev) {
+        cudaEventRecord(e1, st);
+        ev->push_back(e0);
+        ev->push_back(e1);
+    }
+    CU(cudaGetLastError());
+    g->last.kernel_launches += 1;
+    g->last.batches += 1;
+    g->last.lanes = KS;
+    return BC_OK;
+}
+
 // One CTA per source (persistent grid), for long-diameter graphs.
 bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStream_t st,
                      std::vector<cudaEvent_t> *ev, bool cap) {
@@ -1481,7 +1572,10 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
     const int sk = g->slices_kernel;
     const bool can_low = maxdeg <= BC_LOWDEG;
     const bool can_sm2 = can_low && sm2_bytes <= (size_t)BC_SLICES_SM2_MAXB;
-    if ((sk == 3 && !can_low) || (sk == 4 && !can_sm2))
+    if ((sk == 5 || sk == 6) && can_low)  // KS sources per CTA in lockstep (slices_multi.cuh)
+        return sk == 5 ? run_slices_multi<4>(g, run, d_src, ns, st, ev, cap, BC_SLICES_ELL && maxdeg <= 4)
+                       : run_slices_multi<8>(g, run, d_src, ns, st, ev, cap, BC_SLICES_ELL && maxdeg <= 4);
+    if ((sk >= 3 && !can_low) || (sk == 4 && !can_sm2))
         return fail(BC_ERR_INVALID, "slices kernel %d needs max degree <= %d%s", sk, BC_LOWDEG,
                     sk == 4 ? " and n <= 1179648" : "");
     const bool lowdeg = sk == 0 ? can_low : (sk == 3 || sk == 4);  // vertex-per-thread pull variant, no fp atomics
@@ -1976,7 +2070,7 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
             g->mode = (int)value;
             return BC_OK;
         case BC_OPT_SLICES_KERNEL:
-            if (value < 0 || value > 4) return fail(BC_ERR_INVALID, "slices kernel must be 0..4");
+            if (value < 0 || value > 6) return fail(BC_ERR_INVALID, "slices kernel must be 0..6");
             g->slices_kernel = (int)value;
             return BC_OK;
         case BC_OPT_DEVICE_LOOP:
