@@ -96,13 +96,20 @@ bc_status bc_prune_degree1(bc_graph *g, int64_t *out_removed);
  *                sources contribute 0.
  *   out_bc       double[n], HOST or DEVICE pointer (detected).  Overwritten,
  *                never accumulated.
- *   cuda_stream  cudaStream_t or NULL (library-internal stream).  With a
- *                DEVICE out_bc the call is stream-ordered and returns once
- *                the work is enqueued... except that the level loop polls a
- *                per-level device flag, so the call returns after the last
- *                backward level is enqueued; out_bc is valid once `stream`
- *                reaches that point.  With a HOST out_bc the call is
- *                synchronous.
+ *   cuda_stream  cudaStream_t or NULL (library-internal stream).  The call is
+ *                stream-ordered on it.  With a DEVICE out_bc and device-driven
+ *                batches (BC_OPT_DEVICE_LOOP, the default when eligible; slices
+ *                mode always) it is also ASYNCHRONOUS: it returns once the work
+ *                is enqueued -- no host wait per level or at the end -- so work
+ *                queued behind it on `cuda_stream` (e.g. an NCCL all-reduce of
+ *                out_bc) sees the result; bc_get_stats waits for the call's
+ *                counters.  It waits before returning when out_bc is a HOST
+ *                pointer, when a capture is pending (bc_set_capture), under
+ *                BC_OPT_PROFILE or BC_TRACE, with the host-driven level loop
+ *                (BC_OPT_DEVICE_LOOP 0 or an ineligible configuration: one host
+ *                wait per BFS level, the paper's nq test PAPER.md:387), and with
+ *                4-byte rows forced or chosen for memory (it must learn whether a
+ *                batch needs the fp64 re-run).
  * Pruned handles: S = {s} stands for s plus its removed degree-1 children
  * (R13), i.e. the result equals the unpruned BC over S+; with
  * S = all it is the exact BC.  A removed source is BC_ERR_INVALID.
@@ -203,10 +210,8 @@ typedef enum {
                                with fp64 atomics); 2 = general with prefix-sum reuse (the forward's CD
                                prefixes kept and reused by the backward); 3 = degree-
                                bounded, thread per frontier vertex, pull, global bitmaps; 4 = the same with
-                               a 2-bit per-vertex state in shared memory (n <= 1179648); 5 / 6 = 4 / 8
-                               sources per CTA swept in lockstep as lanes of one traversal (2-bit depth
-                               code per lane, one union frontier per level).  3-6 need max degree <= 64,
-                               else bc_compute fails with BC_ERR_INVALID */
+                               a 2-bit per-vertex state in shared memory (n <= 1179648).  3/4 need max
+                               degree <= 64, else bc_compute fails with BC_ERR_INVALID */
 } bc_option;
 
 bc_status bc_set_option(bc_graph *g, int option, int64_t value);

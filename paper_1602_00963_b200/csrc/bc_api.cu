@@ -18,7 +18,6 @@
 #include "lanes.cuh"
 #include "graph_kernels.cuh"
 #include "slices.cuh"
-#include "slices_multi.cuh"
 #include "bwd_push.cuh"
 #include "batch_ctl.cuh"
 #include <cub/device/device_radix_sort.cuh>
@@ -261,21 +260,7 @@ struct SlicesWS {
     int4 *ell = nullptr;   // [n] padded neighbours (max degree <= 4)
     int4 *qrow = nullptr;  // [rows][n] neighbour rows in queue order (BC_SM_QROW)
     int *cdq = nullptr;    // [rows][n] the forward's chunk degree prefixes (prefix-sum reuse variant)
-    // slices_multi_kernel (KS sources per CTA)
-    int mrows = 0, mks = 0;
-    uint32_t *mst2 = nullptr;
-    int *mapl = nullptr, *mq = nullptr, *mloff = nullptr;
-    double *msg = nullptr;
-    void release_multi() {
-        dfree(mst2);
-        dfree(mapl);
-        dfree(mq);
-        dfree(mloff);
-        dfree(msg);
-        mrows = mks = 0;
-    }
     void release() {
-        release_multi();
         dfree(cdq);
         dfree(bm);
         dfree(qrow);
@@ -1471,82 +1456,6 @@ bc_status ensure_slices(bc_graph *g, int rows, bool full, bool reuse) {
     return BC_OK;
 }
 
-bc_status ensure_multi(bc_graph *g, int rows, int ks) {
-    SlicesWS &w = g->sws;
-    if (w.mrows >= rows && w.mks == ks) return BC_OK;
-    w.release_multi();
-    const size_t n = (size_t)g->n;
-    CK(dalloc(&w.mst2, n * rows));
-    CK(dalloc(&w.mapl, n * rows));
-    CK(dalloc(&w.mq, n * ks * rows));
-    CK(dalloc(&w.mloff, (n + 2) * rows));
-    CK(dalloc(&w.msg, n * ks * rows));
-    CU(cudaMemset(w.mst2, 0, n * rows * 4));
-    CU(cudaMemset(w.mapl, 0xff, n * rows * 4));
-    CU(cudaDeviceSynchronize());
-    w.mrows = rows;
-    w.mks = ks;
-    return BC_OK;
-}
-
-template <int KS>
-bc_status run_slices_multi(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStream_t st,
-                           std::vector<cudaEvent_t> *ev, bool cap, bool ell) {
-    auto kern = ell ? (cap ? slices_multi_kernel<KS, true, true> : slices_multi_kernel<KS, true>)
-                    : (cap ? slices_multi_kernel<KS, false, true> : slices_multi_kernel<KS, false>);
-    int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BC_SMU_NT, 0);
-    const int groups = (ns + KS - 1) / KS;
-    const int rows = std::max(1, std::min(groups, g->num_sms * std::max(1, occ)));
-    CK(ensure_multi(g, rows, KS));
-    if (ell) {
-        if (!g->sws.ell) CK(dalloc(&g->sws.ell, (size_t)g->n));
-        build_ell4_kernel<<<(unsigned)((g->n + 255) / 256), 256, 0, st>>>((int)g->n, run.rp, run.col, g->sws.ell);
-        g->last.kernel_launches += 1;
-    }
-    SlicesParams p{};
-    p.n = (int)g->n;
-    p.rp = run.rp;
-    p.col = run.col;
-    p.omega = g->pruned ? run.omega : nullptr;
-    p.src = d_src;
-    p.nsrc = ns;
-    p.next_src = g->d_work_ctr + 1;
-    p.bc = g->d_bc;
-    p.ell4 = ell ? g->sws.ell : nullptr;
-    p.stats = g->d_stats;
-    if (cap) {
-        p.cap_vslot = g->capt.d_vslot;
-        p.cap_depth = g->capt.d_depth;
-        p.cap_sigma = g->capt.d_sigma;
-        p.cap_delta = g->capt.d_delta;
-    }
-    MultiParams mp{};
-    mp.st2 = g->sws.mst2;
-    mp.apl = g->sws.mapl;
-    mp.sg = g->sws.msg;
-    mp.q = g->sws.mq;
-    mp.qcap = (long long)g->n * KS;
-    mp.loff = g->sws.mloff;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (ev) {
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        cudaEventRecord(e0, st);
-    }
-    kern<<<rows, BC_SMU_NT, 0, st>>>(p, mp);
-    if (ev) {
-        cudaEventRecord(e1, st);
-        ev->push_back(e0);
-        ev->push_back(e1);
-    }
-    CU(cudaGetLastError());
-    g->last.kernel_launches += 1;
-    g->last.batches += 1;
-    g->last.lanes = KS;
-    return BC_OK;
-}
-
 // One CTA per source (persistent grid), for long-diameter graphs.
 bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStream_t st,
                      std::vector<cudaEvent_t> *ev, bool cap) {
@@ -1572,10 +1481,7 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
     const int sk = g->slices_kernel;
     const bool can_low = maxdeg <= BC_LOWDEG;
     const bool can_sm2 = can_low && sm2_bytes <= (size_t)BC_SLICES_SM2_MAXB;
-    if ((sk == 5 || sk == 6) && can_low)  // KS sources per CTA in lockstep (slices_multi.cuh)
-        return sk == 5 ? run_slices_multi<4>(g, run, d_src, ns, st, ev, cap, BC_SLICES_ELL && maxdeg <= 4)
-                       : run_slices_multi<8>(g, run, d_src, ns, st, ev, cap, BC_SLICES_ELL && maxdeg <= 4);
-    if ((sk >= 3 && !can_low) || (sk == 4 && !can_sm2))
+    if ((sk == 3 && !can_low) || (sk == 4 && !can_sm2))
         return fail(BC_ERR_INVALID, "slices kernel %d needs max degree <= %d%s", sk, BC_LOWDEG,
                     sk == 4 ? " and n <= 1179648" : "");
     const bool lowdeg = sk == 0 ? can_low : (sk == 3 || sk == 4);  // vertex-per-thread pull variant, no fp atomics
@@ -1650,6 +1556,13 @@ bc_status run_slices(bc_graph *g, DevCSR &run, const int *d_src, int ns, cudaStr
     g->last.kernel_launches += lowdeg ? 1 : 2;
     g->last.batches += 1;
     g->last.lanes = 1;
+    return BC_OK;
+}
+
+// Entry points that rebuild or reuse the handle's device state wait for an
+// asynchronous bc_compute still in flight.
+bc_status wait_idle(bc_graph *g) {
+    if (g->stats_ev) CU(cudaEventSynchronize(g->stats_ev));
     return BC_OK;
 }
 
@@ -1971,6 +1884,7 @@ bc_status bc_prune_degree1(bc_graph *g, int64_t *out_removed) {
     if (!g) return fail(BC_ERR_INVALID, "NULL handle");
     if (g->pruned) return fail(BC_ERR_STATE, "graph already pruned (single pass, PAPER.md:580)");
     DeviceGuard dg(g->device);
+    CK(wait_idle(g));
     cudaStream_t st = g->own_stream;
     const int n = (int)g->n;
     CK(dalloc(&g->omega, n));
@@ -2023,6 +1937,7 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
             if (value < 32 || value > (1 << 30)) return fail(BC_ERR_INVALID, "hub degree out of range");
             if (g->hub_deg == (int)value) return BC_OK;
             DeviceGuard dg(g->device);
+            CK(wait_idle(g));
             g->hub_deg = (int)value;
             CK(build_layout(g, g->orig, g->own_stream));
             if (g->pruned) CK(build_layout(g, g->res, g->own_stream));
@@ -2058,6 +1973,7 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
             const int v = (int)value;
             if (v == g->relabel) return BC_OK;
             DeviceGuard dg(g->device);
+            CK(wait_idle(g));
             g->relabel = v;
             CK(build_run(g));
             return BC_OK;
@@ -2070,7 +1986,7 @@ bc_status bc_set_option(bc_graph *g, int option, int64_t value) {
             g->mode = (int)value;
             return BC_OK;
         case BC_OPT_SLICES_KERNEL:
-            if (value < 0 || value > 6) return fail(BC_ERR_INVALID, "slices kernel must be 0..6");
+            if (value < 0 || value > 4) return fail(BC_ERR_INVALID, "slices kernel must be 0..4");
             g->slices_kernel = (int)value;
             return BC_OK;
         case BC_OPT_DEVICE_LOOP:
@@ -2165,6 +2081,12 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     DeviceGuard dg(g->device);
     const int64_t n = g->n;
     DevCSR &csr = g->cur();
+    // an asynchronous previous call (possibly on another stream) still owns
+    // the handle's buffers until its stream reaches stats_ev
+    if (g->stats_ev) {
+        cudaStream_t st0 = cuda_stream ? (cudaStream_t)cuda_stream : g->own_stream;
+        CU(cudaStreamWaitEvent(st0, g->stats_ev, 0));
+    }
     // ---- resolve and validate the source set (host-side argument checks)
     std::vector<int> trav, triv;
     if (!sources) {
@@ -2605,9 +2527,10 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     // enqueued (the counters land in pinned memory; bc_get_stats waits for
     // them).  Otherwise the call has already waited (host-driven level loop,
     // host output, capture, profiling) and completes here.
-    const bool sync = !dev_out || capture || g->profile || trace_on() || !any_dl || mode != 1;
+    const bool device_driven = mode == 2 || any_dl;  // slices mode: one persistent launch, no host round trip
+    const bool sync = !dev_out || capture || g->profile || trace_on() || !device_driven;
+    CU(cudaEventRecord(g->stats_ev, st));
     if (!sync) {
-        CU(cudaEventRecord(g->stats_ev, st));
         g->stats_pending = true;
         return BC_OK;
     }
@@ -2656,6 +2579,7 @@ bc_status bc_sssp(bc_graph *g, int32_t source, int32_t *depth, uint64_t *sigma, 
     if (g->pruned && g->h_removed[source])
         return fail(BC_ERR_INVALID, "source %d was removed by 1-degree pruning", source);
     DeviceGuard dg(g->device);
+    CK(wait_idle(g));
     const int n = (int)g->n;
     cudaStream_t st = g->own_stream;
     bc_stats keep = g->last;

@@ -81,16 +81,16 @@ SUITE = _suite()
 
 
 @pytest.mark.parametrize("mode,words,hub,relabel", [(1, 1, 32, 1), (1, 4, 32, 0), (1, 8, 4096, 2), (1, 2, 64, 1),
-                                                    (2, 0, 4096, 1), (2, 0, 4096, 2), (5, 0, 4096, 2), (6, 0, 4096, 1)])
+                                                    (2, 0, 4096, 1), (2, 0, 4096, 2), (3, 0, 4096, 2), (4, 0, 4096, 1)])
 @pytest.mark.parametrize("prune", [False, True])
 def test_capture_small_suite(mode, words, hub, relabel, prune):
     bcb = _bcb()
     for g in SUITE:
-        if mode >= 5 and g.n and g.degrees.max() > 64:
+        if mode >= 3 and g.n and g.degrees.max() > 64:
             continue
         with bcb.Graph.from_csr(g) as G:
             G.set_option(bcb.OPT_MODE, min(mode, 2))
-            if mode >= 5:  # slices mode, 4 / 8 sources per CTA in lockstep
+            if mode >= 3:  # slices mode, degree-bounded kernel 3 / 4 (global bitmaps / shared state)
                 G.set_option(bcb.OPT_SLICES_KERNEL, mode)
             if words:
                 G.set_option(bcb.OPT_LANE_WORDS, words)

@@ -28,10 +28,15 @@ ap.add_argument("--streams", type=int, default=0)
 ap.add_argument("--two-degree", type=int, default=0)
 ap.add_argument("--sort", default="none", choices=["none", "deg", "degasc"])
 ap.add_argument("--no-profile", action="store_true")
+ap.add_argument("--slices-kernel", type=int, default=0)
+ap.add_argument("--mode", type=int, default=0)
+ap.add_argument("--consecutive", action="store_true", help="the first --sources non-isolated vertices (bench grid steps)")
 ap.add_argument("--all", action="store_true", help="all non-isolated sources")
 a = ap.parse_args()
 g = gg.grid(a.grid, a.grid) if a.grid else gg.rmat(a.scale, a.ef, seed=1)
 S = g.non_isolated() if a.all else gg.sample_sources(g, a.sources, seed=2)
+if a.consecutive:
+    S = g.non_isolated()[:a.sources]
 G = bcb.Graph.from_csr(g)
 if a.prune:
     G.prune_degree1()
@@ -45,6 +50,8 @@ G.set_option(bcb.OPT_BWD_MODE, a.bwd)
 G.set_option(bcb.OPT_SIGMA_WIDTH, a.sigma)
 G.set_option(bcb.OPT_STREAMS, a.streams)
 G.set_option(bcb.OPT_TWO_DEGREE, a.two_degree)
+G.set_option(bcb.OPT_SLICES_KERNEL, a.slices_kernel)
+G.set_option(bcb.OPT_MODE, a.mode)
 if a.sort != "none":
     d = g.degrees[S]
     S = S[np.argsort(-d if a.sort == "deg" else d, kind="stable")]
