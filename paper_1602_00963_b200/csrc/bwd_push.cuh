@@ -64,6 +64,9 @@ __device__ __forceinline__ double rcp_f64(double x) {
 #ifndef BC_PUSH_MINB8
 #define BC_PUSH_MINB8 3  // ... W = 8: 16 coef values per thread
 #endif
+#ifndef BC_PUSH_CFSMEM
+#define BC_PUSH_CFSMEM 0  // backward push: the current slot's coef row staged in shared memory, not in registers
+#endif
 #ifndef BC_PUSH_COMPACT
 #define BC_PUSH_COMPACT 0  // 1: backward push over the slot's compacted lanes (measured slower overall, profiles/exp_r2_push.txt)
 #endif
@@ -76,7 +79,9 @@ struct PushSmem {
     uint64_t u[TV * W];
     alignas(16) uint64_t hc[BC_NW * 32 * W];  // per warp: contributing-lane words of the step's items
     int4 hsv[BC_NW * 32];         // per warp: (slot, y, group mask, -) of the step's items
-    uint16_t lst[BC_NW * 64 * W]; // per warp: the current slot's level-L lanes in lane order (compacted push)
+    static constexpr bool CFS = BC_PUSH_CFSMEM && W <= 4;
+    uint16_t lst[BC_PUSH_COMPACT ? BC_NW * 64 * W : 1]; // per warp: the current slot's level-L lanes in lane order (compacted push)
+    double cfs[CFS ? BC_NW * 64 * W : 1];  // per warp: the current slot's coef row (BC_PUSH_CFSMEM, W <= 4)
     int scan[2 * BC_NW + 2];
     int unit;
 };
@@ -476,6 +481,12 @@ struct PushKernel {
                             for (int j = 0; j < NG; ++j) cf[j] = row[32 * j];
                         } else {
                             slot_coef(hs, !hub_mode && sm.cd[hs] >= ws && sm.cd[hs + 1] <= we, cf);
+                            if constexpr (PushSmem<W>::CFS) {
+                                __syncwarp();  // the previous slot's row is no longer read
+#pragma unroll
+                                for (int j = 0; j < NG; ++j) sm.cfs[wid * K + 32 * j + lane] = cf[j];
+                                __syncwarp();
+                            }
                         }
                     }
                     double *arow = A + (size_t)y * K + lane;
@@ -508,7 +519,8 @@ struct PushKernel {
 #elif defined(BC_EXP_REDZERO)  // experiment: unpredicated red of 0.0 outside c (more L2 sectors, no branches)
                             red_add_f64(arow + 32 * j, (cw >> lane & 1u) ? cf[j] : 0.0);
 #else
-                            red_add_f64_if(arow + 32 * j, cf[j], cw >> lane & 1u);
+                            red_add_f64_if(arow + 32 * j, (!FWD && PushSmem<W>::CFS) ? sm.cfs[wid * K + 32 * j + lane] : cf[j],
+                                           cw >> lane & 1u);
 #endif
                             if (FWD) st_dag += cw >> lane & 1u;
                             if (FWD && lane == (j >> 1)) myword |= (uint64_t)cw << ((j & 1) * 32);

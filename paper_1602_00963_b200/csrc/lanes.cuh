@@ -114,6 +114,9 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // order earlier generic-proxy accesses of shared memory before later async-proxy (bulk copy) writes
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+#ifndef BC_FWD_HIT2
+#define BC_FWD_HIT2 1  // 16-bit forward: two hits per iteration, the second hit's row loads issued before the first is added
+#endif
 #ifndef BC_FWD_BULK
 #define BC_FWD_BULK 0  // 1: 16-bit forward hit rows gathered by bulk copies into a per-warp shared ring (slower: profiles/exp_r2_fwd_bulk.txt)
 #endif
@@ -639,6 +642,65 @@ struct LanesKernel {
                         ++ring_used;
                         __syncwarp();
                         if (hi) issue();
+                    }
+                    __syncwarp();
+                    continue;
+                }
+                if constexpr (NARROW && BC_FWD_HIT2 && !BWD) {
+                    // 16-bit forward, two hits per iteration: both hits' row
+                    // words are loaded before either is added (and before a
+                    // slot flush), so a warp has two rows' latency in flight
+                    // instead of one (the level kernel stalled on the first
+                    // use of each gathered word, profiles/ncu_r2_s20_level.txt)
+                    while (hm) {
+                        const int src = __ffs(hm) - 1;
+                        hm &= hm - 1;
+                        const int src2 = hm ? __ffs(hm) - 1 : -1;  // uniform
+                        if (src2 >= 0) hm &= hm - 1;
+                        const int2 sv = sm.hsv[wid * 32 + src];
+                        uint32_t cw[W], t[W], t2[W];
+                        load_halves<W>(hcw + src * 2 * W, cw);
+                        const uint32_t *roww = reinterpret_cast<const uint32_t *>(Scur() + (size_t)sv.y * K) + lane;
+#pragma unroll
+                        for (int pr = 0; pr < W; ++pr) t[pr] = (cw[pr] & (3u << sh)) ? __ldg(roww + 32 * pr) : 0u;
+                        int2 sv2 = make_int2(-1, 0);
+                        if (src2 >= 0) {
+                            sv2 = sm.hsv[wid * 32 + src2];
+                            load_halves<W>(hcw + src2 * 2 * W, cw);
+                            const uint32_t *roww2 = reinterpret_cast<const uint32_t *>(Scur() + (size_t)sv2.y * K) + lane;
+#pragma unroll
+                            for (int pr = 0; pr < W; ++pr) t2[pr] = (cw[pr] & (3u << sh)) ? __ldg(roww2 + 32 * pr) : 0u;
+                        }
+                        if (sv.x != cur) {
+                            while (cur < sv.x) {
+                                flush(cur, first, ws, we, hub_mode, acc, aovf);
+                                ++cur;
+#pragma unroll
+                                for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
+                                aovf = 0;
+                            }
+                        }
+#pragma unroll
+                        for (int pr = 0; pr < W; ++pr) {
+                            acc[2 * pr] += t[pr] & 0xffffu;
+                            acc[2 * pr + 1] += t[pr] >> 16;
+                        }
+                        if (src2 >= 0) {
+                            if (sv2.x != cur) {
+                                while (cur < sv2.x) {
+                                    flush(cur, first, ws, we, hub_mode, acc, aovf);
+                                    ++cur;
+#pragma unroll
+                                    for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
+                                    aovf = 0;
+                                }
+                            }
+#pragma unroll
+                            for (int pr = 0; pr < W; ++pr) {
+                                acc[2 * pr] += t2[pr] & 0xffffu;
+                                acc[2 * pr + 1] += t2[pr] >> 16;
+                            }
+                        }
                     }
                     __syncwarp();
                     continue;
