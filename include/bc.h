@@ -240,9 +240,11 @@ typedef struct {
     double bwd_fin_ms;       /* backward finalize kernels (BC_OPT_PROFILE)       */
     double bwd_push_ms;      /* backward push kernels (BC_OPT_PROFILE)           */
     int64_t narrow_batches;  /* batches completed with 16-bit sigma rows          */
-    int64_t narrow_fallbacks;/* batches re-run with wider rows after a sigma > 65535 */
+    int64_t narrow_fallbacks;/* batches re-run whole with wider rows after a sigma > 65535 */
     int64_t mid_batches;     /* ... of which completed with 32-bit rows (the rest: fp64) */
     int64_t derived_lanes;   /* 2-degree sources whose tree was derived (BC_OPT_TWO_DEGREE) */
+    int64_t widened_batches; /* host-driven 16-bit batches that switched to 32-bit rows at the level whose
+                                sigma exceeded 65535 (only that level re-expanded, no batch re-run) */
 } bc_stats;
 
 bc_status bc_get_stats(const bc_graph *g, bc_stats *out);

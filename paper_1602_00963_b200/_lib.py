@@ -62,7 +62,7 @@ class bc_stats(ctypes.Structure):
         ("fwd_items", ctypes.c_int64), ("fwd_hits", ctypes.c_int64), ("bwd_items", ctypes.c_int64),
         ("bwd_hits", ctypes.c_int64), ("bwd_fin_ms", ctypes.c_double), ("bwd_push_ms", ctypes.c_double),
         ("narrow_batches", ctypes.c_int64), ("narrow_fallbacks", ctypes.c_int64), ("mid_batches", ctypes.c_int64),
-        ("derived_lanes", ctypes.c_int64),
+        ("derived_lanes", ctypes.c_int64), ("widened_batches", ctypes.c_int64),
     ]
 
     def as_dict(self):

@@ -142,6 +142,8 @@ struct LaneWS {
     double *lane_ns = nullptr;
     void *part = nullptr;  // split-slot partial sums [max CTAs][BC_NW][2][K]
     double *A = nullptr;   // push-backward accumulators [n][K], zero between batches
+    unsigned long long *lvl_snap = nullptr;  // [3][8] counters before each of the last 3 forward levels (widening)
+    double *ns_snap = nullptr;               // [3][K] n_s accumulators likewise
     int *lane_cap = nullptr;       // [K] capture slot of each lane or -1 (bc_set_capture)
     uint64_t *capmask = nullptr;   // [8] lanes of the batch that are captured
     uint64_t **d_lv = nullptr;  // device copies of the level mask / row pointers (2-degree derive)
@@ -155,6 +157,8 @@ struct LaneWS {
         dfree(A);
         dfree(lane_cap);
         dfree(capmask);
+        dfree(lvl_snap);
+        dfree(ns_snap);
         for (auto &q : slev) dfree(q);
         slev.clear();
         dfree(seen);
@@ -180,6 +184,20 @@ constexpr int TILE_ITEMS = 8192; // non-hub adjacency items per level-kernel til
 #define BC_TILE_PER_SM 1         // tiles are halved until a level's adjacency makes this many per SM
 #endif
 constexpr int MAX_STREAMS = 8;   // concurrent batch pipelines (BC_OPT_STREAMS)
+// level (forward) and push (backward) kernel grids = resident CTAs x NUM / DEN:
+// below 1 they leave room on every SM for a concurrent pipeline's kernel
+#ifndef BC_FGRID_NUM
+#define BC_FGRID_NUM 3
+#endif
+#ifndef BC_FGRID_DEN
+#define BC_FGRID_DEN 4
+#endif
+#ifndef BC_PGRID_NUM
+#define BC_PGRID_NUM 3
+#endif
+#ifndef BC_PGRID_DEN
+#define BC_PGRID_DEN 4
+#endif
 #ifndef BC_DEVLOOP_MAX_LEVELS
 #define BC_DEVLOOP_MAX_LEVELS 32  // device-driven batches only for graphs whose depth bound is at most this
 #endif
@@ -773,6 +791,8 @@ bc_status ensure_ws(bc_graph *g, LaneWS &ws, int W, bool verify, int nhub, int r
         CK(dalloc(&ws.lane_ns, K));
         CK(dalloc(&ws.lane_cap, K));
         CK(dalloc(&ws.capmask, 8));
+        CK(dalloc(&ws.lvl_snap, 24));
+        CK(dalloc(&ws.ns_snap, 3 * (size_t)K));
         CK(dalloc((double **)&ws.part, (size_t)g->num_sms * 8 * BC_NW * 2 * K));
         if (!verify) {
             CK(dalloc(&ws.A, n * K));
@@ -832,6 +852,21 @@ bc_status ensure_level(bc_graph *g, LaneWS &ws, int L) {
     return BC_OK;
 }
 
+// Widening a 16-bit forward at level Lo (bc_api.cu run_batch): the
+// discarded expansions wrote levels Lo+1 and Lo+2 -- their lanes leave the
+// seen set and their masks are cleared.
+__global__ void unsee_levels_kernel(uint64_t *seen, uint64_t *a, uint64_t *b, size_t cnt) {
+    const size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x, step = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = i0; i < cnt; i += step) {
+        const uint64_t m = a[i] | b[i];
+        if (m) {
+            seen[i] &= ~m;
+            a[i] = 0;
+            b[i] = 0;
+        }
+    }
+}
+
 // per lane: 1 + omega(source) and, with a capture active, the capture slot
 // of the lane's source (capmask pre-zeroed)
 __global__ void lane_setup_kernel(const int *src, int nl, int K, const uint32_t *omega, double *w1,
@@ -855,7 +890,7 @@ int level_grid(bc_graph *g, F kern, int units, size_t smem) {
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BC_NT, smem);
     if (occ < 1) occ = 1;
-    int grid = g->num_sms * occ;
+    int grid = g->num_sms * occ * BC_FGRID_NUM / BC_FGRID_DEN;
     return std::max(1, std::min(grid, units));
 }
 
@@ -876,6 +911,8 @@ struct BatchCtx {
     std::vector<uint64_t *> *lvl_out;  // verification: level masks used (nullable)
     int *levels_out;
     bool *narrow_failed;    // narrow forward: set when some sigma > 65535 (nothing committed)
+    bool *need_fp64;        // ... and set when it had widened to 32-bit rows and sigma >= 2^32 (skip the 32-bit re-run)
+    bool *widened;          // set when the forward widened to 32-bit rows at some level (no re-run)
     bool layout;            // 2-degree layout: lanes with src < 0 are unused, derived lanes below
     uint64_t active[8];     // ... lanes traversed by the forward (layout only)
     uint64_t derived[8];    // ... 2-degree lanes (tree derived after the forward)
@@ -957,6 +994,24 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
     }
     const int hub_grid = (c.csr->nhub * 32 + BC_NT - 1) / BC_NT;
 
+    // Widening (16-bit tier only): when expansion Lo overflows 16 bits, that
+    // one expansion is redone with 32-bit output rows and the batch goes on
+    // with 32-bit rows -- levels <= Lo keep their 16-bit rows -- instead of
+    // re-running the whole batch.  Counters and n_s are snapshotted before
+    // every expansion so the discarded ones can be undone.
+    constexpr bool CAN_WIDEN_T = std::is_same<SigT, unsigned>::value;
+    const bool can_widen = CAN_WIDEN_T && !any_derived && c.widened != nullptr;
+    int wide_from = -1;  // first expansion that writes 32-bit rows
+    auto kf_mix = lanes_level_kernel<W, long long, false, true>;  // 16-bit rows in, 32-bit out
+    auto kf_32 = lanes_level_kernel<W, long long>;
+    constexpr size_t SMEM32 = sizeof(LanesSmem<W, long long>);
+    int grid_mix = grid, grid_32 = grid;
+    if (can_widen) {
+        grid_mix = level_grid(g, kf_mix, units, SMEM32);
+        grid_32 = level_grid(g, kf_32, units, SMEM32);
+        cudaFuncSetAttribute(lanes_hub_finalize<W, long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)SMEM32);
+    }
     int L = 1, Lmax = 0;
     bool narrow_bad = false;
     for (;;) {
@@ -964,6 +1019,13 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
         CK(ensure_flags(g, x, L + 2));
         CU(cudaMemsetAsync(level_ptr(g, ws, L + 1), 0, mbytes, st));
         CU(cudaMemsetAsync(x.d_flags + L + 1, 0, sizeof(int), st));
+        if (can_widen && wide_from < 0) {
+            CU(cudaMemcpyAsync(ws.lvl_snap + 8 * (L % 3), x.d_stats, 8 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToDevice, st));
+            if (p.lane_ns)
+                CU(cudaMemcpyAsync(ws.ns_snap + (size_t)K * (L % 3), p.lane_ns, (size_t)K * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, st));
+        }
         p.level = L;
         p.S_cur = ws.slev[L];
         p.S_nxt = ws.slev[L + 1];
@@ -985,7 +1047,7 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
                 auto kpf = lanes_push_kernel<W, true>;
                 int occp = 1;
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occp, kpf, BC_NT, 0);
-                const int gridp = std::max(1, std::min(g->num_sms * std::max(1, occp), units));
+                const int gridp = std::max(1, std::min(g->num_sms * std::max(1, occp) * BC_PGRID_NUM / BC_PGRID_DEN, units));
                 kpf<<<gridp, BC_NT, 0, st>>>(p, ws.A);
                 const unsigned cb = (unsigned)std::min<int64_t>(((int64_t)n * 32 + BC_NT - 1) / BC_NT,
                                                                 (int64_t)g->num_sms * 8);
@@ -994,8 +1056,14 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
             }
         }
         if (!pushed) {
-            kf<<<grid, BC_NT, SMEM, st>>>(p);
-            if (p.nhub > 0) lanes_hub_finalize<W, SigT><<<hub_grid, BC_NT, SMEM, st>>>(p);
+            if (wide_from < 0 || L < wide_from) {
+                kf<<<grid, BC_NT, SMEM, st>>>(p);
+                if (p.nhub > 0) lanes_hub_finalize<W, SigT><<<hub_grid, BC_NT, SMEM, st>>>(p);
+            } else {
+                if (L == wide_from) kf_mix<<<grid_mix, BC_NT, SMEM32, st>>>(p);
+                else kf_32<<<grid_32, BC_NT, SMEM32, st>>>(p);
+                if (p.nhub > 0) lanes_hub_finalize<W, long long><<<hub_grid, BC_NT, SMEM32, st>>>(p);
+            }
         }
         if (ev_f) {
             cudaEventRecord(e1, st);
@@ -1021,7 +1089,32 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
                 x.sync_us += now_us() - t0;
                 x.syncs += 1;
             }
-            if (NARROW && hp[1]) narrow_bad = true;  // sigma overflowed 16 bits: the batch is re-run in fp64
+            if (NARROW && hp[1]) {
+                if (can_widen && wide_from < 0) {
+                    // expansion Lo = L-1 wrote a sigma > 65535: undo it and the
+                    // speculative expansion L, then redo Lo with 32-bit rows
+                    const int Lo = L - 1;
+                    CU(cudaStreamSynchronize(st));
+                    const unsigned ub = (unsigned)std::min<size_t>((n * (size_t)W + 255) / 256, (size_t)g->num_sms * 8);
+                    unsee_levels_kernel<<<ub, 256, 0, st>>>(ws.seen, level_ptr(g, ws, Lo + 1), level_ptr(g, ws, Lo + 2),
+                                                            (size_t)n * W);
+                    CU(cudaMemcpyAsync(x.d_stats, ws.lvl_snap + 8 * (Lo % 3), 8 * sizeof(unsigned long long),
+                                       cudaMemcpyDeviceToDevice, st));
+                    if (p.lane_ns)
+                        CU(cudaMemcpyAsync(p.lane_ns, ws.ns_snap + (size_t)K * (Lo % 3), (size_t)K * sizeof(double),
+                                           cudaMemcpyDeviceToDevice, st));
+                    CU(cudaMemsetAsync(p.narrow_ovf, 0, sizeof(int), st));
+                    CU(cudaGetLastError());
+                    x.last.kernel_launches += 1;
+                    x.last.fwd_launches -= 2;  // the two discarded expansions
+                    wide_from = Lo;
+                    *c.widened = true;
+                    L = Lo;
+                    continue;
+                }
+                narrow_bad = true;  // sigma overflowed: the batch is re-run wider
+                if (wide_from >= 0 && c.need_fp64) *c.need_fp64 = true;  // 32-bit rows overflowed too
+            }
             if (narrow_bad || hp[0] == 0) {
                 Lmax = L - 1;
                 x.last.fwd_launches -= 1;  // the no-op launch
@@ -1077,10 +1170,16 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
         // verification capture: depth and sigma of the captured lanes, from
         // the level masks and sigma rows of this (completed) forward
         const unsigned vb = (unsigned)(((int64_t)n + 255) / 256);
-        for (int l = 0; l <= Lb; ++l)
-            cap_extract_kernel<W, RT><<<vb, 256, 0, st>>>(n, l, level_ptr(g, ws, l), (const RT *)ws.slev[l], ws.lane_cap,
-                                                          ws.capmask, c.cap_depth, c.cap_sigma);
-        cap_tier_kernel<<<(K + 255) / 256, 256, 0, st>>>(K, ws.lane_cap, 8 * (int)sizeof(RT), c.cap_tier);
+        for (int l = 0; l <= Lb; ++l) {
+            if (wide_from >= 0 && l > wide_from)  // widened batch: 32-bit rows past the widening level
+                cap_extract_kernel<W, uint32_t><<<vb, 256, 0, st>>>(n, l, level_ptr(g, ws, l), (const uint32_t *)ws.slev[l],
+                                                                    ws.lane_cap, ws.capmask, c.cap_depth, c.cap_sigma);
+            else
+                cap_extract_kernel<W, RT><<<vb, 256, 0, st>>>(n, l, level_ptr(g, ws, l), (const RT *)ws.slev[l],
+                                                              ws.lane_cap, ws.capmask, c.cap_depth, c.cap_sigma);
+        }
+        cap_tier_kernel<<<(K + 255) / 256, 256, 0, st>>>(K, ws.lane_cap, wide_from >= 0 ? 32 : 8 * (int)sizeof(RT),
+                                                         c.cap_tier);
         CU(cudaGetLastError());
     }
     if constexpr (!std::is_same<SigT, unsigned long long>::value) {
@@ -1129,10 +1228,12 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
             // pushes it into the parents' accumulators; hubs are finalised by a
             // warp-per-hub kernel after it, level 1 by the finalize scan
             auto kpush = lanes_push_kernel<W, false, RT>;
+            auto kpush32 = lanes_push_kernel<W, false, uint32_t>;  // levels past a widening (32-bit rows)
             cudaFuncSetAttribute(kpush, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            if (wide_from >= 0) cudaFuncSetAttribute(kpush32, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
             int occp = 1;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occp, kpush, BC_NT, 0);
-            const int gridp = std::max(1, std::min(g->num_sms * std::max(1, occp), units));
+            const int gridp = std::max(1, std::min(g->num_sms * std::max(1, occp) * BC_PGRID_NUM / BC_PGRID_DEN, units));
             const unsigned fin_blocks = (unsigned)std::min<int64_t>(((int64_t)n * 32 + BC_NT - 1) / BC_NT,
                                                                     (int64_t)g->num_sms * 8);
             p.lane_cap = c.cap_vslot ? ws.lane_cap : nullptr;
@@ -1153,7 +1254,11 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
                     cudaEventCreate(&e3);
                     cudaEventRecord(e0, st);
                 }
-                if (l >= 2) kpush<<<gridp, BC_NT, 0, st>>>(p, ws.A);
+                const bool w32 = wide_from >= 0 && l > wide_from;
+                if (l >= 2) {
+                    if (w32) kpush32<<<gridp, BC_NT, 0, st>>>(p, ws.A);
+                    else kpush<<<gridp, BC_NT, 0, st>>>(p, ws.A);
+                }
                 if (ev_b) {
                     cudaEventRecord(e1, st);
                     cudaEventRecord(e2, st);
@@ -1163,7 +1268,10 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
                     lanes_bwd_finalize_kernel<W, false, RT><<<fin_blocks, BC_NT, 0, st>>>(p, ws.A);
                     ++nk;
                 } else if (p.nhub > 0) {
-                    lanes_bwd_hub_fin_kernel<W, RT><<<(p.nhub * 32 + BC_NT - 1) / BC_NT, BC_NT, 0, st>>>(p, ws.A);
+                    if (w32)
+                        lanes_bwd_hub_fin_kernel<W, uint32_t><<<(p.nhub * 32 + BC_NT - 1) / BC_NT, BC_NT, 0, st>>>(p, ws.A);
+                    else
+                        lanes_bwd_hub_fin_kernel<W, RT><<<(p.nhub * 32 + BC_NT - 1) / BC_NT, BC_NT, 0, st>>>(p, ws.A);
                     ++nk;
                 }
                 if (ev_b) {
@@ -1306,7 +1414,7 @@ void enqueue_tier(bc_graph *g, LaneCtx &x, const DevBatchCfg &cfg, const int *ne
     cudaFuncSetAttribute(kpush, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int occp = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occp, kpush, BC_NT, 0);
-    const int gridp = std::max(1, std::min(g->num_sms * std::max(1, occp), units));
+    const int gridp = std::max(1, std::min(g->num_sms * std::max(1, occp) * BC_PGRID_NUM / BC_PGRID_DEN, units));
     const unsigned fin_blocks = (unsigned)std::min<int64_t>(((int64_t)n * 32 + BC_NT - 1) / BC_NT, (int64_t)g->num_sms * 8);
     for (int l = cfg.lcap; l >= 1; --l) {
         p.level = l;
@@ -2432,15 +2540,22 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
                     auto *pef = g->profile ? &x.ef : nullptr;
                     auto *peb = g->profile ? &x.eb : nullptr;
                     if (narrow) {
-                        // 16-bit rows, then 32-bit rows, then fp64
-                        bool failed = false;
+                        // 16-bit rows (widened in place to 32-bit rows at the
+                        // level that overflows), else the whole batch again with
+                        // 32-bit rows, then fp64
+                        bool failed = false, widened = false, need64 = false;
                         c.narrow_failed = &failed;
+                        c.widened = &widened;
+                        c.need_fp64 = &need64;
                         const int64_t lv = x.last.levels_total;
                         CU(cudaMemcpyAsync(x.d_stats + 8, x.d_stats, 8 * sizeof(unsigned long long),
                                            cudaMemcpyDeviceToDevice, xs));
                         CK(run_batch_w<unsigned>(g, x, W, c, pef, peb));
+                        c.widened = nullptr;
+                        c.need_fp64 = nullptr;
                         if (!failed) {
-                            x.last.narrow_batches += 1;
+                            if (widened) x.last.widened_batches += 1;
+                            else x.last.narrow_batches += 1;
                             continue;
                         }
                         CU(cudaMemcpyAsync(x.d_stats, x.d_stats + 8, 8 * sizeof(unsigned long long),
@@ -2448,10 +2563,12 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
                         x.last.levels_total = lv;
                         x.last.narrow_fallbacks += 1;
                         failed = false;
-                        CK(run_batch_w<long long>(g, x, W, c, pef, peb));
-                        if (!failed) {
-                            x.last.mid_batches += 1;
-                            continue;
+                        if (!need64) {
+                            CK(run_batch_w<long long>(g, x, W, c, pef, peb));
+                            if (!failed) {
+                                x.last.mid_batches += 1;
+                                continue;
+                            }
                         }
                         CU(cudaMemcpyAsync(x.d_stats, x.d_stats + 8, 8 * sizeof(unsigned long long),
                                            cudaMemcpyDeviceToDevice, xs));
@@ -2501,6 +2618,7 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
             g->last.narrow_batches += x.last.narrow_batches;
             g->last.narrow_fallbacks += x.last.narrow_fallbacks;
             g->last.mid_batches += x.last.mid_batches;
+            g->last.widened_batches += x.last.widened_batches;
         }
     }
     if (!triv.empty()) {

@@ -315,7 +315,10 @@ __device__ __forceinline__ uint64_t gather_words(uint32_t bits, int lane) {
     return mine;
 }
 
-template <int W, typename SigT, bool BWD = false>
+// IN16: the level-L rows read by the forward hold 16-bit sigma -- the narrow
+// tier (SigT = unsigned), or the level at which a batch widens to 32-bit rows
+// (SigT = long long, the "widening" instantiation: 16-bit rows in, 32-bit out)
+template <int W, typename SigT, bool BWD = false, bool IN16 = std::is_same<SigT, unsigned>::value>
 struct LanesKernel {
     static constexpr int K = 64 * W;
     static constexpr int LPT = 2 * W;           // lanes per thread
@@ -646,7 +649,7 @@ struct LanesKernel {
                     __syncwarp();
                     continue;
                 }
-                if constexpr (NARROW && BC_FWD_HIT2 && !BWD) {
+                if constexpr (IN16 && BC_FWD_HIT2 && !BWD) {
                     // 16-bit forward, two hits per iteration: both hits' row
                     // words are loaded before either is added (and before a
                     // slot flush), so a warp has two rows' latency in flight
@@ -660,14 +663,14 @@ struct LanesKernel {
                         const int2 sv = sm.hsv[wid * 32 + src];
                         uint32_t cw[W], t[W], t2[W];
                         load_halves<W>(hcw + src * 2 * W, cw);
-                        const uint32_t *roww = reinterpret_cast<const uint32_t *>(Scur() + (size_t)sv.y * K) + lane;
+                        const uint32_t *roww = reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint16_t *>(p.S_cur) + (size_t)sv.y * K) + lane;
 #pragma unroll
                         for (int pr = 0; pr < W; ++pr) t[pr] = (cw[pr] & (3u << sh)) ? __ldg(roww + 32 * pr) : 0u;
                         int2 sv2 = make_int2(-1, 0);
                         if (src2 >= 0) {
                             sv2 = sm.hsv[wid * 32 + src2];
                             load_halves<W>(hcw + src2 * 2 * W, cw);
-                            const uint32_t *roww2 = reinterpret_cast<const uint32_t *>(Scur() + (size_t)sv2.y * K) + lane;
+                            const uint32_t *roww2 = reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint16_t *>(p.S_cur) + (size_t)sv2.y * K) + lane;
 #pragma unroll
                             for (int pr = 0; pr < W; ++pr) t2[pr] = (cw[pr] & (3u << sh)) ? __ldg(roww2 + 32 * pr) : 0u;
                         }
@@ -722,9 +725,9 @@ struct LanesKernel {
                     }
                     // rows are zero outside their level: add whole pairs
                     // (lanes outside c only collect values the commit discards)
-                    if constexpr (NARROW) {
+                    if constexpr (IN16) {
                         // 16-bit rows: one 32-bit load per pair (lanes 2t, 2t+1)
-                        const uint32_t *roww = reinterpret_cast<const uint32_t *>(Scur() + (size_t)sv.y * K) + lane;
+                        const uint32_t *roww = reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint16_t *>(p.S_cur) + (size_t)sv.y * K) + lane;
 #pragma unroll
                         for (int pr = 0; pr < W; ++pr) {
                             if (cw[pr] & (3u << sh)) {
@@ -963,13 +966,13 @@ struct LanesKernel {
 #define BC_MINB8 3  // ... and at W = 8 (16 lanes per thread)
 #endif
 
-template <int W, typename SigT, bool BWD = false>
+template <int W, typename SigT, bool BWD = false, bool IN16 = std::is_same<SigT, unsigned>::value>
 __global__ void __launch_bounds__(BC_NT, (W == 8 ? BC_MINB8 : (W == 4 ? BC_MINB4 : BC_MINB))) lanes_level_kernel(LanesParams p) {
     extern __shared__ __align__(16) unsigned char smraw[];
     if (p.prev_new && *p.prev_new == 0) return;  // speculative launch past the last level
     if (gated_off(p)) return;                     // device-driven batch: tier not in use
     LanesSmem<W, SigT> &sm = *reinterpret_cast<LanesSmem<W, SigT> *>(smraw);
-    LanesKernel<W, SigT, BWD> k(p, sm);
+    LanesKernel<W, SigT, BWD, IN16> k(p, sm);
     const int total = p.nseg + p.ntiles;
     for (;;) {
         if (threadIdx.x == 0) {

@@ -88,7 +88,9 @@ def test_config5_rmat23_bench_step_with_32bit_tier():
         got, depth, sigma, delta, tier = G.compute_captured(S, caps)
         st = G.stats()
     assert st["num_sources"] == 2048
-    assert st["narrow_fallbacks"] >= 1 and st["mid_batches"] >= 1, st
+    # host-driven at this size: a batch whose sigma passes 16 bits widens to
+    # 32-bit rows at that level (no batch re-run)
+    assert st["widened_batches"] + st["mid_batches"] >= 1, st
     assert 32 in set(tier.tolist()), tier
     inv = _total_invariant(st)
     assert abs(got.sum() - inv) <= 1e-9 * inv

@@ -587,3 +587,38 @@ def test_slices_kernel_variants(kernel):
                         G.compute()
                     continue
                 assert_bc_close(G.compute(), oracle.bc(g))
+
+
+@pytest.mark.parametrize("layers", [8, 12])
+def test_host_loop_widens_sigma_rows_in_place(layers):
+    """Host-driven level loop: a 16-bit batch whose sigma passes 65535 at
+    some level widens to 32-bit rows from that level on (only that level is
+    re-expanded; no batch re-run); past 2^32 (layers = 12) it goes to the
+    fp64 re-run directly.  BC, counters and the captured sigma of widened
+    lanes match the oracle."""
+    from test_gpu_capture import assert_capture_matches
+
+    bcb = _bcb()
+    g = gg.disjoint_union(layered(10, layers), gg.rmat(9, 8, seed=3))
+    want, stats = oracle.bc(g, stats=True)
+    S = g.non_isolated()
+    caps = [0, 5, int(S[-1])]
+    with bcb.Graph.from_csr(g) as G:
+        G.set_option(bcb.OPT_MODE, 1)
+        G.set_option(bcb.OPT_LANE_WORDS, 1)
+        G.set_option(bcb.OPT_SOURCE_ORDER, 0)
+        G.set_option(bcb.OPT_DEVICE_LOOP, 0)
+        got, depth, sigma, delta, tier = G.compute_captured(S, caps)
+        st = G.stats()
+    assert_bc_close(got, want)
+    assert st["reached"] == int(stats[S, 0].sum())
+    assert st["adj_reached"] == int(stats[S, 1].sum())
+    assert st["dag_edges"] == int(stats[S, 2].sum())
+    assert_capture_matches(g, caps, depth, sigma, delta)
+    assert st["narrow_batches"] + st["widened_batches"] + st["narrow_fallbacks"] == st["batches"]
+    if layers == 8:
+        assert st["widened_batches"] >= 1 and st["narrow_fallbacks"] == 0, st
+        assert 32 in set(tier.tolist())
+    else:
+        assert st["narrow_fallbacks"] >= 1 and st["mid_batches"] == 0, st
+        assert 64 in set(tier.tolist())
