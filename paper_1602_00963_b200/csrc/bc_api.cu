@@ -184,8 +184,10 @@ constexpr int TILE_ITEMS = 8192; // non-hub adjacency items per level-kernel til
 #define BC_TILE_PER_SM 1         // tiles are halved until a level's adjacency makes this many per SM
 #endif
 constexpr int MAX_STREAMS = 8;   // concurrent batch pipelines (BC_OPT_STREAMS)
-// level (forward) and push (backward) kernel grids = resident CTAs x NUM / DEN:
-// below 1 they leave room on every SM for a concurrent pipeline's kernel
+// level (forward) and push (backward) kernel grids = resident CTAs x NUM / DEN
+// when several batch pipelines run concurrently: the gaps let a pipeline's
+// forward and another's backward share the SMs (S20, 3 pipelines: 307.5 ->
+// 302-304 ms per 8192 sources, profiles/exp_r2_gridfrac.txt)
 #ifndef BC_FGRID_NUM
 #define BC_FGRID_NUM 3
 #endif
@@ -329,6 +331,7 @@ struct bc_graph {
     std::vector<int> td_lanes;
     int depth_bound = -1;      // every BFS depth of the graph is <= this (bc_graph_create); -1 unknown
     int slices_kernel = 0;     // BC_OPT_SLICES_KERNEL: 0 auto, 1 general, 2 general + prefix reuse, 3/4 degree-bounded
+    bool conc = false;         // the current call runs several batch pipelines (kernel grid fraction)
     int device_loop = 1;       // BC_OPT_DEVICE_LOOP: device-driven batches (CUDA graph per pipeline) when eligible
     struct Sizing {            // last call's lane width / row width / pipelines (skips cudaMemGetInfo when unchanged)
         int64_t key[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
@@ -890,7 +893,7 @@ int level_grid(bc_graph *g, F kern, int units, size_t smem) {
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BC_NT, smem);
     if (occ < 1) occ = 1;
-    int grid = g->num_sms * occ * BC_FGRID_NUM / BC_FGRID_DEN;
+    int grid = g->conc ? g->num_sms * occ * BC_FGRID_NUM / BC_FGRID_DEN : g->num_sms * occ;
     return std::max(1, std::min(grid, units));
 }
 
@@ -1047,7 +1050,8 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
                 auto kpf = lanes_push_kernel<W, true>;
                 int occp = 1;
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occp, kpf, BC_NT, 0);
-                const int gridp = std::max(1, std::min(g->num_sms * std::max(1, occp) * BC_PGRID_NUM / BC_PGRID_DEN, units));
+                const int gridp = std::max(1, std::min(g->conc ? g->num_sms * std::max(1, occp) * BC_PGRID_NUM / BC_PGRID_DEN
+                                                          : g->num_sms * std::max(1, occp), units));
                 kpf<<<gridp, BC_NT, 0, st>>>(p, ws.A);
                 const unsigned cb = (unsigned)std::min<int64_t>(((int64_t)n * 32 + BC_NT - 1) / BC_NT,
                                                                 (int64_t)g->num_sms * 8);
@@ -1233,7 +1237,8 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
             if (wide_from >= 0) cudaFuncSetAttribute(kpush32, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
             int occp = 1;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occp, kpush, BC_NT, 0);
-            const int gridp = std::max(1, std::min(g->num_sms * std::max(1, occp) * BC_PGRID_NUM / BC_PGRID_DEN, units));
+            const int gridp = std::max(1, std::min(g->conc ? g->num_sms * std::max(1, occp) * BC_PGRID_NUM / BC_PGRID_DEN
+                                                          : g->num_sms * std::max(1, occp), units));
             const unsigned fin_blocks = (unsigned)std::min<int64_t>(((int64_t)n * 32 + BC_NT - 1) / BC_NT,
                                                                     (int64_t)g->num_sms * 8);
             p.lane_cap = c.cap_vslot ? ws.lane_cap : nullptr;
@@ -1414,7 +1419,8 @@ void enqueue_tier(bc_graph *g, LaneCtx &x, const DevBatchCfg &cfg, const int *ne
     cudaFuncSetAttribute(kpush, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int occp = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occp, kpush, BC_NT, 0);
-    const int gridp = std::max(1, std::min(g->num_sms * std::max(1, occp) * BC_PGRID_NUM / BC_PGRID_DEN, units));
+    const int gridp = std::max(1, std::min(g->conc ? g->num_sms * std::max(1, occp) * BC_PGRID_NUM / BC_PGRID_DEN
+                                                          : g->num_sms * std::max(1, occp), units));
     const unsigned fin_blocks = (unsigned)std::min<int64_t>(((int64_t)n * 32 + BC_NT - 1) / BC_NT, (int64_t)g->num_sms * 8);
     for (int l = cfg.lcap; l >= 1; --l) {
         p.level = l;
@@ -1473,6 +1479,7 @@ bc_status device_batch_graph(bc_graph *g, LaneCtx &x, int W, const DevBatchCfg &
                                   (uintptr_t)cfg.csr->tile_vs,
                                   (uintptr_t)cfg.csr->hub_ids,
                                   (uintptr_t)g->hub_deg,
+                                  (uintptr_t)g->conc,
                                   (uintptr_t)x.ws.seen,
                                   (uintptr_t)x.ws.A,
                                   (uintptr_t)x.ws.hub_acc,
@@ -2384,6 +2391,7 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
         // ---- device-driven batches: one CUDA graph launch per batch, no host
         // round trip inside a batch (enqueue_device_batch)
         NS = std::max(1, std::min(NS, (int)plan.size()));
+        g->conc = NS > 1;
         cudaEvent_t start = nullptr;
         CU(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
         CU(cudaEventRecord(start, st));
@@ -2479,6 +2487,7 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
         }
     } else if (mode == 1 && !trav.empty()) {
         NS = std::max(1, std::min(NS, (int)plan.size()));
+        g->conc = NS > 1;
         for (int i = 0; i < NS; ++i) {
             CK(ctx_init(g, g->ctx[i]));
             CK(ensure_ws(g, g->ctx[i].ws, W, false, std::max(run.nhub, g->orig.nhub), rb));
