@@ -413,7 +413,7 @@ def main():
             kern = {"slices": {"ms": dom_ms, "alg_gb": sbytes / 1e9, "gbs": achieved}}
             extra = {}
             limiter = ("latency: each level's dependent L2 load chain (queue -> row -> sigma) and the barrier that "
-                       "ends it (DESIGN.md §4.2); DRAM traffic is below the algorithmic bytes")
+                       "ends it (DESIGN.md §4.3); DRAM traffic is below the algorithmic bytes")
         td = tr.get(dom, {})
         traffic = td.get("dram_bytes_per_launch")
         if traffic is not None and td.get("time_s"):
