@@ -20,6 +20,7 @@ namespace bcb {
 __global__ void gb_begin_kernel(const int2 *table, int *ctl, const int *src_all, int K, int *bsrc, uint64_t *active,
                                 const unsigned long long *stats, unsigned long long *stats_bak) {
     const int2 e = table[ctl[1]];
+    BC_CHECK(e.x >= 0 && e.y >= 1 && e.y <= K);
     for (int l = threadIdx.x; l < K; l += blockDim.x) bsrc[l] = l < e.y ? src_all[e.x + l] : -1;
     if (threadIdx.x < 8) {
         const int lo = 64 * threadIdx.x;

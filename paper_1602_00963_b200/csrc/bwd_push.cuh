@@ -347,6 +347,7 @@ struct PushKernel {
                     const int s = slot_of(sm.cd, nslots, e);
                     sl[k] = s;
                     vv[k] = ld_stream(p.col + sm.rs[s] + (e - sm.cd[s]), pol);
+                    BC_CHECK(s >= 0 && s < nslots && vv[k] >= 0 && vv[k] < p.n);
                 }
             }
             uint64_t cc[R][W];
@@ -437,6 +438,7 @@ struct PushKernel {
                     const int s = slot_of(sm.cd, nslots, e);
                     sl[k] = s;
                     vv[k] = ld_stream(p.col + sm.rs[s] + (e - sm.cd[s]), pol);
+                    BC_CHECK(s >= 0 && s < nslots && vv[k] >= 0 && vv[k] < p.n);
                 }
             }
             uint64_t cc[R][W];

@@ -423,6 +423,7 @@ struct LanesKernel {
     // ---- forward commit: x discovered in its undiscovered lanes (ub) where
     // acc != 0 (or overflowed); the level-(L+1) row of x is written whole.
     __device__ void commit_fwd(int x, int deg, uint32_t ub, const SigT (&acc)[LPT], uint32_t aovf) {
+        BC_CHECK(x >= 0 && x < p.n);
         uint32_t nb = aovf;
 #pragma unroll
         for (int i = 0; i < LPT; ++i)
@@ -555,6 +556,7 @@ struct LanesKernel {
                     int s = slot_of(sm.cd, nslots, e);
                     sl[k] = s;
                     vv[k] = ld_stream(p.col + sm.rs[s] + (e - sm.cd[s]), pol);
+                    BC_CHECK(s >= 0 && s < nslots && vv[k] >= 0 && vv[k] < p.n);
                 }
             }
             uint64_t cc[R][W];
@@ -884,10 +886,12 @@ struct LanesKernel {
         __syncthreads();
         const int h = sm.scan[0];
         __syncthreads();
+        BC_CHECK(h >= 0 && h < p.nhub);
         const int x = p.hub_ids[h];
         const int seg = unit - p.hub_seg_off[h];
         const int a = p.rp[x] + seg * p.seg_len;
         const int b = min(p.rp[x + 1], a + p.seg_len);
+        BC_CHECK(seg >= 0 && a < b);
         uint64_t u[W];
         bool any = false;
 #pragma unroll
@@ -1277,6 +1281,7 @@ __global__ void cap_extract_kernel(int n, int L, const uint64_t *mask, const RT 
             const int b = __ffsll((long long)m) - 1;
             m &= m - 1;
             const int l = 64 * j + b, c = lane_cap[l];
+            BC_CHECK(c >= 0);
             cap_depth[(size_t)c * n + v] = L;
             cap_sigma[(size_t)c * n + v] = (double)rows[(size_t)v * K + l];
         }

@@ -536,6 +536,9 @@ __device__ __forceinline__ unsigned lowdeg_code(int L) { return (unsigned)(L % 3
 #ifndef BC_SM_AGG
 #define BC_SM_AGG 1  // one tail atomic per warp per neighbour group (test-and-sets issued together)
 #endif
+#ifndef BC_SM_PF
+#define BC_SM_PF 1  // a thread's next frontier slot (vertex, row) is loaded while it works on the current one
+#endif
 #ifndef BC_SM_QROW
 #define BC_SM_QROW 0  // discoverer copies the new vertex's ELL row next to its queue slot
 #endif
@@ -632,9 +635,16 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
             int *cnt = &sm.cnt[r3];
             const int r3n = r3 == 2 ? 0 : r3 + 1;
             if (tid == 0) sm.cnt[r3n] = 0;
+            int v_pf = -1;  // BC_SM_PF: the next slot's vertex and row, loaded one slot ahead
+            int4 row_pf = make_int4(0, 0, 0, 0);
             for (int i = qs + tid; i < qe; i += BC_SM_NT) {
-                const int v = Q[i];
-                const int4 row = (QROW && L >= 1) ? QR[i] : lowdeg_row<ELL>(p, v);
+                const int v = v_pf >= 0 ? v_pf : Q[i];
+                const int4 row = v_pf >= 0 ? row_pf : ((QROW && L >= 1) ? QR[i] : lowdeg_row<ELL>(p, v));
+                v_pf = -1;
+                if (BC_SM_PF && !QROW && i + BC_SM_NT < qe) {
+                    v_pf = Q[i + BC_SM_NT];
+                    row_pf = lowdeg_row<ELL>(p, v_pf);
+                }
                 if (L >= 1) {
                     double sg = 0.0;
                     lowdeg_row_nbrs<ELL>(p, row, [&](const int *u) {
@@ -717,6 +727,7 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
             __syncthreads();
             qs = qe;
             qe += *cnt;
+            BC_CHECK(qe <= p.n && L + 2 <= p.n + 1);
             r3 = r3n;
             ++L;
             if (tid == 0) loff[L + 1] = qe;
@@ -743,10 +754,17 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
         for (L = Lmax; L >= 1; --L) {
             const unsigned cch = lowdeg_code(L + 1);
             for (int i = a + tid; i < b; i += BC_SM_NT) {
-                const bool first = i == a + tid;
-                const int w = first ? wq : Q[i];
-                const int4 row = first ? rq : (QROW ? QR[i] : lowdeg_row<ELL>(p, w));
-                const double sg = first ? sq : sc[w];
+                // the slot's (vertex, row, sigma): loaded before the level's barrier
+                // (first slot) or during the previous slot (BC_SM_PF)
+                const bool pre = i == a + tid || (BC_SM_PF && !QROW);
+                const int w = pre ? wq : Q[i];
+                const int4 row = pre ? rq : (QROW ? QR[i] : lowdeg_row<ELL>(p, w));
+                const double sg = pre ? sq : sc[w];
+                if (BC_SM_PF && !QROW && i + BC_SM_NT < b) {
+                    wq = Q[i + BC_SM_NT];
+                    rq = lowdeg_row<ELL>(p, wq);
+                    sq = sc[wq];
+                }
                 double acc = 0.0;
                 lowdeg_row_nbrs<ELL>(p, row, [&](const int *v) {
                     double x[BC_LD_GRP];

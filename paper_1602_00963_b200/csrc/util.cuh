@@ -8,6 +8,23 @@
 #endif
 #define BC_NW (BC_NT / 32)        // warps per CTA
 
+// Device-side bounds checks (compute-sanitizer is not available on the GPU
+// pool): a -DBC_DEVICE_CHECKS=1 build traps on a violated index invariant,
+// which surfaces as a CUDA error in the calling test.  Off in the product build.
+#ifndef BC_DEVICE_CHECKS
+#define BC_DEVICE_CHECKS 0
+#endif
+#if BC_DEVICE_CHECKS
+#define BC_CHECK(cond)        \
+    do {                      \
+        if (!(cond)) __trap(); \
+    } while (0)
+#else
+#define BC_CHECK(cond) \
+    do {               \
+    } while (0)
+#endif
+
 namespace bcb {
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
