@@ -35,13 +35,29 @@ namespace bcb {
 __device__ __forceinline__ void red_add_f64(double *p, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
+#ifndef BC_PUSH_RED_HINT
+#define BC_PUSH_RED_HINT 0  // L2 policy of the push reds: 0 none, 1 evict_first, 2 evict_last
+#endif
 // predicated form: no branch around the red (the per-lane condition is data
 // dependent, a branch would diverge)
 __device__ __forceinline__ void red_add_f64_if(double *p, double v, uint32_t pred) {
+#if BC_PUSH_RED_HINT
+    uint64_t pol;
+#if BC_PUSH_RED_HINT == 1
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#else
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#endif
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.global.add.L2::cache_hint.f64 [%0], %1, %3;\n\t}" ::"l"(p),
+        "d"(v), "r"(pred), "l"(pol)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.global.add.f64 [%0], %1;\n\t}" ::"l"(p), "d"(v),
         "r"(pred)
         : "memory");
+#endif
 }
 
 // 1/x for x >= 1 (sigma): hardware approximation + two Newton steps, within

@@ -537,7 +537,7 @@ __device__ __forceinline__ unsigned lowdeg_code(int L) { return (unsigned)(L % 3
 #define BC_SM_AGG 1  // one tail atomic per warp per neighbour group (test-and-sets issued together)
 #endif
 #ifndef BC_SM_PF
-#define BC_SM_PF 1  // a thread's next frontier slot (vertex, row) is loaded while it works on the current one
+#define BC_SM_PF 0  // 1: a thread's next frontier slot loaded while it works on the current one (slower: profiles/exp_r2_grid_pf.txt)
 #endif
 #ifndef BC_SM_QROW
 #define BC_SM_QROW 0  // discoverer copies the new vertex's ELL row next to its queue slot
