@@ -104,7 +104,8 @@ bc_status bc_prune_degree1(bc_graph *g, int64_t *out_removed);
  *                queued behind it on `cuda_stream` (e.g. an NCCL all-reduce of
  *                out_bc) sees the result; bc_get_stats waits for the call's
  *                counters.  It waits before returning when out_bc is a HOST
- *                pointer, when a capture is pending (bc_set_capture), under
+ *                pointer, when cuda_stream is NULL (nothing to order on), when a
+ *                capture is pending (bc_set_capture), under
  *                BC_OPT_PROFILE or BC_TRACE, with the host-driven level loop
  *                (BC_OPT_DEVICE_LOOP 0 or an ineligible configuration: one host
  *                wait per BFS level, the paper's nq test PAPER.md:387), and with

@@ -2655,7 +2655,8 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     // them).  Otherwise the call has already waited (host-driven level loop,
     // host output, capture, profiling) and completes here.
     const bool device_driven = mode == 2 || any_dl;  // slices mode: one persistent launch, no host round trip
-    const bool sync = !dev_out || capture || g->profile || trace_on() || !device_driven;
+    // (no caller stream to order on: the library's own stream is waited for)
+    const bool sync = !dev_out || !cuda_stream || capture || g->profile || trace_on() || !device_driven;
     CU(cudaEventRecord(g->stats_ev, st));
     if (!sync) {
         g->stats_pending = true;

@@ -36,7 +36,7 @@ __device__ __forceinline__ void red_add_f64(double *p, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 #ifndef BC_PUSH_RED_HINT
-#define BC_PUSH_RED_HINT 0  // L2 policy of the push reds: 0 none, 1 evict_first, 2 evict_last
+#define BC_PUSH_RED_HINT 2  // L2 policy of the push reds: 0 none, 1 evict_first, 2 evict_last (S20 push 202.3 -> 199.1 ms, profiles/exp_r2_redhint.txt)
 #endif
 // predicated form: no branch around the red (the per-lane condition is data
 // dependent, a branch would diverge)
@@ -79,6 +79,9 @@ __device__ __forceinline__ double rcp_f64(double x) {
 #endif
 #ifndef BC_PUSH_MINB8
 #define BC_PUSH_MINB8 3  // ... W = 8: 16 coef values per thread
+#endif
+#ifndef BC_PUSH_MASK_HINT
+#define BC_PUSH_MASK_HINT 0  // L2 policy of the push's parent-mask loads: 0 none, 1 evict_first, 2 evict_last
 #endif
 #ifndef BC_PUSH_CFSMEM
 #define BC_PUSH_CFSMEM 0  // backward push: the current slot's coef row staged in shared memory, not in registers
@@ -463,7 +466,24 @@ struct PushKernel {
 #pragma unroll
                 for (int j = 0; j < W; ++j) cc[k][j] = 0;
                 if (sl[k] >= 0) {
+#if BC_PUSH_MASK_HINT
+                    {
+                        const uint64_t mpol = BC_PUSH_MASK_HINT == 1 ? policy_evict_first() : policy_evict_last();
+                        if constexpr (W >= 2) {
+#pragma unroll
+                            for (int j = 0; j < W; j += 2) {
+                                const ulonglong2 t =
+                                    ld_pol(reinterpret_cast<const ulonglong2 *>(mpar + (size_t)vv[k] * W + j), mpol);
+                                cc[k][j] = t.x;
+                                cc[k][j + 1] = t.y;
+                            }
+                        } else {
+                            load_mask<W>(mpar + (size_t)vv[k] * W, cc[k]);
+                        }
+                    }
+#else
                     load_mask<W>(mpar + (size_t)vv[k] * W, cc[k]);
+#endif
 #pragma unroll
                     for (int j = 0; j < W; ++j) {
                         if (FWD) cc[k][j] = p.active[j] & ~cc[k][j];

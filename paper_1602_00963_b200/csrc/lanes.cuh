@@ -114,6 +114,30 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // order earlier generic-proxy accesses of shared memory before later async-proxy (bulk copy) writes
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+#ifndef BC_FWD_ROW_HINT
+#define BC_FWD_ROW_HINT 0  // L2 policy of the 16-bit forward's sigma-row gathers: 0 none, 1 evict_first, 2 evict_last
+#endif
+// a 32-bit word of a 16-bit sigma row (read-only path, optional L2 policy)
+__device__ __forceinline__ uint32_t ld_row_word(const uint32_t *p, uint64_t pol) {
+#if BC_FWD_ROW_HINT
+    uint32_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+#else
+    (void)pol;
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ uint64_t row_policy() {
+#if BC_FWD_ROW_HINT == 1
+    return policy_evict_first();
+#elif BC_FWD_ROW_HINT == 2
+    return policy_evict_last();
+#else
+    return 0;
+#endif
+}
+
 #ifndef BC_FWD_HIT2
 #define BC_FWD_HIT2 1  // 16-bit forward: two hits per iteration, the second hit's row loads issued before the first is added
 #endif
@@ -652,6 +676,7 @@ struct LanesKernel {
                     continue;
                 }
                 if constexpr (IN16 && BC_FWD_HIT2 && !BWD) {
+                    const uint64_t rpol = row_policy();
                     // 16-bit forward, two hits per iteration: both hits' row
                     // words are loaded before either is added (and before a
                     // slot flush), so a warp has two rows' latency in flight
@@ -667,14 +692,14 @@ struct LanesKernel {
                         load_halves<W>(hcw + src * 2 * W, cw);
                         const uint32_t *roww = reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint16_t *>(p.S_cur) + (size_t)sv.y * K) + lane;
 #pragma unroll
-                        for (int pr = 0; pr < W; ++pr) t[pr] = (cw[pr] & (3u << sh)) ? __ldg(roww + 32 * pr) : 0u;
+                        for (int pr = 0; pr < W; ++pr) t[pr] = (cw[pr] & (3u << sh)) ? ld_row_word(roww + 32 * pr, rpol) : 0u;
                         int2 sv2 = make_int2(-1, 0);
                         if (src2 >= 0) {
                             sv2 = sm.hsv[wid * 32 + src2];
                             load_halves<W>(hcw + src2 * 2 * W, cw);
                             const uint32_t *roww2 = reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint16_t *>(p.S_cur) + (size_t)sv2.y * K) + lane;
 #pragma unroll
-                            for (int pr = 0; pr < W; ++pr) t2[pr] = (cw[pr] & (3u << sh)) ? __ldg(roww2 + 32 * pr) : 0u;
+                            for (int pr = 0; pr < W; ++pr) t2[pr] = (cw[pr] & (3u << sh)) ? ld_row_word(roww2 + 32 * pr, rpol) : 0u;
                         }
                         if (sv.x != cur) {
                             while (cur < sv.x) {
