@@ -115,7 +115,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 #ifndef BC_FWD_ROW_HINT
-#define BC_FWD_ROW_HINT 0  // L2 policy of the 16-bit forward's sigma-row gathers: 0 none, 1 evict_first, 2 evict_last
+#define BC_FWD_ROW_HINT 2  // L2 policy of the 16-bit forward's sigma-row gathers: 0 none, 1 evict_first, 2 evict_last (~1 %, profiles/exp_r2_fwd_rowhint.txt)
 #endif
 // a 32-bit word of a 16-bit sigma row (read-only path, optional L2 policy)
 __device__ __forceinline__ uint32_t ld_row_word(const uint32_t *p, uint64_t pol) {
