@@ -32,6 +32,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+_emit = None  # set by main(): writes one JSON line to the real stdout
+
 METRIC = "BC TEPS (sources·m/s) at 1/2/4/8 B200; % HBM roofline; speedup vs CPU oracle"
 
 CONFIGS = {
@@ -195,7 +197,7 @@ def run_reference(args, cfg):
             "cpu_baseline": {"value": v, "unit": "TEPS", "cores": cores, "kind": "oracle",
                              "sample": f"{per_step} sources per step (one per core), uniform sample seed 11"},
             "e2e": {"value": v, "unit": "TEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    _emit(line)
 
 
 def algorithmic_bytes(st, K):
@@ -229,6 +231,12 @@ def slices_bytes(st):
 
 
 def main():
+    # the one JSON line goes to the real stdout; everything else the process
+    # prints there (NCCL's version banner, library chatter) goes to stderr
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+    global _emit
+    _emit = lambda line: os.write(json_fd, (json.dumps(line) + "\n").encode())  # noqa: E731
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=8)
@@ -450,7 +458,7 @@ def main():
             "stats": {k: agg[k] for k in ("levels_total", "batches", "narrow_batches", "narrow_fallbacks",
                                           "reached", "adj_reached", "dag_edges")},
         }
-        print(json.dumps(line), flush=True)
+        _emit(line)
     if world > 1:
         dist.destroy_process_group()
     G.close()

@@ -83,6 +83,17 @@ __device__ __forceinline__ double rcp_f64(double x) {
 #ifndef BC_PUSH_MASK_HINT
 #define BC_PUSH_MASK_HINT 0  // L2 policy of the push's parent-mask loads: 0 none, 1 evict_first, 2 evict_last
 #endif
+#ifndef BC_PUSH_OWN_HINT
+#define BC_PUSH_OWN_HINT 0  // 1: the slot's own accumulator row read and re-zeroed with L2 evict_first
+#endif
+__device__ __forceinline__ double ld_ef_f64(const double *p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_ef_f64(double *p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
 #ifndef BC_PUSH_CFSMEM
 #define BC_PUSH_CFSMEM 0  // backward push: the current slot's coef row staged in shared memory, not in registers
 #endif
@@ -234,7 +245,11 @@ struct PushKernel {
                 av[q] = 0.0;
                 if (bits >> (h + q) & 1u) {
                     sv[q] = (double)row[32 * (h + q)];
+#if BC_PUSH_OWN_HINT
+                    av[q] = ld_ef_f64(arow + 32 * (h + q), policy_evict_first());
+#else
                     av[q] = arow[32 * (h + q)];
+#endif
                 }
             }
 #pragma unroll
@@ -245,7 +260,11 @@ struct PushKernel {
                     const double delta = sv[q] * av[q];
                     cf[j] = (1.0 + om + delta) * rcp_f64(sv[q]);
                     if (owned) {
+#if BC_PUSH_OWN_HINT
+                        st_ef_f64(arow + 32 * j, 0.0, policy_evict_first());
+#else
                         arow[32 * j] = 0.0;
+#endif
                         contrib += p.lane_w1[32 * j + lane] * (delta + om);
                         cap_delta_put(p, 32 * j + lane, x, delta);
                     }
