@@ -2437,7 +2437,10 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
             r = body();
         }
         cudaEventDestroy(start);
-        if (r != BC_OK) return r;
+        if (r != BC_OK) {
+            if (r == BC_ERR_NOMEM) g->sizing.key[0] = -1;  // re-size on the next call
+            return r;
+        }
         if (!cfg.fp64_inline) {
             // 4-byte rows: batches whose 32-bit sigma overflowed (sigma >= 2^32,
             // never on R-MAT) re-run on the host-driven fp64 path
@@ -2610,7 +2613,10 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
         if (start) cudaEventDestroy(start);
         if (trace_on()) tr_join = now_us();
         for (int i = 0; i < NS; ++i)
-            if (sts[i] != BC_OK) return fail(sts[i], "%s", msgs[i].c_str());
+            if (sts[i] != BC_OK) {
+                if (sts[i] == BC_ERR_NOMEM) g->sizing.key[0] = -1;  // re-size on the next call
+                return fail(sts[i], "%s", msgs[i].c_str());
+            }
         for (int i = 0; i < NS; ++i) {
             LaneCtx &x = g->ctx[i];
             if (NS > 1) CU(cudaStreamWaitEvent(st, x.done, 0));

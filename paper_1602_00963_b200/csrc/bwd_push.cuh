@@ -84,7 +84,8 @@ __device__ __forceinline__ double rcp_f64(double x) {
 #define BC_PUSH_MASK_HINT 0  // L2 policy of the push's parent-mask loads: 0 none, 1 evict_first, 2 evict_last
 #endif
 #ifndef BC_PUSH_OWN_HINT
-#define BC_PUSH_OWN_HINT 0  // 1: the slot's own accumulator row read and re-zeroed with L2 evict_first
+#define BC_PUSH_OWN_HINT 1  // the slot's own accumulator row read and re-zeroed with L2 evict_first
+                            // (S20 push 198.8 -> 194.1 ms, profiles/exp_r2_push_l2hints.txt); 2: its sigma row too
 #endif
 __device__ __forceinline__ double ld_ef_f64(const double *p, uint64_t pol) {
     double v;
@@ -244,7 +245,18 @@ struct PushKernel {
                 sv[q] = 1.0;
                 av[q] = 0.0;
                 if (bits >> (h + q) & 1u) {
+#if BC_PUSH_OWN_HINT == 2
+                    if constexpr (std::is_same<RT, uint16_t>::value) {
+                        unsigned short t;
+                        asm volatile("ld.global.L2::cache_hint.u16 %0, [%1], %2;"
+                                     : "=h"(t) : "l"(row + 32 * (h + q)), "l"(policy_evict_first()));
+                        sv[q] = (double)t;
+                    } else {
+                        sv[q] = (double)row[32 * (h + q)];
+                    }
+#else
                     sv[q] = (double)row[32 * (h + q)];
+#endif
 #if BC_PUSH_OWN_HINT
                     av[q] = ld_ef_f64(arow + 32 * (h + q), policy_evict_first());
 #else

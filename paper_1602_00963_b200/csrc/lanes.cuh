@@ -114,6 +114,9 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // order earlier generic-proxy accesses of shared memory before later async-proxy (bulk copy) writes
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+#ifndef BC_FWD_MASK_HINT
+#define BC_FWD_MASK_HINT 0  // L2 policy of the forward's item mask loads (lvl[L][v]): 0 none, 2 evict_last
+#endif
 #ifndef BC_FWD_ROW_HINT
 #define BC_FWD_ROW_HINT 2  // L2 policy of the 16-bit forward's sigma-row gathers: 0 none, 1 evict_first, 2 evict_last (~1 %, profiles/exp_r2_fwd_rowhint.txt)
 #endif
@@ -589,7 +592,21 @@ struct LanesKernel {
 #pragma unroll
                 for (int j = 0; j < W; ++j) cc[k][j] = 0;
                 if (sl[k] >= 0) {
+#if BC_FWD_MASK_HINT
+                    if constexpr (W >= 2) {
+                        const uint64_t mpol = policy_evict_last();
+#pragma unroll
+                        for (int j = 0; j < W; j += 2) {
+                            const ulonglong2 t = ld_pol(reinterpret_cast<const ulonglong2 *>(mread + (size_t)vv[k] * W + j), mpol);
+                            cc[k][j] = t.x;
+                            cc[k][j + 1] = t.y;
+                        }
+                    } else {
+                        load_mask<W>(mread + (size_t)vv[k] * W, cc[k]);
+                    }
+#else
                     load_mask<W>(mread + (size_t)vv[k] * W, cc[k]);
+#endif
 #pragma unroll
                     for (int j = 0; j < W; ++j) cc[k][j] &= sm.u[sl[k] * W + j];
                 }
