@@ -93,4 +93,9 @@ __global__ void gb_end_kernel(int *ctl, const int *flags, int lcap, unsigned lon
     ctl[1] += 1;
 }
 
+// the condition of a conditional (IF) graph node: run its body iff *flag != 0
+__global__ void gb_set_cond_kernel(cudaGraphConditionalHandle h, const int *flag) {
+    cudaGraphSetConditional(h, *flag ? 1u : 0u);
+}
+
 }  // namespace bcb

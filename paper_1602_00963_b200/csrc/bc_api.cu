@@ -241,10 +241,13 @@ struct LaneCtx {
     cudaGraphExec_t gexec = nullptr;
     std::vector<uintptr_t> gkey;
     size_t gnodes = 0;                // nodes of the graph (kernels and copies) launched per batch
+    cudaStream_t side[2] = {nullptr, nullptr};  // capture of the conditional tiers' bodies
     bool ready = false;
     void release() {
         if (gexec) cudaGraphExecDestroy(gexec), gexec = nullptr;
         gkey.clear();
+        for (auto &sd : side)
+            if (sd) cudaStreamDestroy(sd), sd = nullptr;
         dfree(gb_src);
         dfree(gb_ctl);
         dfree(gb_active);
@@ -1441,27 +1444,82 @@ void enqueue_tier(bc_graph *g, LaneCtx &x, const DevBatchCfg &cfg, const int *ne
         lanes_endpoint_kernel<<<(K + 255) / 256, 256, 0, st>>>(x.gb_src, K, cfg.omega, ws.lane_ns, x.d_bc, need, halt);
 }
 
-template <int W>
-bc_status enqueue_device_batch(bc_graph *g, LaneCtx &x, const DevBatchCfg &cfg) {
-    constexpr int K = 64 * W;
+#ifndef BC_DEVLOOP_COND
+#define BC_DEVLOOP_COND 1  // on graphs with n > 2^18 the 32-bit / fp64 tiers sit in conditional (IF) graph
+#endif                     // nodes instead of gated launches (S20 -0.9 %; on S12 the IF nodes cost more than the
+                           // ~70 no-op launches they skip: 1.85 -> 2.55 ms, profiles/exp_r2_devloop_cond.txt)
+
+// At the capture point of x.st: an IF node whose condition (*flag != 0) a
+// one-thread kernel sets on the device, with `body` captured into the node's
+// body graph on the side stream `side` (x.st points at it meanwhile).
+template <typename F>
+bc_status capture_if(LaneCtx &x, cudaStream_t side, const int *flag, F &&body) {
     cudaStream_t st = x.st;
-    gb_begin_kernel<<<1, 512, 0, st>>>(x.gb_table, x.gb_ctl, g->d_src, K, x.gb_src, x.gb_active, x.d_stats,
-                                       x.gb_stats_bak);
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t graph = nullptr;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    CU(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd));
+    cudaGraphConditionalHandle h;
+    CU(cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault));
+    gb_set_cond_kernel<<<1, 1, 0, st>>>(h, flag);
+    CU(cudaGetLastError());
+    CU(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeIf;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    CU(cudaGraphAddNode(&node, graph, deps, nd, &np));
+    cudaGraph_t body_graph = np.conditional.phGraph_out[0];
+    CU(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+    CU(cudaStreamBeginCaptureToGraph(side, body_graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    x.st = side;
+    const bc_status s = body();
+    x.st = st;
+    cudaGraph_t tmp = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(side, &tmp);
+    if (s != BC_OK) return s;
+    CU(e);
+    return BC_OK;
+}
+
+template <int W>
+bc_status enqueue_device_batch(bc_graph *g, LaneCtx &x, const DevBatchCfg &cfg, cudaStream_t side1,
+                               cudaStream_t side2) {
+    constexpr int K = 64 * W;
+    gb_begin_kernel<<<1, 512, 0, x.st>>>(x.gb_table, x.gb_ctl, g->d_src, K, x.gb_src, x.gb_active, x.d_stats,
+                                         x.gb_stats_bak);
     enqueue_tier<W, unsigned>(g, x, cfg, nullptr, x.gb_ctl + 2);
-    enqueue_tier<W, long long>(g, x, cfg, x.gb_ctl + 2, x.gb_ctl + 3);
-    if (cfg.fp64_inline) enqueue_tier<W, double>(g, x, cfg, x.gb_ctl + 3, nullptr);
-    gb_end_kernel<<<1, 32, 0, st>>>(x.gb_ctl, x.d_flags, cfg.lcap, x.gb_cnt, x.gb_redo, cfg.fp64_inline ? 1 : 0,
-                                    x.d_stats, x.gb_stats_bak);
+    if (BC_DEVLOOP_COND && side1 && g->n > (1 << 18)) {
+        // 32-bit tier only if the 16-bit one overflowed, fp64 only if the 32-bit one did
+        CK(capture_if(x, side1, x.gb_ctl + 2, [&]() -> bc_status {
+            enqueue_tier<W, long long>(g, x, cfg, x.gb_ctl + 2, x.gb_ctl + 3);
+            if (cfg.fp64_inline)
+                CK(capture_if(x, side2, x.gb_ctl + 3, [&]() -> bc_status {
+                    enqueue_tier<W, double>(g, x, cfg, x.gb_ctl + 3, nullptr);
+                    return BC_OK;
+                }));
+            return BC_OK;
+        }));
+    } else {
+        enqueue_tier<W, long long>(g, x, cfg, x.gb_ctl + 2, x.gb_ctl + 3);
+        if (cfg.fp64_inline) enqueue_tier<W, double>(g, x, cfg, x.gb_ctl + 3, nullptr);
+    }
+    gb_end_kernel<<<1, 32, 0, x.st>>>(x.gb_ctl, x.d_flags, cfg.lcap, x.gb_cnt, x.gb_redo, cfg.fp64_inline ? 1 : 0,
+                                      x.d_stats, x.gb_stats_bak);
     CU(cudaGetLastError());
     return BC_OK;
 }
 
-bc_status enqueue_device_batch_w(bc_graph *g, LaneCtx &x, int W, const DevBatchCfg &cfg) {
+bc_status enqueue_device_batch_w(bc_graph *g, LaneCtx &x, int W, const DevBatchCfg &cfg, cudaStream_t s1,
+                                 cudaStream_t s2) {
     switch (W) {
-        case 1: return enqueue_device_batch<1>(g, x, cfg);
-        case 2: return enqueue_device_batch<2>(g, x, cfg);
-        case 4: return enqueue_device_batch<4>(g, x, cfg);
-        case 8: return enqueue_device_batch<8>(g, x, cfg);
+        case 1: return enqueue_device_batch<1>(g, x, cfg, s1, s2);
+        case 2: return enqueue_device_batch<2>(g, x, cfg, s1, s2);
+        case 4: return enqueue_device_batch<4>(g, x, cfg, s1, s2);
+        case 8: return enqueue_device_batch<8>(g, x, cfg, s1, s2);
         default: return fail(BC_ERR_INTERNAL, "bad lane words %d", W);
     }
 }
@@ -1497,8 +1555,12 @@ bc_status device_batch_graph(bc_graph *g, LaneCtx &x, int W, const DevBatchCfg &
     if (x.gexec && key == x.gkey) return BC_OK;
     if (x.gexec) cudaGraphExecDestroy(x.gexec), x.gexec = nullptr;
     x.gkey.clear();
+    if (!x.side[0]) {  // side streams the conditional tiers' bodies are captured on
+        CU(cudaStreamCreateWithFlags(&x.side[0], cudaStreamNonBlocking));
+        CU(cudaStreamCreateWithFlags(&x.side[1], cudaStreamNonBlocking));
+    }
     CU(cudaStreamBeginCapture(x.st, cudaStreamCaptureModeThreadLocal));
-    bc_status s = enqueue_device_batch_w(g, x, W, cfg);
+    bc_status s = enqueue_device_batch_w(g, x, W, cfg, x.side[0], x.side[1]);
     cudaGraph_t graph = nullptr;
     const cudaError_t e = cudaStreamEndCapture(x.st, &graph);
     if (s != BC_OK) {

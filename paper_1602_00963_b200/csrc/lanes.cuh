@@ -328,16 +328,28 @@ __device__ __forceinline__ uint64_t interleave2(uint32_t a, uint32_t b) {
     y = (y | (y << 1)) & 0x5555555555555555ull;
     return x | (y << 1);
 }
+#ifndef BC_GATHER_REDUX
+#define BC_GATHER_REDUX 1  // mask words by two warp OR-reductions per word instead of ballots + bit interleave
+#endif
 // warp-collective: the W mask words whose thread-t bits are bits of `bits`;
-// word j is returned to lane j (other lanes: 0)
+// word j is returned to lane j (other lanes: 0).  Thread t's pair of word j
+// sits at bits 2t, 2t+1: threads 0-15 fill the low half, 16-31 the high half,
+// so each half is one OR-reduction of the threads' pairs shifted into place.
 template <int W>
 __device__ __forceinline__ uint64_t gather_words(uint32_t bits, int lane) {
     uint64_t mine = 0;
 #pragma unroll
     for (int j = 0; j < W; ++j) {
+#if BC_GATHER_REDUX
+        const uint32_t v = ((bits >> (2 * j)) & 3u) << ((2 * lane) & 31);
+        const uint32_t lo = __reduce_or_sync(0xffffffffu, lane < 16 ? v : 0u);
+        const uint32_t hi = __reduce_or_sync(0xffffffffu, lane >= 16 ? v : 0u);
+        if (lane == j) mine = (uint64_t)lo | ((uint64_t)hi << 32);
+#else
         const uint32_t b0 = __ballot_sync(0xffffffffu, (bits >> (2 * j)) & 1u);
         const uint32_t b1 = __ballot_sync(0xffffffffu, (bits >> (2 * j + 1)) & 1u);
         if (lane == j) mine = interleave2(b0, b1);
+#endif
     }
     return mine;
 }
