@@ -215,7 +215,14 @@ struct PushKernel {
     double *A;
     PushSmem<W> &sm;
     const int lane, wid;
+#ifndef BC_PUSH_CNT32
+#define BC_PUSH_CNT32 1  // 32-bit per-thread counters (fewer live registers in the hit loop)
+#endif
+#if BC_PUSH_CNT32
+    unsigned st_items = 0, st_hits = 0, st_dag = 0;  // per thread per launch: < 2^32 items / hits
+#else
     unsigned long long st_items = 0, st_hits = 0, st_dag = 0;
+#endif
 
     __device__ PushKernel(const LanesParams &pp, double *a, PushSmem<W> &s)
         : p(pp), A(a), sm(s), lane(lane_id()), wid(warp_id()) {}
@@ -385,7 +392,7 @@ struct PushKernel {
         for (int j = 0; j < NG; ++j) cf[j] = 0.0;
 #pragma unroll
         for (int q = 0; q < NG / 2; ++q) lp[q] = 0xffffffffu;
-        st_items += (lane == 0) ? (unsigned long long)(we - ws) : 0ull;
+        st_items += (lane == 0) ? (we - ws) : 0;
         for (int e0 = ws; e0 < we; e0 += 32 * R) {
             int sl[R], vv[R];
 #pragma unroll
@@ -476,7 +483,7 @@ struct PushKernel {
         double cf[NG];
 #pragma unroll
         for (int j = 0; j < NG; ++j) cf[j] = 0.0;
-        st_items += (lane == 0) ? (unsigned long long)(we - ws) : 0ull;
+        st_items += (lane == 0) ? (we - ws) : 0;
         for (int e0 = ws; e0 < we; e0 += 32 * R) {
             int sl[R], vv[R];
 #pragma unroll
@@ -697,8 +704,9 @@ struct PushKernel {
     }
 
     __device__ void epilogue() {
-        const unsigned long long it = warp_sum_u64(st_items), ht = warp_sum_u64(st_hits),
-                                 dg = warp_sum_u64(st_dag);
+        const unsigned long long it = warp_sum_u64((unsigned long long)st_items),
+                                 ht = warp_sum_u64((unsigned long long)st_hits),
+                                 dg = warp_sum_u64((unsigned long long)st_dag);
         if (lane == 0) {
             if (it) atomicAdd(p.stats + (FWD ? 4 : 6), it);
             if (ht) atomicAdd(p.stats + (FWD ? 5 : 7), ht);
