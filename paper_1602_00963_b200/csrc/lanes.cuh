@@ -328,6 +328,9 @@ __device__ __forceinline__ uint64_t interleave2(uint32_t a, uint32_t b) {
     y = (y | (y << 1)) & 0x5555555555555555ull;
     return x | (y << 1);
 }
+#ifndef BC_FWD_UNCOND
+#define BC_FWD_UNCOND 1  // 16-bit forward: hit rows loaded whole (no per-pair c test; rows are zero outside their level)
+#endif
 #ifndef BC_GATHER_REDUX
 #define BC_GATHER_REDUX 1  // mask words by two warp OR-reductions per word instead of ballots + bit interleave
 #endif
@@ -636,7 +639,11 @@ struct LanesKernel {
                 st_hits += (lane == 0) ? __popc(hm) : 0;
                 // publish (slot, v, c) of every item of this step in shared memory:
                 // a hit then costs two shared broadcasts instead of 2 + 2W shuffles
-                {
+                constexpr bool UNCOND = IN16 && BC_FWD_HIT2 && BC_FWD_UNCOND && !BWD && !Smem::BULK;
+                if constexpr (UNCOND) {  // the hit's c words are not read: (slot, v) only
+                    sm.hsv[wid * 32 + lane] = make_int2(sl[k], vv[k]);
+                    __syncwarp();
+                } else {
                     sm.hsv[wid * 32 + lane] = make_int2(sl[k], vv[k]);
                     uint32_t *hc = sm.hc + (wid * 32 + lane) * 2 * W;
                     uint32_t lo[W], hi[W];
@@ -718,17 +725,29 @@ struct LanesKernel {
                         if (src2 >= 0) hm &= hm - 1;
                         const int2 sv = sm.hsv[wid * 32 + src];
                         uint32_t cw[W], t[W], t2[W];
-                        load_halves<W>(hcw + src * 2 * W, cw);
                         const uint32_t *roww = reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint16_t *>(p.S_cur) + (size_t)sv.y * K) + lane;
+                        if constexpr (UNCOND) {
+                            // whole rows: lanes outside c read zeros (y not at level L
+                            // there) or values the commit discards (x not in u there)
 #pragma unroll
-                        for (int pr = 0; pr < W; ++pr) t[pr] = (cw[pr] & (3u << sh)) ? ld_row_word(roww + 32 * pr, rpol) : 0u;
+                            for (int pr = 0; pr < W; ++pr) t[pr] = ld_row_word(roww + 32 * pr, rpol);
+                        } else {
+                            load_halves<W>(hcw + src * 2 * W, cw);
+#pragma unroll
+                            for (int pr = 0; pr < W; ++pr) t[pr] = (cw[pr] & (3u << sh)) ? ld_row_word(roww + 32 * pr, rpol) : 0u;
+                        }
                         int2 sv2 = make_int2(-1, 0);
                         if (src2 >= 0) {
                             sv2 = sm.hsv[wid * 32 + src2];
-                            load_halves<W>(hcw + src2 * 2 * W, cw);
                             const uint32_t *roww2 = reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint16_t *>(p.S_cur) + (size_t)sv2.y * K) + lane;
+                            if constexpr (UNCOND) {
 #pragma unroll
-                            for (int pr = 0; pr < W; ++pr) t2[pr] = (cw[pr] & (3u << sh)) ? ld_row_word(roww2 + 32 * pr, rpol) : 0u;
+                                for (int pr = 0; pr < W; ++pr) t2[pr] = ld_row_word(roww2 + 32 * pr, rpol);
+                            } else {
+                                load_halves<W>(hcw + src2 * 2 * W, cw);
+#pragma unroll
+                                for (int pr = 0; pr < W; ++pr) t2[pr] = (cw[pr] & (3u << sh)) ? ld_row_word(roww2 + 32 * pr, rpol) : 0u;
+                            }
                         }
                         if (sv.x != cur) {
                             while (cur < sv.x) {
@@ -981,6 +1000,8 @@ struct LanesKernel {
             }
             // narrow: a segment partial above the limit already means overflow;
             // otherwise each add is <= 65535 and the hub row cannot wrap
+            // lanes outside u collect values the commit discards: not checked, not added
+            if (!((sm.u[l >> 6] >> (l & 63)) & 1ull)) sum = SigT(0);
             if (INTROW && (unsigned long long)sum > LIMIT) *p.narrow_ovf = 1;
             if (sum != SigT(0)) {
                 SigT *dst = reinterpret_cast<SigT *>(p.hub_acc) + (size_t)h * K + l;

@@ -539,6 +539,15 @@ __device__ __forceinline__ unsigned lowdeg_code(int L) { return (unsigned)(L % 3
 #ifndef BC_SM_PF
 #define BC_SM_PF 0  // 1: a thread's next frontier slot loaded while it works on the current one (slower: profiles/exp_r2_grid_pf.txt)
 #endif
+#ifndef BC_SM_RING
+#define BC_SM_RING 0  // > 0: the forward also keeps each level's queue slots (<= BC_SM_RING) in a shared double buffer
+#endif
+#ifndef BC_SM_BPF2
+#define BC_SM_BPF2 0  // backward: the next level's first-slot vertex id is loaded one level earlier (row / sigma at level start)
+#endif
+#ifndef BC_SM_LOFF
+#define BC_SM_LOFF 0  // > 0: level offsets of the first BC_SM_LOFF levels in shared memory (backward: one L2 hop less per level)
+#endif
 #ifndef BC_SM_QROW
 #define BC_SM_QROW 0  // discoverer copies the new vertex's ELL row next to its queue slot
 #endif
@@ -585,12 +594,28 @@ template <bool ELL, bool CAP = false>
 __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(SlicesParams p) {
     __shared__ SlicesSmem sm;
     extern __shared__ unsigned f2[];  // 2 bits per vertex
+#if BC_SM_LOFF
+    __shared__ int loff_s[BC_SM_LOFF];  // level offsets of levels < BC_SM_LOFF (the rest: global loff)
+#endif
+#if BC_SM_RING
+    __shared__ int qring[2 * BC_SM_RING];  // level L's slots at qring[(L & 1) * BC_SM_RING + (i - qs)]
+#endif
     const size_t n = (size_t)p.n;
     const int nw = (p.n + 15) / 16;
     const int tid = threadIdx.x;
     double *sc = p.sigma + blockIdx.x * n;  // sigma, then coef (in place)
     int *Q = p.queue + blockIdx.x * n;
-    int *loff = p.loff + blockIdx.x * (n + 2);
+    int *loff_g = p.loff + blockIdx.x * (n + 2);
+#if BC_SM_LOFF
+    auto lo_get = [&](int i) -> int { return i < BC_SM_LOFF ? loff_s[i] : loff_g[i]; };
+    auto lo_set = [&](int i, int v) {
+        if (i < BC_SM_LOFF) loff_s[i] = v;
+        else loff_g[i] = v;
+    };
+#else
+    auto lo_get = [&](int i) -> int { return loff_g[i]; };
+    auto lo_set = [&](int i, int v) { loff_g[i] = v; };
+#endif
     constexpr bool QROW = ELL && BC_SM_QROW;
     int4 *QR = QROW ? p.qrow + blockIdx.x * n : nullptr;
     const int lane = lane_id();
@@ -613,8 +638,11 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
             f2[s >> 4] |= lowdeg_code(0) << ((s & 15) * 2);
             sc[s] = 1.0;
             Q[0] = s;
-            loff[0] = 0;
-            loff[1] = 1;
+#if BC_SM_RING
+            qring[0] = s;
+#endif
+            lo_set(0, 0);
+            lo_set(1, 1);
             sm.cnt[0] = sm.cnt[1] = sm.cnt[2] = 0;
         }
         __syncthreads();
@@ -637,8 +665,16 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
             if (tid == 0) sm.cnt[r3n] = 0;
             int v_pf = -1;  // BC_SM_PF: the next slot's vertex and row, loaded one slot ahead
             int4 row_pf = make_int4(0, 0, 0, 0);
+#if BC_SM_RING
+            const int *ring_cur = qring + (L & 1) * BC_SM_RING;
+            int *ring_nxt = qring + ((L + 1) & 1) * BC_SM_RING;
+#endif
             for (int i = qs + tid; i < qe; i += BC_SM_NT) {
+#if BC_SM_RING
+                const int v = v_pf >= 0 ? v_pf : (i - qs < BC_SM_RING ? ring_cur[i - qs] : Q[i]);
+#else
                 const int v = v_pf >= 0 ? v_pf : Q[i];
+#endif
                 const int4 row = v_pf >= 0 ? row_pf : ((QROW && L >= 1) ? QR[i] : lowdeg_row<ELL>(p, v));
                 v_pf = -1;
                 if (BC_SM_PF && !QROW && i + BC_SM_NT < qe) {
@@ -693,6 +729,9 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
                             if (won[k]) {
                                 const int pos = base + __popc(bal[k] & lt);
                                 st_slot_stream(Q + pos, w[k]);
+#if BC_SM_RING
+                                if (pos - qe < BC_SM_RING) ring_nxt[pos - qe] = w[k];
+#endif
                                 if constexpr (QROW) QR[pos] = p.ell4[w[k]];
                             }
                             base += __popc(bal[k]);
@@ -717,6 +756,9 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
                             if (won) {
                                 const int pos = base + __popc(bal & ((1u << lane) - 1u));
                                 st_slot_stream(Q + pos, w[k]);
+#if BC_SM_RING
+                                if (pos - qe < BC_SM_RING) ring_nxt[pos - qe] = w[k];
+#endif
                                 if constexpr (QROW) QR[pos] = p.ell4[w[k]];
                             }
                         }
@@ -730,7 +772,7 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
             BC_CHECK(qe <= p.n && L + 2 <= p.n + 1);
             r3 = r3n;
             ++L;
-            if (tid == 0) loff[L + 1] = qe;
+            if (tid == 0) lo_set(L + 1, qe);
         }
         const int Lmax = L - 1;
         const int reached = qe;
@@ -742,17 +784,31 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
         int a = 0, b = 0, wq = -1;
         int4 rq = make_int4(0, 0, 0, 0);
         double sq = 0.0;
+        int wq1 = -1;  // BC_SM_BPF2: level L-1's first-slot vertex, loaded during level L+1
         if (Lmax >= 1) {
-            a = loff[Lmax];
-            b = loff[Lmax + 1];
+            a = lo_get(Lmax);
+            b = lo_get(Lmax + 1);
             if (a + tid < b) {
                 wq = Q[a + tid];
                 rq = QROW ? QR[a + tid] : lowdeg_row<ELL>(p, wq);
                 sq = sc[wq];
             }
+            if (BC_SM_BPF2 && Lmax - 1 >= 1 && lo_get(Lmax - 1) + tid < lo_get(Lmax)) wq1 = Q[lo_get(Lmax - 1) + tid];
         }
         for (L = Lmax; L >= 1; --L) {
             const unsigned cch = lowdeg_code(L + 1);
+#if BC_SM_BPF2
+            // level L-1's first slot (row, sigma: final since the forward) is
+            // loaded now, alongside level L's work, and level L-2's vertex id
+            int4 rq1 = make_int4(0, 0, 0, 0);
+            double sq1 = 0.0;
+            if (wq1 >= 0) {
+                rq1 = lowdeg_row<ELL>(p, wq1);
+                sq1 = sc[wq1];
+            }
+            int wq2 = -1;
+            if (L - 2 >= 1 && lo_get(L - 2) + tid < lo_get(L - 1)) wq2 = Q[lo_get(L - 2) + tid];
+#endif
             for (int i = a + tid; i < b; i += BC_SM_NT) {
                 // the slot's (vertex, row, sigma): loaded before the level's barrier
                 // (first slot) or during the previous slot (BC_SM_PF)
@@ -788,13 +844,20 @@ __global__ void __launch_bounds__(BC_SM_NT, BC_SM_MINB) slices_lowdeg_sm_kernel(
                 st_dsum += (unsigned long long)L;
                 ns_loc += 1.0 + om;
             }
-            const int an = loff[L - 1], bn = loff[L];
+            const int an = lo_get(L - 1), bn = lo_get(L);
+#if BC_SM_BPF2
+            wq = wq1;
+            rq = rq1;
+            sq = sq1;
+            wq1 = wq2;
+#else
             wq = -1;
             if (L - 1 >= 1 && an + tid < bn) {
                 wq = Q[an + tid];
                 rq = QROW ? QR[an + tid] : lowdeg_row<ELL>(p, wq);
                 sq = sc[wq];
             }
+#endif
             __syncthreads();
             a = an;
             b = bn;

@@ -1,0 +1,7 @@
+# grid kernel: threads per CTA / CTAs per SM (2-bit shared state: 64 KB per CTA at 512x512)
+for v in g512 g256m3 g384m3 g128m3 g512 g256m3 g384m3; do
+  echo -n "$v grid consecutive: "; BC_SO=build_exp/lib_$v.so timeout 120 python tools/prof_batch.py --grid 512 --sources 8192 --consecutive --repeat 2 --no-profile | tail -1 | cut -c1-100
+done
+for v in g256m3 g384m3; do
+echo -n "$v parity: "; BC_SO=build_exp/lib_$v.so timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_capture.py tests/test_gpu_configs.py -m gpu -q -x -p no:cacheprovider -k "slices or capture_small or grid" 2>&1 | tail -1
+done
