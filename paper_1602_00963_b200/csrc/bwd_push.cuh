@@ -133,7 +133,7 @@ __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double
 #pragma unroll
     for (int j = 0; j < NG; ++j) bits |= (((uint32_t)(m[j >> 1] >> ((j & 1) * 32)) >> lane) & 1u) << j;
     double *arow = A + (size_t)x * K + lane;
-    RT *row = S + (size_t)x * K + lane;
+    RT *row = S + (size_t)x * K;
     double av[NG], sv[NG];
 #pragma unroll
     for (int j = 0; j < NG; ++j) {
@@ -141,7 +141,7 @@ __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double
         sv[j] = 1.0;
         if (bits >> j & 1u) {
             av[j] = arow[32 * j];
-            sv[j] = (double)row[32 * j];
+            sv[j] = (double)row[row_idx<W, RT>(32 * j + lane)];
         }
     }
     const double om = p.omega ? (double)p.omega[x] : 0.0;
@@ -151,7 +151,7 @@ __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double
         if (bits >> j & 1u) {
             const double delta = sv[j] * av[j];
             arow[32 * j] = 0.0;
-            if constexpr (COEF) row[32 * j] = (1.0 + om + delta) / sv[j];
+            if constexpr (COEF) row[32 * j + lane] = (1.0 + om + delta) / sv[j];  // fp64 rows: lane order
             contrib += p.lane_w1[32 * j + lane] * (delta + om);
             cap_delta_put(p, 32 * j + lane, x, delta);
         }
@@ -239,7 +239,7 @@ struct PushKernel {
 #pragma unroll
         for (int j = 0; j < NG; ++j)
             bits |= (((uint32_t)(sm.u[hs * W + (j >> 1)] >> ((j & 1) * 32)) >> lane) & 1u) << j;
-        const RT *row = reinterpret_cast<const RT *>(p.S_cur) + (size_t)x * K + lane;
+        const RT *row = reinterpret_cast<const RT *>(p.S_cur) + (size_t)x * K;
         double *arow = A + (size_t)x * K + lane;
         const double om = p.omega ? (double)p.omega[x] : 0.0;
         double contrib = 0.0;
@@ -256,13 +256,13 @@ struct PushKernel {
                     if constexpr (std::is_same<RT, uint16_t>::value) {
                         unsigned short t;
                         asm volatile("ld.global.L2::cache_hint.u16 %0, [%1], %2;"
-                                     : "=h"(t) : "l"(row + 32 * (h + q)), "l"(policy_evict_first()));
+                                     : "=h"(t) : "l"(row + row_idx<W, RT>(32 * (h + q) + lane)), "l"(policy_evict_first()));
                         sv[q] = (double)t;
                     } else {
-                        sv[q] = (double)row[32 * (h + q)];
+                        sv[q] = (double)row[row_idx<W, RT>(32 * (h + q) + lane)];
                     }
 #else
-                    sv[q] = (double)row[32 * (h + q)];
+                    sv[q] = (double)row[row_idx<W, RT>(32 * (h + q) + lane)];
 #endif
 #if BC_PUSH_OWN_HINT
                     av[q] = ld_ef_f64(arow + 32 * (h + q), policy_evict_first());
@@ -354,7 +354,7 @@ struct PushKernel {
                 sv[q] = 1.0;
                 av[q] = 0.0;
                 if (h + q < nr && l < K) {
-                    sv[q] = (double)row[l];
+                    sv[q] = (double)row[row_idx<W, RT>(l)];
                     av[q] = arow[l];
                 }
             }

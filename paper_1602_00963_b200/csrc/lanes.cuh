@@ -63,6 +63,22 @@ template <> struct Vec2<long long> { using t = longlong2; };
 template <typename SigT> struct RowOf { using t = SigT; };
 template <> struct RowOf<unsigned> { using t = uint16_t; };
 template <> struct RowOf<long long> { using t = uint32_t; };
+
+#ifndef BC_NARROW_TMAJOR
+#define BC_NARROW_TMAJOR 1  // 16-bit sigma rows thread-major (a thread's W lane pairs are one vector)
+#endif
+// Position of lane l in a sigma row.  16-bit rows are stored thread-major:
+// the pair (2t, 2t+1) of 64-lane word i -- owned by thread t of the level
+// kernels -- is 32-bit word t*W + i, so a thread gathers or writes its W
+// pairs of a row with one W*4-byte vector access (16 B at W = 4).  Wider
+// rows keep lane order.
+template <int W, typename RT>
+__host__ __device__ __forceinline__ int row_idx(int l) {
+    if constexpr (BC_NARROW_TMAJOR && std::is_same<RT, uint16_t>::value)
+        return (((l & 63) >> 1) * W + (l >> 6)) * 2 + (l & 1);
+    else
+        return l;
+}
 template <typename SigT> struct RowLimit { static constexpr unsigned long long v = 0; };
 template <> struct RowLimit<unsigned> { static constexpr unsigned long long v = 65535ull; };
 template <> struct RowLimit<long long> { static constexpr unsigned long long v = 4294967295ull; };
@@ -131,6 +147,40 @@ __device__ __forceinline__ uint32_t ld_row_word(const uint32_t *p, uint64_t pol)
     return __ldg(p);
 #endif
 }
+// a thread's W consecutive 32-bit words of a thread-major 16-bit row
+template <int W>
+__device__ __forceinline__ void ld_row_vec(const uint32_t *p, uint64_t pol, uint32_t (&t)[W]) {
+    if constexpr (W >= 4) {
+#pragma unroll
+        for (int q = 0; q < W; q += 4) {
+#if BC_FWD_ROW_HINT
+            asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                         : "=r"(t[q]), "=r"(t[q + 1]), "=r"(t[q + 2]), "=r"(t[q + 3]) : "l"(p + q), "l"(pol));
+#else
+            const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p + q));
+            t[q] = v.x, t[q + 1] = v.y, t[q + 2] = v.z, t[q + 3] = v.w;
+#endif
+        }
+    } else if constexpr (W == 2) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(p));
+        t[0] = v.x, t[1] = v.y;
+        (void)pol;
+    } else {
+        t[0] = ld_row_word(p, pol);
+    }
+}
+template <int W>
+__device__ __forceinline__ void st_row_vec(uint32_t *p, const uint32_t (&t)[W]) {
+    if constexpr (W >= 4) {
+#pragma unroll
+        for (int q = 0; q < W; q += 4) *reinterpret_cast<uint4 *>(p + q) = make_uint4(t[q], t[q + 1], t[q + 2], t[q + 3]);
+    } else if constexpr (W == 2) {
+        *reinterpret_cast<uint2 *>(p) = make_uint2(t[0], t[1]);
+    } else {
+        p[0] = t[0];
+    }
+}
+
 __device__ __forceinline__ uint64_t row_policy() {
 #if BC_FWD_ROW_HINT == 1
     return policy_evict_first();
@@ -435,11 +485,18 @@ struct LanesKernel {
     __device__ __forceinline__ void store_slice(RT *row, uint32_t keep, const SigT (&v)[LPT]) {
         if constexpr (NARROW) {
             // lanes 2t, 2t+1 of a pair are the low / high half of one 32-bit word
+            uint32_t wv[W];
 #pragma unroll
             for (int pr = 0; pr < W; ++pr) {
                 const uint32_t lo = (keep >> (2 * pr) & 1u) ? (v[2 * pr] & 0xffffu) : 0u;
                 const uint32_t hi = (keep >> (2 * pr + 1) & 1u) ? (v[2 * pr + 1] & 0xffffu) : 0u;
-                *reinterpret_cast<uint32_t *>(row + 64 * pr + t2) = lo | (hi << 16);
+                wv[pr] = lo | (hi << 16);
+            }
+            if constexpr (BC_NARROW_TMAJOR) {
+                st_row_vec<W>(reinterpret_cast<uint32_t *>(row) + lane * W, wv);
+            } else {
+#pragma unroll
+                for (int pr = 0; pr < W; ++pr) *reinterpret_cast<uint32_t *>(row + 64 * pr + t2) = wv[pr];
             }
             return;
         }
@@ -658,6 +715,7 @@ struct LanesKernel {
                 }
                 const uint32_t *hcw = sm.hc + wid * 32 * 2 * W + (lane >> 4) * W;
                 const int sh = t2 & 31;
+                static_assert(!(Smem::BULK && BC_NARROW_TMAJOR), "the bulk-copy forward reads lane-order rows");
                 if constexpr (Smem::BULK && !BWD) {
                     // 16-bit forward, Blackwell bulk copies: lane 0 streams the
                     // hit rows (K x 16 bit, zero outside level L, so whole rows
@@ -725,28 +783,36 @@ struct LanesKernel {
                         if (src2 >= 0) hm &= hm - 1;
                         const int2 sv = sm.hsv[wid * 32 + src];
                         uint32_t cw[W], t[W], t2[W];
-                        const uint32_t *roww = reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint16_t *>(p.S_cur) + (size_t)sv.y * K) + lane;
+                        const uint32_t *roww = reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint16_t *>(p.S_cur) + (size_t)sv.y * K) + (BC_NARROW_TMAJOR ? lane * W : lane);
                         if constexpr (UNCOND) {
                             // whole rows: lanes outside c read zeros (y not at level L
                             // there) or values the commit discards (x not in u there)
+                            if constexpr (BC_NARROW_TMAJOR) {
+                                ld_row_vec<W>(roww, rpol, t);
+                            } else {
 #pragma unroll
-                            for (int pr = 0; pr < W; ++pr) t[pr] = ld_row_word(roww + 32 * pr, rpol);
+                                for (int pr = 0; pr < W; ++pr) t[pr] = ld_row_word(roww + 32 * pr, rpol);
+                            }
                         } else {
                             load_halves<W>(hcw + src * 2 * W, cw);
 #pragma unroll
-                            for (int pr = 0; pr < W; ++pr) t[pr] = (cw[pr] & (3u << sh)) ? ld_row_word(roww + 32 * pr, rpol) : 0u;
+                            for (int pr = 0; pr < W; ++pr) t[pr] = (cw[pr] & (3u << sh)) ? ld_row_word(roww + (BC_NARROW_TMAJOR ? pr : 32 * pr), rpol) : 0u;
                         }
                         int2 sv2 = make_int2(-1, 0);
                         if (src2 >= 0) {
                             sv2 = sm.hsv[wid * 32 + src2];
-                            const uint32_t *roww2 = reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint16_t *>(p.S_cur) + (size_t)sv2.y * K) + lane;
+                            const uint32_t *roww2 = reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint16_t *>(p.S_cur) + (size_t)sv2.y * K) + (BC_NARROW_TMAJOR ? lane * W : lane);
                             if constexpr (UNCOND) {
+                                if constexpr (BC_NARROW_TMAJOR) {
+                                    ld_row_vec<W>(roww2, rpol, t2);
+                                } else {
 #pragma unroll
-                                for (int pr = 0; pr < W; ++pr) t2[pr] = ld_row_word(roww2 + 32 * pr, rpol);
+                                    for (int pr = 0; pr < W; ++pr) t2[pr] = ld_row_word(roww2 + 32 * pr, rpol);
+                                }
                             } else {
                                 load_halves<W>(hcw + src2 * 2 * W, cw);
 #pragma unroll
-                                for (int pr = 0; pr < W; ++pr) t2[pr] = (cw[pr] & (3u << sh)) ? ld_row_word(roww2 + 32 * pr, rpol) : 0u;
+                                for (int pr = 0; pr < W; ++pr) t2[pr] = (cw[pr] & (3u << sh)) ? ld_row_word(roww2 + (BC_NARROW_TMAJOR ? pr : 32 * pr), rpol) : 0u;
                             }
                         }
                         if (sv.x != cur) {
@@ -802,11 +868,11 @@ struct LanesKernel {
                     // (lanes outside c only collect values the commit discards)
                     if constexpr (IN16) {
                         // 16-bit rows: one 32-bit load per pair (lanes 2t, 2t+1)
-                        const uint32_t *roww = reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint16_t *>(p.S_cur) + (size_t)sv.y * K) + lane;
+                        const uint32_t *roww = reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint16_t *>(p.S_cur) + (size_t)sv.y * K) + (BC_NARROW_TMAJOR ? lane * W : lane);
 #pragma unroll
                         for (int pr = 0; pr < W; ++pr) {
                             if (cw[pr] & (3u << sh)) {
-                                const uint32_t t = __ldg(roww + 32 * pr);
+                                const uint32_t t = __ldg(roww + (BC_NARROW_TMAJOR ? pr : 32 * pr));
                                 acc[2 * pr] += t & 0xffffu;
                                 acc[2 * pr + 1] += t >> 16;
                             }
@@ -1237,18 +1303,18 @@ __global__ void __launch_bounds__(256) lanes_derive_kernel(DeriveParams q) {
                     double sa = 0.0;
                     unsigned long long ia = 0;
                     if (ma >> b & 1ull) {
-                        sa += (double)rl[lc - 2];
-                        ia += (unsigned long long)rl[lc - 2];
+                        sa += (double)rl[row_idx<W, RT>(lc - 2)];
+                        ia += (unsigned long long)rl[row_idx<W, RT>(lc - 2)];
                     }
                     if (mb >> b & 1ull) {
-                        sa += (double)rl[lc - 1];
-                        ia += (unsigned long long)rl[lc - 1];
+                        sa += (double)rl[row_idx<W, RT>(lc - 1)];
+                        ia += (unsigned long long)rl[row_idx<W, RT>(lc - 1)];
                     }
                     if constexpr (LIMIT != 0) {
                         big |= ia > LIMIT;
-                        rn[lc] = (RT)ia;
+                        rn[row_idx<W, RT>(lc)] = (RT)ia;
                     } else {
-                        rn[lc] = (RT)sa;
+                        rn[row_idx<W, RT>(lc)] = (RT)sa;
                     }
                 }
             }
@@ -1296,9 +1362,9 @@ __global__ void lanes_materialize_kernel(int n, const uint64_t *mask, SigT *S, c
 #pragma unroll
         for (int j = 0; j < W; ++j)
             if (j == word) mw = mask[(size_t)v * W + j];
-        SigT *row = S + (size_t)v * K + lane * LPT;
+        SigT *row = S + (size_t)v * K;
 #pragma unroll
-        for (int i = 0; i < LPT; ++i) row[i] = (mw >> (off + i) & 1ull) ? SigT(1) : SigT(0);
+        for (int i = 0; i < LPT; ++i) row[row_idx<W, SigT>(lane * LPT + i)] = (mw >> (off + i) & 1ull) ? SigT(1) : SigT(0);
     }
 }
 
@@ -1358,7 +1424,7 @@ __global__ void cap_extract_kernel(int n, int L, const uint64_t *mask, const RT 
             const int l = 64 * j + b, c = lane_cap[l];
             BC_CHECK(c >= 0);
             cap_depth[(size_t)c * n + v] = L;
-            cap_sigma[(size_t)c * n + v] = (double)rows[(size_t)v * K + l];
+            cap_sigma[(size_t)c * n + v] = (double)rows[(size_t)v * K + row_idx<W, RT>(l)];
         }
     }
 }

@@ -1,0 +1,9 @@
+# 16-bit sigma rows thread-major (BC_NARROW_TMAJOR=1: one vector gather per hit row) vs lane order (0)
+for v in tm0 tm1 tm0 tm1; do
+  echo -n "$v S20 1pipe: "; BC_SO=build_exp/lib_$v.so timeout 200 python tools/prof_batch.py --sources 8192 --streams 1 --repeat 2 | tail -1 | cut -c1-120
+done
+for v in tm0 tm1; do
+  echo -n "$v S20 auto: "; BC_SO=build_exp/lib_$v.so timeout 200 python tools/prof_batch.py --sources 8192 --lane-words 0 --repeat 3 --no-profile | tail -1 | cut -c1-80
+  echo -n "$v S16 16k: "; BC_SO=build_exp/lib_$v.so timeout 200 python tools/prof_batch.py --scale 16 --sources 16384 --lane-words 0 --repeat 2 --no-profile | tail -1 | cut -c1-80
+done
+echo -n "tm1 suite: "; BC_SO=build_exp/lib_tm1.so timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -1
