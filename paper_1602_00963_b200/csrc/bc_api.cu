@@ -801,8 +801,8 @@ bc_status ensure_ws(bc_graph *g, LaneWS &ws, int W, bool verify, int nhub, int r
         CK(dalloc(&ws.ns_snap, 3 * (size_t)K));
         CK(dalloc((double **)&ws.part, (size_t)g->num_sms * 8 * BC_NW * 2 * K));
         if (!verify) {
-            CK(dalloc(&ws.A, n * K));
-            CU(cudaMemset(ws.A, 0, n * K * sizeof(double)));
+            CK(dalloc(&ws.A, n * (K + BC_A_PAD)));
+            CU(cudaMemset(ws.A, 0, n * (K + BC_A_PAD) * sizeof(double)));
         }
         ws.W = W;
         ws.verify = verify;

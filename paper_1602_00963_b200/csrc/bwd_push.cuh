@@ -32,6 +32,12 @@
 
 namespace bcb {
 
+#ifndef BC_A_PAD
+#define BC_A_PAD 0  // doubles of padding after each accumulator row (row stride K + pad)
+#endif
+// row stride of the fp64 backward accumulators A[v][K]
+template <int W> struct AStride { static constexpr size_t v = 64 * W + BC_A_PAD; };
+
 __device__ __forceinline__ void red_add_f64(double *p, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
@@ -132,7 +138,7 @@ __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double
     uint32_t bits = 0;
 #pragma unroll
     for (int j = 0; j < NG; ++j) bits |= (((uint32_t)(m[j >> 1] >> ((j & 1) * 32)) >> lane) & 1u) << j;
-    double *arow = A + (size_t)x * K + lane;
+    double *arow = A + (size_t)x * AStride<W>::v + lane;
     RT *row = S + (size_t)x * K;
     double av[NG], sv[NG];
 #pragma unroll
@@ -240,7 +246,7 @@ struct PushKernel {
         for (int j = 0; j < NG; ++j)
             bits |= (((uint32_t)(sm.u[hs * W + (j >> 1)] >> ((j & 1) * 32)) >> lane) & 1u) << j;
         const RT *row = reinterpret_cast<const RT *>(p.S_cur) + (size_t)x * K;
-        double *arow = A + (size_t)x * K + lane;
+        double *arow = A + (size_t)x * AStride<W>::v + lane;
         const double om = p.omega ? (double)p.omega[x] : 0.0;
         double contrib = 0.0;
         // two halves of the groups (bounded live registers: cf stays live in the hit loop)
@@ -342,7 +348,7 @@ struct PushKernel {
                                                 double (&cf)[NG]) {
         const int x = sm.vert[hs];
         const RT *row = reinterpret_cast<const RT *>(p.S_cur) + (size_t)x * K;
-        double *arow = A + (size_t)x * K;
+        double *arow = A + (size_t)x * AStride<W>::v;
         const double om = p.omega ? (double)p.omega[x] : 0.0;
         double contrib = 0.0;
 #pragma unroll
@@ -446,7 +452,7 @@ struct PushKernel {
 #pragma unroll
                         for (int j = 0; j < W; ++j) st_dag += __popcll(sm.hc[(wid * 32 + src) * W + j] & p.derived[j]);
                     }
-                    double *arow = A + (size_t)y * K;
+                    double *arow = A + (size_t)y * AStride<W>::v;
 #pragma unroll
                     for (int r = 0; r < NG; ++r) {
                         if (r < nr) {  // uniform
@@ -565,7 +571,7 @@ struct PushKernel {
                             }
                         }
                     }
-                    double *arow = A + (size_t)y * K + lane;
+                    double *arow = A + (size_t)y * AStride<W>::v + lane;
                     uint64_t myword = 0;  // fwd: thread j < W ORs word j of c into lvl[L+1][y]
                     uint64_t cwords[W];
                     static_assert(W <= 8, "");
@@ -765,7 +771,7 @@ __global__ void __launch_bounds__(BC_NT) lanes_fwd_commit_kernel(LanesParams p, 
             any |= m[j] != 0;
         }
         if (!any) continue;  // warp-uniform
-        double *arow = A + (size_t)x * K + lane;
+        double *arow = A + (size_t)x * AStride<W>::v + lane;
         double *row = S + (size_t)x * K + lane;
         double av[NG];
         uint32_t bits = 0;
