@@ -142,6 +142,7 @@ struct LaneWS {
     double *lane_ns = nullptr;
     void *part = nullptr;  // split-slot partial sums [max CTAs][BC_NW][2][K]
     double *A = nullptr;   // push-backward accumulators [n][K], zero between batches
+    double *Arep = nullptr;  // replicas of the hub parents' rows [BC_REP_R][BC_REP_H][K], zero between levels
     unsigned long long *lvl_snap = nullptr;  // [3][8] counters before each of the last 3 forward levels (widening)
     double *ns_snap = nullptr;               // [3][K] n_s accumulators likewise
     int *lane_cap = nullptr;       // [K] capture slot of each lane or -1 (bc_set_capture)
@@ -803,6 +804,10 @@ bc_status ensure_ws(bc_graph *g, LaneWS &ws, int W, bool verify, int nhub, int r
         if (!verify) {
             CK(dalloc(&ws.A, n * (K + BC_A_PAD)));
             CU(cudaMemset(ws.A, 0, n * (K + BC_A_PAD) * sizeof(double)));
+            if (BC_REP_H > 0) {
+                CK(dalloc(&ws.Arep, (size_t)BC_REP_R * BC_REP_H * K));
+                CU(cudaMemset(ws.Arep, 0, (size_t)BC_REP_R * BC_REP_H * K * sizeof(double)));
+            }
         }
         ws.W = W;
         ws.verify = verify;
@@ -1202,6 +1207,7 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
             cudaFuncSetAttribute(khb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
             p.lane_cap = c.cap_vslot ? ws.lane_cap : nullptr;
             p.cap_delta = c.cap_delta;
+            p.arep = ws.Arep;
             for (int l = Lb; l >= 1; --l) {
                 p.level = l;
                 p.S_cur = ws.slev[l];
@@ -1263,6 +1269,7 @@ bc_status run_batch(bc_graph *g, LaneCtx &x, const BatchCtx &c, std::vector<cuda
                     cudaEventRecord(e0, st);
                 }
                 const bool w32 = wide_from >= 0 && l > wide_from;
+                if (p.arep && l < Lb) lanes_rep_fold_kernel<W><<<(BC_REP_H * K + BC_NT - 1) / BC_NT, BC_NT, 0, st>>>(p, ws.A);
                 if (l >= 2) {
                     if (w32) kpush32<<<gridp, BC_NT, 0, st>>>(p, ws.A);
                     else kpush<<<gridp, BC_NT, 0, st>>>(p, ws.A);
@@ -1425,6 +1432,7 @@ void enqueue_tier(bc_graph *g, LaneCtx &x, const DevBatchCfg &cfg, const int *ne
     const int gridp = std::max(1, std::min(g->conc ? g->num_sms * std::max(1, occp) * BC_PGRID_NUM / BC_PGRID_DEN
                                                           : g->num_sms * std::max(1, occp), units));
     const unsigned fin_blocks = (unsigned)std::min<int64_t>(((int64_t)n * 32 + BC_NT - 1) / BC_NT, (int64_t)g->num_sms * 8);
+    p.arep = ws.Arep;
     for (int l = cfg.lcap; l >= 1; --l) {
         p.level = l;
         p.S_cur = ws.slev[l];
@@ -1434,6 +1442,7 @@ void enqueue_tier(bc_graph *g, LaneCtx &x, const DevBatchCfg &cfg, const int *ne
         p.mask_nxt = nullptr;
         p.any_new = x.gb_ctl + 5;  // unused
         p.prev_new = x.d_flags + l;  // level l non-empty
+        if (p.arep && l < cfg.lcap) lanes_rep_fold_kernel<W><<<(BC_REP_H * K + BC_NT - 1) / BC_NT, BC_NT, 0, st>>>(p, ws.A);
         if (l >= 2) kpush<<<gridp, BC_NT, 0, st>>>(p, ws.A);
         if (l == 1)
             lanes_bwd_finalize_kernel<W, false, RT><<<fin_blocks, BC_NT, 0, st>>>(p, ws.A);

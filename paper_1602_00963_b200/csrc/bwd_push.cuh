@@ -38,6 +38,36 @@ namespace bcb {
 // row stride of the fp64 backward accumulators A[v][K]
 template <int W> struct AStride { static constexpr size_t v = 64 * W + BC_A_PAD; };
 
+#ifndef BC_REP_H
+#define BC_REP_H 64  // parents with id < BC_REP_H (degree order: the hubs) get replicated accumulator rows
+#endif
+#ifndef BC_REP_R
+#define BC_REP_R 8   // ... in BC_REP_R copies, so their reds spread over more L2 slices
+#endif
+// A[y] += sum of the replicas of row y (y < BC_REP_H), replicas re-zeroed.
+// Runs before each backward level: every red into A[y][l] comes from the
+// push at level d_l(y) + 1 and A[y][l] is read at level d_l(y), so folding
+// at every level delivers each lane's sum before it is used.
+template <int W>
+__global__ void __launch_bounds__(BC_NT) lanes_rep_fold_kernel(LanesParams p, double *__restrict__ A) {
+    if ((p.prev_new && *p.prev_new == 0) || gated_off(p)) return;
+    constexpr int K = 64 * W;
+    const int i = blockIdx.x * BC_NT + threadIdx.x;
+    const int y = i / K, l = i % K;
+    if (y >= BC_REP_H || y >= p.n) return;
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < BC_REP_R; ++r) {
+        double *q = p.arep + ((size_t)r * BC_REP_H + y) * K + l;
+        const double v = *q;
+        if (v != 0.0) {
+            s += v;
+            *q = 0.0;
+        }
+    }
+    if (s != 0.0) A[(size_t)y * AStride<W>::v + l] += s;
+}
+
 __device__ __forceinline__ void red_add_f64(double *p, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
@@ -572,6 +602,8 @@ struct PushKernel {
                         }
                     }
                     double *arow = A + (size_t)y * AStride<W>::v + lane;
+                    if (!FWD && BC_REP_H > 0 && y < BC_REP_H && p.arep)  // uniform: a hub parent's replica
+                        arow = p.arep + ((size_t)(blockIdx.x % BC_REP_R) * BC_REP_H + y) * K + lane;
                     uint64_t myword = 0;  // fwd: thread j < W ORs word j of c into lvl[L+1][y]
                     uint64_t cwords[W];
                     static_assert(W <= 8, "");

@@ -306,6 +306,11 @@ struct LanesParams {
     const uint64_t *active_dev;  // [8]
     const int *need;
     const int *halt;
+    // backward: replicas of the accumulator rows of the BC_REP_H lowest ids
+    // (the highest-degree parents), [BC_REP_R][BC_REP_H][K]; a push CTA reds
+    // into copy blockIdx % BC_REP_R, lanes_rep_fold_kernel adds the copies
+    // into A before each backward level; nullable (no replicas)
+    double *arep;
 };
 
 __device__ __forceinline__ bool gated_off(const int *need, const int *halt) {
