@@ -82,6 +82,35 @@ bc_status bc_graph_create(int64_t n, const int64_t *row_ptr, const int32_t *col_
 bc_status bc_prune_degree1(bc_graph *g, int64_t *out_removed);
 
 /*
+ * bc_prune_degree1_share / bc_prune_degree1_apply -- the distributed form of
+ * Alg.6 ("if u mod #P = P_i assign (u,v) to
+ * E_i"; 1-D partitioning keeps all edges of u on one processor,
+ * PAPER.md:584-586).  Each of `nranks` processes holding the same graph
+ * calls _share for its `rank`: the vertices u = rank, rank + nranks, ... are
+ * scanned, u with a single edge (u,v) is removed (removed_part[u] = 1) and
+ * omega_part[v] is incremented (lines 6-9).  The caller sums the nranks
+ * outputs element-wise (one all-reduce of 2 n uint32, e.g. NCCL on the same
+ * stream) and passes the sums to _apply, which drops the symmetric edges of
+ * the removed ones and leaves the handle in exactly the
+ * state bc_prune_degree1 produces (no cascaded tree removal).
+ *   omega_part, removed_part  DEVICE uint32[n] on the handle's device,
+ *                overwritten (zeroed, then this share's contributions).
+ *   cuda_stream  _share: stream-ordered on it and asynchronous (NULL: the
+ *                library stream, synchronous).  _apply: waits for it first.
+ *   omega, removed  DEVICE uint32[n]: the sums over all ranks; removed[v]
+ *                must be 1 exactly for the degree-1 vertices, else
+ *                BC_ERR_INVALID (a share missing or counted twice) and the
+ *                handle is unchanged.
+ *   out_removed  nullable; number of removed vertices.
+ * BC_ERR_STATE if the handle was already pruned; BC_ERR_INVALID on a bad
+ * rank, NULL or host pointers.  Ownership: the caller's buffers.
+ */
+bc_status bc_prune_degree1_share(const bc_graph *g, int rank, int nranks, uint32_t *omega_part,
+                                 uint32_t *removed_part, void *cuda_stream);
+bc_status bc_prune_degree1_apply(bc_graph *g, const uint32_t *omega, const uint32_t *removed, void *cuda_stream,
+                                 int64_t *out_removed);
+
+/*
  * bc_compute -- exact BC restricted to a source set S (Eq.3 with s in S):
  *     out_bc[v] = sum_{s in S, s != v} delta_s(v)
  * computed on the device: per batch of sources, a level-synchronous forward

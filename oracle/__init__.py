@@ -47,6 +47,7 @@ def _lib():
         L.oracle_bc.argtypes = [ctypes.c_int64, i64p, i32p, i32p, ctypes.c_int64, ctypes.c_int, f64p, i64p]
         L.oracle_sssp.argtypes = [ctypes.c_int64, i64p, i32p, ctypes.c_int32, i32p, u64p, u8p, f64p, f64p]
         L.oracle_prune_degree1.argtypes = [ctypes.c_int64, i64p, i32p, u32p, u8p, i64p, i32p, i64p]
+        L.oracle_prune_degree1_share.argtypes = [ctypes.c_int64, i64p, i32p, ctypes.c_int, ctypes.c_int, u32p, u32p]
         L.oracle_bc_pruned.argtypes = [ctypes.c_int64, i64p, i32p, i32p, ctypes.c_int64, ctypes.c_int, f64p]
         L.oracle_two_degree_tree.argtypes = [ctypes.c_int64, ctypes.c_int32, i32p, u64p, u8p, i32p, u64p, u8p, i32p,
                                              u64p, u8p]
@@ -148,6 +149,20 @@ def prune_degree1(g):
                                 _p(rm, ctypes.c_uint8), _p(rrp, ctypes.c_int64), _p(rcol, ctypes.c_int32),
                                 ctypes.byref(nnz))
     return om, rm, rrp, rcol[: nnz.value].copy()
+
+
+def prune_degree1_share(g, nprocs: int, i: int):
+    """Alg.6 on processor i of nprocs (edges (u,v) with u mod nprocs = i):
+    (omega_part uint32[n], removed_part uint32[n]); the sums over i are
+    prune_degree1's omega and removed."""
+    n, rp, col = _csr(g)
+    om = np.empty(n, np.uint32)
+    rm = np.empty(n, np.uint32)
+    rc = _lib().oracle_prune_degree1_share(n, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32), int(nprocs), int(i),
+                                           _p(om, ctypes.c_uint32), _p(rm, ctypes.c_uint32))
+    if rc != 0:
+        raise ValueError("processor index out of range")
+    return om, rm
 
 
 def bc_pruned(g, sources=None, threads: int = 0):

@@ -23,6 +23,7 @@
  *  oracle_bc        Eq.(3): BC(v) = sum_{s in S, s != v}
  *                   delta_s(v), unnormalised ordered pairs (reading R14).
  *  oracle_prune_degree1   Alg.6 "1-Degree Preprocessing",
+ *  oracle_prune_degree1_share  Alg.6 on processor i of #P (u mod #P split),
  *                   single processor, one pass, no cascade (PAPER.md:580 fn.).
  *  oracle_bc_pruned Eq.(4)/(5) with the readings R7-R13 of DESIGN.md
  *                   (omega taken before each increment; n_s = sum over reached
@@ -253,6 +254,32 @@ int oracle_prune_degree1(int64_t n, const int64_t *rp, const int32_t *col, uint3
         res_rp[u + 1] = k;
     }
     *res_nnz = k;
+    return 0;
+}
+
+/* Alg.6 on processor P_i of #P: E_i = the
+ * edges (u,v) with u mod #P = i (1-D partitioning: all edges of u on one
+ * processor), scanned sorted by u (the CSR order).  For
+ * each (u,v) in E_i: if no other edge (w,z) of E_i has w = u, append (v,u)
+ * to R -- removed_part[u] = 1 -- and omega_part[v] += 1; otherwise (u,v)
+ * belongs to E'_i.  Outputs omega_part[n], removed_part[n] (zero outside
+ * this processor's contributions).  Summing the #P outputs gives omega and
+ * removed of the single-processor pass; the residual graph is then E' minus
+ * the symmetric copies of R, as in oracle_prune_degree1. */
+int oracle_prune_degree1_share(int64_t n, const int64_t *rp, const int32_t *col, int P, int i,
+                               uint32_t *omega_part, uint32_t *removed_part) {
+    if (P < 1 || i < 0 || i >= P) return 1;
+    for (int64_t v = 0; v < n; ++v) { omega_part[v] = 0; removed_part[v] = 0; }
+    for (int64_t u = 0; u < n; ++u) {
+        if (u % P != i) continue;                    /* (u,v) not assigned to E_i */
+        for (int64_t e = rp[u]; e < rp[u + 1]; ++e) {
+            int has_other = (e > rp[u]) || (e + 1 < rp[u + 1]);  /* predecessor / successor with w = u */
+            if (!has_other) {
+                removed_part[u] = 1;                 /* (v,u) -> R */
+                omega_part[col[e]] += 1;             /* omega[v] = omega[v] + 1 */
+            }
+        }
+    }
     return 0;
 }
 

@@ -100,6 +100,36 @@ class Graph:
         self.pruned = True
         return int(removed.value)
 
+    def prune_degree1_share(self, rank: int, nranks: int, omega_part, removed_part, stream=None):
+        """Alg.6 share of processor ``rank`` of ``nranks`` (u mod nranks =
+        rank) into two torch uint32/int32 CUDA tensors of n elements,
+        stream-ordered on ``stream`` (default: torch's current stream)."""
+        import torch
+
+        for t in (omega_part, removed_part):
+            if not (isinstance(t, torch.Tensor) and t.is_cuda and t.numel() == self.n and t.element_size() == 4
+                    and t.is_contiguous()):
+                raise ValueError("share outputs must be contiguous 4-byte CUDA tensors of n elements")
+        st = stream if stream is not None else torch.cuda.current_stream(omega_part.device)
+        _check(_L.load().bc_prune_degree1_share(self._h, int(rank), int(nranks), omega_part.data_ptr(),
+                                                removed_part.data_ptr(), st.cuda_stream))
+
+    def prune_degree1_apply(self, omega, removed, stream=None) -> int:
+        """Residual graph from the summed shares (see bc.h); returns the
+        number of removed vertices."""
+        import torch
+
+        for t in (omega, removed):
+            if not (isinstance(t, torch.Tensor) and t.is_cuda and t.numel() == self.n and t.element_size() == 4
+                    and t.is_contiguous()):
+                raise ValueError("inputs must be contiguous 4-byte CUDA tensors of n elements")
+        st = stream if stream is not None else torch.cuda.current_stream(omega.device)
+        r = ctypes.c_int64(0)
+        _check(_L.load().bc_prune_degree1_apply(self._h, omega.data_ptr(), removed.data_ptr(), st.cuda_stream,
+                                                ctypes.byref(r)))
+        self.pruned = True
+        return int(r.value)
+
     def compute(self, sources=None, out=None, stream=None):
         """BC over ``sources`` (None = all / all eligible).
 

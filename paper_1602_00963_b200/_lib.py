@@ -74,6 +74,8 @@ _i64, _i32, _u32, _vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.
 SIGNATURES = {
     "bc_graph_create": (ctypes.c_int, [_i64, _vp, _vp, ctypes.c_int, _u32, ctypes.POINTER(_vp)]),
     "bc_prune_degree1": (ctypes.c_int, [_vp, ctypes.POINTER(_i64)]),
+    "bc_prune_degree1_share": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
+    "bc_prune_degree1_apply": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.POINTER(_i64)]),
     "bc_compute": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp]),
     "bc_destroy": (ctypes.c_int, [_vp]),
     "bc_status_string": (ctypes.c_char_p, [ctypes.c_int]),

@@ -2066,20 +2066,13 @@ bc_status bc_graph_create(int64_t n, const int64_t *row_ptr, const int32_t *col_
     return BC_OK;
 }
 
-bc_status bc_prune_degree1(bc_graph *g, int64_t *out_removed) {
-    if (!g) return fail(BC_ERR_INVALID, "NULL handle");
-    if (g->pruned) return fail(BC_ERR_STATE, "graph already pruned (single pass, PAPER.md:580)");
-    DeviceGuard dg(g->device);
-    CK(wait_idle(g));
-    cudaStream_t st = g->own_stream;
+// residual CSR from g->omega / g->removed and the residual degrees (device),
+// then the compute layout; shared by the single pass and the exchanged shares
+static bc_status prune_finish(bc_graph *g, int *rdeg, cudaStream_t st, int64_t *out_removed) {
     const int n = (int)g->n;
-    CK(dalloc(&g->omega, n));
-    CK(dalloc(&g->removed, n));
-    int *rdeg = nullptr, *tot = nullptr;
-    CK(dalloc(&rdeg, n));
+    int *tot = nullptr;
     CK(dalloc(&tot, 1));
     const unsigned wblocks = (unsigned)(((int64_t)n * 32 + 255) / 256);
-    prune_count_kernel<<<wblocks, 256, 0, st>>>(n, g->orig.rp, g->orig.col, g->omega, g->removed, rdeg);
     CK(dalloc(&g->res.rp, (size_t)n + 1));
     CK(dev_scan(g, rdeg, g->res.rp, n, tot, st));
     CU(cudaMemcpyAsync(g->res.rp + n, tot, sizeof(int), cudaMemcpyDeviceToDevice, st));
@@ -2087,7 +2080,7 @@ bc_status bc_prune_degree1(bc_graph *g, int64_t *out_removed) {
     CU(cudaMemcpyAsync(&rnnz, tot, sizeof(int), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     CK(dalloc(&g->res.col, (size_t)rnnz));
-    prune_compact_kernel<<<wblocks, 256, 0, st>>>(n, g->orig.rp, g->orig.col, g->res.rp, g->res.col);
+    prune_compact_kernel<<<wblocks, 256, 0, st>>>(n, g->orig.rp, g->orig.col, g->removed, g->res.rp, g->res.col);
     CU(cudaGetLastError());
     g->res.nnz = rnnz;
     g->h_omega.resize(n);
@@ -2098,7 +2091,6 @@ bc_status bc_prune_degree1(bc_graph *g, int64_t *out_removed) {
     CU(cudaMemcpyAsync(rd.data(), rdeg, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     g->res.h_deg = rd;
-    dfree(rdeg);
     dfree(tot);
     g->pruned = true;
     CK(build_layout(g, g->res, st));  // bc_sssp traverses the residual graph in caller ids
@@ -2109,6 +2101,87 @@ bc_status bc_prune_degree1(bc_graph *g, int64_t *out_removed) {
         *out_removed = r;
     }
     return BC_OK;
+}
+
+bc_status bc_prune_degree1(bc_graph *g, int64_t *out_removed) {
+    if (!g) return fail(BC_ERR_INVALID, "NULL handle");
+    if (g->pruned) return fail(BC_ERR_STATE, "graph already pruned (single pass, PAPER.md:580)");
+    DeviceGuard dg(g->device);
+    CK(wait_idle(g));
+    cudaStream_t st = g->own_stream;
+    const int n = (int)g->n;
+    CK(dalloc(&g->omega, n));
+    CK(dalloc(&g->removed, n));
+    int *rdeg = nullptr;
+    CK(dalloc(&rdeg, n));
+    const unsigned wblocks = (unsigned)(((int64_t)n * 32 + 255) / 256);
+    prune_count_kernel<<<wblocks, 256, 0, st>>>(n, g->orig.rp, g->orig.col, g->omega, g->removed, rdeg);
+    const bc_status rc = prune_finish(g, rdeg, st, out_removed);
+    dfree(rdeg);
+    return rc;
+}
+
+bc_status bc_prune_degree1_share(const bc_graph *g, int rank, int nranks, uint32_t *omega_part,
+                                 uint32_t *removed_part, void *cuda_stream) {
+    if (!g) return fail(BC_ERR_INVALID, "NULL handle");
+    if (g->pruned) return fail(BC_ERR_STATE, "graph already pruned (single pass, PAPER.md:580)");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(BC_ERR_INVALID, "rank %d of %d out of range", rank, nranks);
+    if (!omega_part || !removed_part) return fail(BC_ERR_INVALID, "NULL output");
+    DeviceGuard dg(g->device);
+    if (!is_device_ptr(omega_part) || !is_device_ptr(removed_part))
+        return fail(BC_ERR_INVALID, "share outputs must be device memory");
+    bc_graph *gm = const_cast<bc_graph *>(g);
+    CK(wait_idle(gm));
+    cudaStream_t st = cuda_stream ? (cudaStream_t)cuda_stream : g->own_stream;
+    const int n = (int)g->n;
+    CU(cudaMemsetAsync(omega_part, 0, (size_t)n * 4, st));
+    CU(cudaMemsetAsync(removed_part, 0, (size_t)n * 4, st));
+    const long long mine = ((long long)n - rank + nranks - 1) / nranks;  // vertices u = rank, rank + nranks, ...
+    if (mine > 0)
+        prune_share_kernel<<<(unsigned)((mine + 255) / 256), 256, 0, st>>>(n, g->orig.rp, g->orig.col, rank, nranks,
+                                                                            omega_part, removed_part);
+    CU(cudaGetLastError());
+    if (!cuda_stream) CU(cudaStreamSynchronize(st));
+    return BC_OK;
+}
+
+bc_status bc_prune_degree1_apply(bc_graph *g, const uint32_t *omega, const uint32_t *removed, void *cuda_stream,
+                                 int64_t *out_removed) {
+    if (!g) return fail(BC_ERR_INVALID, "NULL handle");
+    if (g->pruned) return fail(BC_ERR_STATE, "graph already pruned (single pass, PAPER.md:580)");
+    if (!omega || !removed) return fail(BC_ERR_INVALID, "NULL input");
+    DeviceGuard dg(g->device);
+    if (!is_device_ptr(omega) || !is_device_ptr(removed)) return fail(BC_ERR_INVALID, "inputs must be device memory");
+    CK(wait_idle(g));
+    if (cuda_stream) CU(cudaStreamSynchronize((cudaStream_t)cuda_stream));  // the exchange that produced the inputs
+    cudaStream_t st = g->own_stream;
+    const int n = (int)g->n;
+    uint8_t *rm = nullptr;
+    uint32_t *om = nullptr;
+    int *rdeg = nullptr, *err = nullptr;
+    CK(dalloc(&rm, n));
+    CK(dalloc(&om, n));
+    CK(dalloc(&rdeg, n));
+    CK(dalloc(&err, 1));
+    CU(cudaMemsetAsync(err, 0, sizeof(int), st));
+    CU(cudaMemcpyAsync(om, omega, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    const unsigned wblocks = (unsigned)(((int64_t)n * 32 + 255) / 256);
+    prune_flags_kernel<<<wblocks, 256, 0, st>>>(n, g->orig.rp, g->orig.col, removed, rm, rdeg, err);
+    int herr = 0;
+    CU(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    dfree(err);
+    if (herr) {
+        dfree(rm);
+        dfree(om);
+        dfree(rdeg);
+        return fail(BC_ERR_INVALID, "removed flags are not the sum of all shares (a vertex is removed iff its degree is 1)");
+    }
+    g->omega = om;
+    g->removed = rm;
+    const bc_status rc = prune_finish(g, rdeg, st, out_removed);
+    dfree(rdeg);
+    return rc;
 }
 
 bc_status bc_set_option(bc_graph *g, int option, int64_t value) {

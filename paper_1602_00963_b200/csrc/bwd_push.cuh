@@ -39,7 +39,7 @@ namespace bcb {
 template <int W> struct AStride { static constexpr size_t v = 64 * W + BC_A_PAD; };
 
 #ifndef BC_REP_H
-#define BC_REP_H 64  // parents with id < BC_REP_H (degree order: the hubs) get replicated accumulator rows
+#define BC_REP_H 0  // > 0: parents with id < BC_REP_H (degree order: the hubs) get replicated accumulator rows (slower, off)
 #endif
 #ifndef BC_REP_R
 #define BC_REP_R 8   // ... in BC_REP_R copies, so their reds spread over more L2 slices

@@ -66,13 +66,16 @@ __global__ void prune_count_kernel(int n, const int *rp, const int *col, uint32_
 }
 
 // Alg.6 lines 10-11 + PAPER.md:590-591: residual edge list E' keeps (u,v)
-// when neither endpoint was removed; order within a row is preserved.
-__global__ void prune_compact_kernel(int n, const int *rp, const int *col, const int *rrp, int *rcol) {
+// when neither endpoint was removed (removed[] of the whole graph: this
+// device's pass, or the sum of the processors' shares); order within a row
+// is preserved.
+__global__ void prune_compact_kernel(int n, const int *rp, const int *col, const uint8_t *removed, const int *rrp,
+                                     int *rcol) {
     const int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = lane_id();
     if (v >= n) return;
     const int a = rp[v], b = rp[v + 1];
-    if (b - a == 1) return;  // removed vertex: empty residual row
+    if (removed[v]) return;  // removed vertex: empty residual row
     int out = rrp[v];
     for (int e0 = a; e0 < b; e0 += 32) {
         const int e = e0 + lane;
@@ -80,11 +83,51 @@ __global__ void prune_compact_kernel(int n, const int *rp, const int *col, const
         bool keep = false;
         if (e < b) {
             u = col[e];
-            keep = (rp[u + 1] - rp[u]) != 1;
+            keep = !removed[u];
         }
         unsigned m = __ballot_sync(0xffffffffu, keep);
         if (keep) rcol[out + __popc(m & ((1u << lane) - 1u))] = u;
         out += __popc(m);
+    }
+}
+
+// Alg.6 on processor `rank` of `nranks` (the
+// 1-D split "u mod #P = P_i"): thread per vertex u of this share; u with a
+// single edge (u,v) is removed and omega(v) incremented.  The outputs are
+// zero-initialised by the caller; their sums over the ranks are the
+// single-pass omega and removed flags.
+__global__ void prune_share_kernel(int n, const int *rp, const int *col, int rank, int nranks, uint32_t *omega_part,
+                                   uint32_t *removed_part) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long u = i * nranks + rank;
+    if (u >= n) return;
+    const int a = rp[u], b = rp[u + 1];
+    if (b - a == 1) {
+        removed_part[u] = 1u;
+        atomicAdd(omega_part + col[a], 1u);
+    }
+}
+
+// From the exchanged (summed) flags: removed as bytes, residual degrees, and
+// a consistency check -- a vertex is removed exactly when its degree is 1
+// (every share counted once); err |= 1 otherwise.  Warp per vertex.
+__global__ void prune_flags_kernel(int n, const int *rp, const int *col, const uint32_t *removed_sum,
+                                   uint8_t *removed, int *rdeg, int *err) {
+    const int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = lane_id();
+    if (v >= n) return;
+    const int a = rp[v], b = rp[v + 1];
+    const uint32_t rv = removed_sum[v];
+    int keep = 0;
+    for (int e = a + lane; e < b; e += 32) {
+        const int u = col[e];
+        keep += removed_sum[u] == 0u;
+    }
+    keep = __reduce_add_sync(0xffffffffu, keep);
+    if (lane == 0) {
+        if (rv > 1u || (rv == 1u) != (b - a == 1)) atomicOr(err, 1);
+        removed[v] = rv ? 1 : 0;
+        rdeg[v] = rv ? 0 : keep;
     }
 }
 

@@ -9,6 +9,11 @@ NCCL all-reduce (sum, fp64, n elements) over NVLink/NVSwitch through
 
 ``compute_fn(sources) -> tensor`` is the per-rank BC over a source subset
 (the CUDA path in production; tests substitute a CPU reference on gloo).
+
+``prune_degree1_distributed`` is Alg.6 in its distributed form
+(NEXT-4): rank i scans the vertices u = i mod #ranks,
+the two share vectors (omega increments, removed flags; 2 n uint32) are
+summed by one all-reduce, and every rank builds the same residual graph.
 """
 from __future__ import annotations
 
@@ -48,3 +53,36 @@ def graph_bc_distributed(graph, sources, device=None, group=None):
         return out
 
     return distributed_bc(_local, sources, group)
+
+
+def prune_shares_reduced(share_fn, n: int, group=None, device=None):
+    """Sum over ranks of share_fn(rank, world) -> (omega_part, removed_part)
+    (two int32 tensors of n elements), by one all-reduce of their
+    concatenation; returns (omega, removed) on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    om, rm = share_fn(rank, world)
+    buf = torch.cat([om.reshape(-1), rm.reshape(-1)])
+    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    return buf[:n], buf[n:]
+
+
+def prune_degree1_distributed(graph, group=None):
+    """Alg.6 over the ranks of `group` on this rank's replica `graph` (a
+    paper_1602_00963_b200.Graph): share on the device, NCCL all-reduce of
+    the shares, residual graph built locally.  Returns the removed count."""
+    import torch
+
+    dev = torch.device("cuda", graph.device)
+
+    def _share(rank, world):
+        om = torch.empty(graph.n, dtype=torch.int32, device=dev)
+        rm = torch.empty(graph.n, dtype=torch.int32, device=dev)
+        graph.prune_degree1_share(rank, world, om, rm)
+        return om, rm
+
+    om, rm = prune_shares_reduced(_share, graph.n, group)
+    return graph.prune_degree1_apply(om.contiguous(), rm.contiguous())

@@ -141,3 +141,41 @@ def test_literal_eq4_increment_order_is_wrong():
 def test_rmat_pruned_matches_unpruned():
     g = gg.rmat(10, 16, seed=1)
     assert _close(oracle.bc_pruned(g), oracle.bc(g), 1e-10)
+
+
+# ---- Alg.6 distributed over #P processors (u mod #P = P_i), NEXT-4
+@pytest.mark.parametrize("idx", range(0, len(RG), 2))
+def test_prune_shares_sum_to_single_pass(idx):
+    """The #P processors' shares (Alg.6 lines 3-9 on E_i = edges with
+    u mod #P = i) sum to the one-processor omega / removed for every #P: each
+    u belongs to exactly one E_i with all its edges."""
+    g = RG[idx]
+    om, rm, _, _ = oracle.prune_degree1(g)
+    deg = g.degrees
+    for P in (1, 2, 3, 5):
+        oms, rms = zip(*(oracle.prune_degree1_share(g, P, i) for i in range(P)))
+        assert np.array_equal(np.sum(oms, axis=0), om.astype(np.int64)), P
+        assert np.array_equal(np.sum(rms, axis=0), rm.astype(np.int64)), P
+        for i in range(P):  # a share only removes its own vertices, and only degree-1 ones
+            own = np.arange(g.n) % P == i
+            assert not np.any(rms[i][~own]) and np.array_equal(rms[i][own].astype(bool), deg[own] == 1)
+
+
+def test_prune_share_star_closed_form():
+    """Star K_{1,k} (centre 0): the leaves are removed wherever they sit and
+    omega(centre) = k = sum over the shares of the leaves each holds."""
+    k = 11
+    g = gg.star(k)
+    for P in (1, 2, 4):
+        tot = np.zeros(g.n, np.int64)
+        for i in range(P):
+            om, rm = oracle.prune_degree1_share(g, P, i)
+            leaves_here = sum(1 for u in range(1, k + 1) if u % P == i)
+            assert om[0] == leaves_here and rm[0] == 0
+            tot += om
+        assert tot[0] == k and tot[1:].sum() == 0
+
+
+def test_prune_share_rejects_bad_processor():
+    with pytest.raises(ValueError):
+        oracle.prune_degree1_share(gg.path(4), 2, 2)
