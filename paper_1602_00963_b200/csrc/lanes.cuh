@@ -383,6 +383,9 @@ __device__ __forceinline__ uint64_t interleave2(uint32_t a, uint32_t b) {
     y = (y | (y << 1)) & 0x5555555555555555ull;
     return x | (y << 1);
 }
+#ifndef BC_FWD_PIPE
+#define BC_FWD_PIPE 0  // > 0: whole-row forward with a rolling pipeline of BC_FWD_PIPE gathers in flight (else BC_FWD_HIT2)
+#endif
 #ifndef BC_FWD_UNCOND
 #define BC_FWD_UNCOND 1  // 16-bit forward: hit rows loaded whole (no per-pair c test; rows are zero outside their level)
 #endif
@@ -770,6 +773,63 @@ struct LanesKernel {
                         ++ring_used;
                         __syncwarp();
                         if (hi) issue();
+                    }
+                    __syncwarp();
+                    continue;
+                }
+                if constexpr (UNCOND && BC_NARROW_TMAJOR && BC_FWD_PIPE > 0) {
+                    // 16-bit forward, rolling gather pipeline: BC_FWD_PIPE hit rows
+                    // in flight at all times within a step -- buffer d is
+                    // consumed and at once refilled with the hit BC_FWD_PIPE
+                    // places later, so hits are added in order (slot order)
+                    constexpr int PD = BC_FWD_PIPE;
+                    const uint64_t rpol = row_policy();
+                    const uint16_t *S16 = reinterpret_cast<const uint16_t *>(p.S_cur);
+                    uint32_t rbuf[PD][W];
+                    int rslot[PD];
+                    unsigned q = hm;
+#pragma unroll
+                    for (int d = 0; d < PD; ++d) {
+                        rslot[d] = -1;
+                        if (q) {  // uniform
+                            const int src = __ffs(q) - 1;
+                            q &= q - 1;
+                            const int2 sv = sm.hsv[wid * 32 + src];
+                            rslot[d] = sv.x;
+                            ld_row_vec<W>(reinterpret_cast<const uint32_t *>(S16 + (size_t)sv.y * K) + lane * W, rpol,
+                                          rbuf[d]);
+                        }
+                    }
+                    bool more = true;
+                    while (more) {
+#pragma unroll
+                        for (int d = 0; d < PD; ++d) {
+                            if (more && rslot[d] < 0) more = false;  // uniform: later buffers are empty too
+                            if (more) {
+                                const int hs = rslot[d];
+                                while (cur < hs) {
+                                    flush(cur, first, ws, we, hub_mode, acc, aovf);
+                                    ++cur;
+#pragma unroll
+                                    for (int i = 0; i < LPT; ++i) acc[i] = SigT(0);
+                                    aovf = 0;
+                                }
+#pragma unroll
+                                for (int pr = 0; pr < W; ++pr) {
+                                    acc[2 * pr] += rbuf[d][pr] & 0xffffu;
+                                    acc[2 * pr + 1] += rbuf[d][pr] >> 16;
+                                }
+                                rslot[d] = -1;
+                                if (q) {  // uniform: refill with the hit PD places later
+                                    const int src = __ffs(q) - 1;
+                                    q &= q - 1;
+                                    const int2 sv = sm.hsv[wid * 32 + src];
+                                    rslot[d] = sv.x;
+                                    ld_row_vec<W>(reinterpret_cast<const uint32_t *>(S16 + (size_t)sv.y * K) + lane * W,
+                                                  rpol, rbuf[d]);
+                                }
+                            }
+                        }
                     }
                     __syncwarp();
                     continue;
