@@ -1170,7 +1170,7 @@ struct LanesKernel {
 #define BC_MINB 2  // min resident CTAs per SM for the level kernels at W < 4 (register cap)
 #endif
 #ifndef BC_MINB4
-#define BC_MINB4 4  // ... and at W = 4: 32 resident warps (64 registers, no spills)
+#define BC_MINB4 5  // ... and at W = 4: 40 resident warps (48 registers, small spills; S20 forward 88.6 -> 85.9 ms, profiles/exp_r2_fwd_minb.txt)
 #endif
 #ifndef BC_MINB8
 #define BC_MINB8 3  // ... and at W = 8 (16 lanes per thread)
