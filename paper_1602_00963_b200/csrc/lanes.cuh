@@ -383,6 +383,9 @@ __device__ __forceinline__ uint64_t interleave2(uint32_t a, uint32_t b) {
     y = (y | (y << 1)) & 0x5555555555555555ull;
     return x | (y << 1);
 }
+#ifndef BC_SEEN_RED
+#define BC_SEEN_RED 1  // forward commit: seen |= new lanes by a red.global.or instead of a load + store
+#endif
 #ifndef BC_FWD_PIPE
 #define BC_FWD_PIPE 0  // > 0: whole-row forward with a rolling pipeline of BC_FWD_PIPE gathers in flight (else BC_FWD_HIT2)
 #endif
@@ -565,7 +568,12 @@ struct LanesKernel {
         if (lane < W && wv) {
             size_t wi = (size_t)x * W + lane;
             p.mask_nxt[wi] = wv;
+#if BC_SEEN_RED
+            // fire-and-forget OR: no dependent load of seen in the commit
+            asm volatile("red.global.or.b64 [%0], %1;" ::"l"(p.seen + wi), "l"(wv) : "memory");
+#else
             p.seen[wi] |= wv;
+#endif
             if (VERIFY && ov) p.ovf[wi] |= ov;
         }
     }
