@@ -193,7 +193,7 @@ __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double
         }
     }
     contrib = warp_sum(contrib);
-    if (lane == 0 && contrib != 0.0) p.bc[x] += contrib;
+    if (lane == 0 && contrib != 0.0) bc_add(p.bc + x, contrib);
 }
 
 // 32 vertices per warp step: lane i tests vertex base + i, then the warp
@@ -328,7 +328,7 @@ struct PushKernel {
         }
         if (owned) {  // warp-uniform
             contrib = warp_sum(contrib);
-            if (lane == 0 && contrib != 0.0) p.bc[x] += contrib;
+            if (lane == 0 && contrib != 0.0) bc_add(p.bc + x, contrib);
         }
     }
 
@@ -411,7 +411,7 @@ struct PushKernel {
         }
         if (owned) {  // warp-uniform
             contrib = warp_sum(contrib);
-            if (lane == 0 && contrib != 0.0) p.bc[x] += contrib;
+            if (lane == 0 && contrib != 0.0) bc_add(p.bc + x, contrib);
         }
     }
 

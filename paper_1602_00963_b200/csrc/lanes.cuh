@@ -383,6 +383,16 @@ __device__ __forceinline__ uint64_t interleave2(uint32_t a, uint32_t b) {
     y = (y | (y << 1)) & 0x5555555555555555ull;
     return x | (y << 1);
 }
+#ifndef BC_BC_RED
+#define BC_BC_RED 1  // BC[x] += contribution as a fire-and-forget red.global.add (one adder per x per level: same order)
+#endif
+__device__ __forceinline__ void bc_add(double *p, double v) {
+#if BC_BC_RED
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+#else
+    *p += v;
+#endif
+}
 #ifndef BC_SEEN_RED
 #define BC_SEEN_RED 1  // forward commit: seen |= new lanes by a red.global.or instead of a load + store
 #endif
@@ -614,7 +624,7 @@ struct LanesKernel {
                 }
             }
             contrib = warp_sum(contrib);
-            if (lane == 0 && contrib != 0.0) p.bc[x] += contrib;
+            if (lane == 0 && contrib != 0.0) bc_add(p.bc + x, contrib);
         }
     }
 
