@@ -95,8 +95,11 @@ bc_status bc_prune_degree1(bc_graph *g, int64_t *out_removed);
  * state bc_prune_degree1 produces (no cascaded tree removal).
  *   omega_part, removed_part  DEVICE uint32[n] on the handle's device,
  *                overwritten (zeroed, then this share's contributions).
- *   cuda_stream  _share: stream-ordered on it and asynchronous (NULL: the
- *                library stream, synchronous).  _apply: waits for it first.
+ *   cuda_stream  _share: stream-ordered on it and asynchronous (NULL: waits
+ *                for all prior device work, runs on the library stream,
+ *                synchronous).  _apply: waits for it first (NULL: for all
+ *                prior device work -- e.g. an all-reduce on the legacy
+ *                default stream).
  *   omega, removed  DEVICE uint32[n]: the sums over all ranks; removed[v]
  *                must be 1 exactly for the degree-1 vertices, else
  *                BC_ERR_INVALID (a share missing or counted twice) and the

@@ -321,6 +321,7 @@ struct bc_graph {
     int mode = 0;
     int num_sms = 148;
     cudaStream_t own_stream = nullptr;
+    cudaEvent_t legacy_ev = nullptr;  // orders own_stream after the legacy default stream (NULL-stream calls)
     LaneCtx ctx[MAX_STREAMS];  // batch pipelines of bc_compute
     LaneCtx vctx, sctx;        // bc_sssp: integer verification (W = 1, uint64) and its fp64 delta pass
     int two_degree = 0;        // BC_OPT_TWO_DEGREE (NEXT-1)
@@ -1942,6 +1943,7 @@ bc_status bc_destroy(bc_graph *g) {
         if (g->h_pin) cudaFreeHost(g->h_pin);
         if (g->stats_ev) cudaEventDestroy(g->stats_ev);
         if (g->own_stream) cudaStreamDestroy(g->own_stream);
+        if (g->legacy_ev) cudaEventDestroy(g->legacy_ev);
     }
     delete g;
     return BC_OK;
@@ -2130,8 +2132,10 @@ bc_status bc_prune_degree1_share(const bc_graph *g, int rank, int nranks, uint32
     DeviceGuard dg(g->device);
     if (!is_device_ptr(omega_part) || !is_device_ptr(removed_part))
         return fail(BC_ERR_INVALID, "share outputs must be device memory");
-    bc_graph *gm = const_cast<bc_graph *>(g);
-    CK(wait_idle(gm));
+    // reads only the original CSR, which no call modifies; with no caller stream
+    // the outputs may still be in use by work on the legacy default stream (the
+    // library stream does not synchronise with it): wait for the device first
+    if (!cuda_stream) CU(cudaDeviceSynchronize());
     cudaStream_t st = cuda_stream ? (cudaStream_t)cuda_stream : g->own_stream;
     const int n = (int)g->n;
     CU(cudaMemsetAsync(omega_part, 0, (size_t)n * 4, st));
@@ -2153,7 +2157,11 @@ bc_status bc_prune_degree1_apply(bc_graph *g, const uint32_t *omega, const uint3
     DeviceGuard dg(g->device);
     if (!is_device_ptr(omega) || !is_device_ptr(removed)) return fail(BC_ERR_INVALID, "inputs must be device memory");
     CK(wait_idle(g));
-    if (cuda_stream) CU(cudaStreamSynchronize((cudaStream_t)cuda_stream));  // the exchange that produced the inputs
+    // the exchange that produced the inputs: its stream, or -- none given --
+    // every prior device work (the inputs may come from the legacy default
+    // stream, which the library's non-blocking stream does not wait for)
+    if (cuda_stream) CU(cudaStreamSynchronize((cudaStream_t)cuda_stream));
+    else CU(cudaDeviceSynchronize());
     cudaStream_t st = g->own_stream;
     const int n = (int)g->n;
     uint8_t *rm = nullptr;
@@ -2370,6 +2378,14 @@ bc_status bc_compute(bc_graph *g, const int32_t *sources, int64_t num_sources, d
     if (trace_on()) tr_m[0] = now_us();
     const bool dev_out = is_device_ptr(out_bc);
     cudaStream_t st = cuda_stream ? (cudaStream_t)cuda_stream : g->own_stream;
+    if (!cuda_stream && dev_out) {
+        // no caller stream: a device out_bc may still be in use by work on the
+        // legacy default stream, which the library's non-blocking stream does
+        // not wait for -- order after it
+        if (!g->legacy_ev) CU(cudaEventCreateWithFlags(&g->legacy_ev, cudaEventDisableTiming));
+        CU(cudaEventRecord(g->legacy_ev, cudaStreamLegacy));
+        CU(cudaStreamWaitEvent(st, g->legacy_ev, 0));
+    }
     if (!g->run_valid) CK(build_run(g));
     DevCSR &run = g->run;
     if (capture) CK(capture_prepare(g, sources, num_sources, trav, st));
