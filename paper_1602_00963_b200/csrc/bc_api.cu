@@ -188,12 +188,14 @@ constexpr int MAX_STREAMS = 8;   // concurrent batch pipelines (BC_OPT_STREAMS)
 // level (forward) and push (backward) kernel grids = resident CTAs x NUM / DEN
 // when several batch pipelines run concurrently: the gaps let a pipeline's
 // forward and another's backward share the SMs (S20, 3 pipelines: 307.5 ->
-// 302-304 ms per 8192 sources, profiles/exp_r2_gridfrac.txt)
+// 302-304 ms per 8192 sources, profiles/exp_r2_gridfrac.txt).  Since the
+// forward runs 5 CTAs per SM its full grid is best (270.7 vs 273.3-276.2 ms,
+// profiles/exp_r2_gridfrac.txt); the push keeps 3/4
 #ifndef BC_FGRID_NUM
-#define BC_FGRID_NUM 3
+#define BC_FGRID_NUM 1
 #endif
 #ifndef BC_FGRID_DEN
-#define BC_FGRID_DEN 4
+#define BC_FGRID_DEN 1
 #endif
 #ifndef BC_PGRID_NUM
 #define BC_PGRID_NUM 3
