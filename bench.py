@@ -409,7 +409,8 @@ def main():
             extra = {"rows_model": {"achieved": rows_ach, "frac": rows_ach / peak,
                                     "formula": "bytes this build's rows move (16-bit sigma rows): backward "
                                                "A(4/K + 1/8) + 8 D + (sb + 16) N, forward A(4/K + 1/8) + sb D + sb N"}}
-            limiter = "issue / L2 red sectors (backward), dependent-load latency (forward); DESIGN.md §5"
+            limiter = ("L2 atomic units for the fp64 reds, unevenly loaded across slices (backward); row-gather "
+                       "latency (forward); DESIGN.md §5")
         else:
             dom, dom_ms = "slices", agg["fwd_ms"]
             names = {"slices": "slices_lowdeg_sm_kernel (2-bit shared-memory state; forward + backward sweeps of "
