@@ -567,6 +567,40 @@ def test_device_loop_is_stream_ordered():
         assert_bc_close(tot.cpu().numpy(), w1 + w2)
 
 
+def test_default_stream_calls_are_ordered_after_pending_work():
+    """Calls given no stream run on the library's own non-blocking stream;
+    they must still be ordered after work already queued on torch's legacy
+    default stream: a device out_bc whose NaN fill sits behind a long GPU
+    spin, and distributed-pruning shares whose sum is formed behind one."""
+    import torch
+
+    bcb = _bcb()
+    g = gg.disjoint_union(gg.rmat(11, 8, seed=5), gg.star(4), gg.random_tree(20, seed=6))
+    S = np.nonzero(oracle.prune_degree1(g)[1] == 0)[0].astype(np.int32)
+    with bcb.Graph.from_csr(g) as G:
+        dev = torch.device("cuda", G.device)
+        om = torch.zeros(g.n, dtype=torch.int32, device=dev)
+        rm = torch.zeros(g.n, dtype=torch.int32, device=dev)
+        parts = []
+        for i in range(2):
+            a = torch.empty(g.n, dtype=torch.int32, device=dev)
+            b = torch.empty(g.n, dtype=torch.int32, device=dev)
+            G.prune_degree1_share(i, 2, a, b)
+            parts.append((a, b))
+        torch.cuda._sleep(200_000_000)  # the sums below run late on the default stream
+        for a, b in parts:
+            om += a
+            rm += b
+        G.prune_degree1_apply(om, rm)  # no stream: must wait for the sums
+        out = torch.empty(g.n, dtype=torch.float64, device=dev)
+        torch.cuda._sleep(200_000_000)
+        out.fill_(float("nan"))  # queued late: the call below must run after it
+        G.compute(S, out=out)
+        got = out.cpu().numpy()
+    want = oracle.bc(g)
+    assert_bc_close(got, want)
+
+
 @pytest.mark.parametrize("kernel", [1, 2, 3, 4])
 def test_slices_kernel_variants(kernel):
     """BC_OPT_SLICES_KERNEL (NEXT-2 ablation): the general kernel with and
