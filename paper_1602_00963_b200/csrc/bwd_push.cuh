@@ -38,6 +38,12 @@ namespace bcb {
 // row stride of the fp64 backward accumulators A[v][K]
 template <int W> struct AStride { static constexpr size_t v = 64 * W + BC_A_PAD; };
 
+#ifndef BC_A_PLANES
+#define BC_A_PLANES 0  // 1: accumulators group-major, A[j][v][32] (group j of every row in one plane)
+#endif
+// accumulator row of vertex v (lane 0) and the distance between its 32-lane groups
+#define A_ROW(A, vx_) (BC_A_PLANES ? (A) + (size_t)(vx_) * 32 : (A) + (size_t)(vx_) * AStride<W>::v)
+#define A_GRP(p) (BC_A_PLANES ? (size_t)(p).n * 32 : (size_t)32)
 #ifndef BC_REP_H
 #define BC_REP_H 0  // > 0: parents with id < BC_REP_H (degree order: the hubs) get replicated accumulator rows (slower, off)
 #endif
@@ -65,7 +71,7 @@ __global__ void __launch_bounds__(BC_NT) lanes_rep_fold_kernel(LanesParams p, do
             *q = 0.0;
         }
     }
-    if (s != 0.0) A[(size_t)y * AStride<W>::v + l] += s;
+    if (s != 0.0) A_ROW(A, y)[(size_t)(l >> 5) * A_GRP(p) + (l & 31)] += s;
 }
 
 __device__ __forceinline__ void red_add_f64(double *p, double v) {
@@ -168,7 +174,8 @@ __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double
     uint32_t bits = 0;
 #pragma unroll
     for (int j = 0; j < NG; ++j) bits |= (((uint32_t)(m[j >> 1] >> ((j & 1) * 32)) >> lane) & 1u) << j;
-    double *arow = A + (size_t)x * AStride<W>::v + lane;
+    double *arow = A_ROW(A, x) + lane;
+    const size_t ag = A_GRP(p);
     RT *row = S + (size_t)x * K;
     double av[NG], sv[NG];
 #pragma unroll
@@ -176,7 +183,7 @@ __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double
         av[j] = 0.0;
         sv[j] = 1.0;
         if (bits >> j & 1u) {
-            av[j] = arow[32 * j];
+            av[j] = arow[j * ag];
             sv[j] = (double)row[row_idx<W, RT>(32 * j + lane)];
         }
     }
@@ -186,7 +193,7 @@ __device__ __forceinline__ void bwd_finalize_vertex(const LanesParams &p, double
     for (int j = 0; j < NG; ++j) {
         if (bits >> j & 1u) {
             const double delta = sv[j] * av[j];
-            arow[32 * j] = 0.0;
+            arow[j * ag] = 0.0;
             if constexpr (COEF) row[32 * j + lane] = (1.0 + om + delta) / sv[j];  // fp64 rows: lane order
             contrib += p.lane_w1[32 * j + lane] * (delta + om);
             cap_delta_put(p, 32 * j + lane, x, delta);
@@ -276,7 +283,8 @@ struct PushKernel {
         for (int j = 0; j < NG; ++j)
             bits |= (((uint32_t)(sm.u[hs * W + (j >> 1)] >> ((j & 1) * 32)) >> lane) & 1u) << j;
         const RT *row = reinterpret_cast<const RT *>(p.S_cur) + (size_t)x * K;
-        double *arow = A + (size_t)x * AStride<W>::v + lane;
+        double *arow = A_ROW(A, x) + lane;
+    const size_t ag = A_GRP(p);
         const double om = p.omega ? (double)p.omega[x] : 0.0;
         double contrib = 0.0;
         // two halves of the groups (bounded live registers: cf stays live in the hit loop)
@@ -301,9 +309,9 @@ struct PushKernel {
                     sv[q] = (double)row[row_idx<W, RT>(32 * (h + q) + lane)];
 #endif
 #if BC_PUSH_OWN_HINT
-                    av[q] = ld_ef_f64(arow + 32 * (h + q), policy_evict_first());
+                    av[q] = ld_ef_f64(arow + (h + q) * ag, policy_evict_first());
 #else
-                    av[q] = arow[32 * (h + q)];
+                    av[q] = arow[(h + q) * ag];
 #endif
                 }
             }
@@ -316,9 +324,9 @@ struct PushKernel {
                     cf[j] = (1.0 + om + delta) * rcp_f64(sv[q]);
                     if (owned) {
 #if BC_PUSH_OWN_HINT
-                        st_ef_f64(arow + 32 * j, 0.0, policy_evict_first());
+                        st_ef_f64(arow + j * ag, 0.0, policy_evict_first());
 #else
-                        arow[32 * j] = 0.0;
+                        arow[j * ag] = 0.0;
 #endif
                         contrib += p.lane_w1[32 * j + lane] * (delta + om);
                         cap_delta_put(p, 32 * j + lane, x, delta);
@@ -378,7 +386,8 @@ struct PushKernel {
                                                 double (&cf)[NG]) {
         const int x = sm.vert[hs];
         const RT *row = reinterpret_cast<const RT *>(p.S_cur) + (size_t)x * K;
-        double *arow = A + (size_t)x * AStride<W>::v;
+        double *arow = A_ROW(A, x);
+        const size_t ag = A_GRP(p);
         const double om = p.omega ? (double)p.omega[x] : 0.0;
         double contrib = 0.0;
 #pragma unroll
@@ -391,7 +400,7 @@ struct PushKernel {
                 av[q] = 0.0;
                 if (h + q < nr && l < K) {
                     sv[q] = (double)row[row_idx<W, RT>(l)];
-                    av[q] = arow[l];
+                    av[q] = arow[(size_t)(l >> 5) * ag + (l & 31)];
                 }
             }
 #pragma unroll
@@ -402,7 +411,7 @@ struct PushKernel {
                     const double delta = sv[q] * av[q];
                     cf[r] = (1.0 + om + delta) * rcp_f64(sv[q]);
                     if (owned) {
-                        arow[l] = 0.0;
+                        arow[(size_t)(l >> 5) * ag + (l & 31)] = 0.0;
                         contrib += p.lane_w1[l] * (delta + om);
                         cap_delta_put(p, l, x, delta);
                     }
@@ -482,7 +491,8 @@ struct PushKernel {
 #pragma unroll
                         for (int j = 0; j < W; ++j) st_dag += __popcll(sm.hc[(wid * 32 + src) * W + j] & p.derived[j]);
                     }
-                    double *arow = A + (size_t)y * AStride<W>::v;
+                    double *arow = A_ROW(A, y);
+                    static_assert(!BC_A_PLANES || !BC_PUSH_COMPACT, "compact push uses row-major accumulators");
 #pragma unroll
                     for (int r = 0; r < NG; ++r) {
                         if (r < nr) {  // uniform
@@ -601,9 +611,12 @@ struct PushKernel {
                             }
                         }
                     }
-                    double *arow = A + (size_t)y * AStride<W>::v + lane;
-                    if (!FWD && BC_REP_H > 0 && y < BC_REP_H && p.arep)  // uniform: a hub parent's replica
+                    double *arow = A_ROW(A, y) + lane;
+                    size_t ag = A_GRP(p);
+                    if (!FWD && BC_REP_H > 0 && y < BC_REP_H && p.arep) {  // uniform: a hub parent's replica
                         arow = p.arep + ((size_t)(blockIdx.x % BC_REP_R) * BC_REP_H + y) * K + lane;
+                        ag = 32;
+                    }
                     uint64_t myword = 0;  // fwd: thread j < W ORs word j of c into lvl[L+1][y]
                     uint64_t cwords[W];
                     static_assert(W <= 8, "");
@@ -629,11 +642,11 @@ struct PushKernel {
                         if (gm >> j & 1u) {  // uniform
                             const uint32_t cw = (uint32_t)(cwords[j >> 1] >> ((j & 1) * 32));
 #ifdef BC_EXP_NORED  // experiment build only: traversal cost without the reds (wrong results)
-                            red_add_f64_if(arow + 32 * j, cf[j], (cw >> lane & 1u) & (cf[j] == -1.0));
+                            red_add_f64_if(arow + j * ag, cf[j], (cw >> lane & 1u) & (cf[j] == -1.0));
 #elif defined(BC_EXP_REDZERO)  // experiment: unpredicated red of 0.0 outside c (more L2 sectors, no branches)
-                            red_add_f64(arow + 32 * j, (cw >> lane & 1u) ? cf[j] : 0.0);
+                            red_add_f64(arow + j * ag, (cw >> lane & 1u) ? cf[j] : 0.0);
 #else
-                            red_add_f64_if(arow + 32 * j, (!FWD && PushSmem<W>::CFS) ? sm.cfs[wid * K + 32 * j + lane] : cf[j],
+                            red_add_f64_if(arow + j * ag, (!FWD && PushSmem<W>::CFS) ? sm.cfs[wid * K + 32 * j + lane] : cf[j],
                                            cw >> lane & 1u);
 #endif
                             if (FWD) st_dag += cw >> lane & 1u;
@@ -803,21 +816,22 @@ __global__ void __launch_bounds__(BC_NT) lanes_fwd_commit_kernel(LanesParams p, 
             any |= m[j] != 0;
         }
         if (!any) continue;  // warp-uniform
-        double *arow = A + (size_t)x * AStride<W>::v + lane;
+        double *arow = A_ROW(A, x) + lane;
+    const size_t ag = A_GRP(p);
         double *row = S + (size_t)x * K + lane;
         double av[NG];
         uint32_t bits = 0;
 #pragma unroll
         for (int j = 0; j < NG; ++j) {
             bits |= (((uint32_t)(m[j >> 1] >> ((j & 1) * 32)) >> lane) & 1u) << j;
-            av[j] = (bits >> j & 1u) ? arow[32 * j] : 0.0;
+            av[j] = (bits >> j & 1u) ? arow[j * ag] : 0.0;
         }
         const double wx = 1.0 + (p.omega ? (double)p.omega[x] : 0.0);
 #pragma unroll
         for (int j = 0; j < NG; ++j) {
             row[32 * j] = av[j];
             if (bits >> j & 1u) {
-                arow[32 * j] = 0.0;
+                arow[j * ag] = 0.0;
                 if (p.lane_ns) atomicAdd(&ns_sm[32 * j + lane], wx);
             }
         }

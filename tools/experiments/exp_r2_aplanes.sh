@@ -1,0 +1,9 @@
+# backward accumulators group-major (A[j][v][32], ap1) vs row-major (A[v][K], ap0)
+for v in ap0 ap1 ap0 ap1; do
+  echo -n "$v S20 1pipe: "; BC_SO=build_exp/lib_$v.so timeout 200 python tools/prof_batch.py --sources 8192 --streams 1 --repeat 2 | tail -1 | cut -c1-120
+done
+for v in ap0 ap1; do
+  echo -n "$v S20 auto: "; BC_SO=build_exp/lib_$v.so timeout 200 python tools/prof_batch.py --sources 8192 --lane-words 0 --repeat 3 --no-profile | tail -1 | cut -c1-80
+  echo -n "$v S16 all: "; BC_SO=build_exp/lib_$v.so timeout 200 python tools/prof_batch.py --scale 16 --all --lane-words 0 --repeat 2 --no-profile | tail -1 | cut -c1-80
+done
+echo -n "ap1 parity: "; BC_SO=build_exp/lib_ap1.so timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_capture.py -m gpu -q -p no:cacheprovider 2>&1 | tail -1
