@@ -393,6 +393,9 @@ __device__ __forceinline__ void bc_add(double *p, double v) {
     *p += v;
 #endif
 }
+#ifndef BC_FWD_COLPF
+#define BC_FWD_COLPF 0  // 1: forward step loop fetches the next step's columns one step ahead
+#endif
 #ifndef BC_SEEN_RED
 #define BC_SEEN_RED 1  // forward commit: seen |= new lanes by a red.global.or instead of a load + store
 #endif
@@ -670,19 +673,37 @@ struct LanesKernel {
         const uint64_t pol = policy_evict_first();
 
         st_items += (lane == 0) ? (unsigned)(we - ws) : 0u;
-        for (int e0 = ws; e0 < we; e0 += 32 * R) {
-            int sl[R], vv[R];
+        // BC_FWD_COLPF: the next step's (slot, column) is fetched while this
+        // step's masks and hits are processed (the column load latency was
+        // the step loop's top stall)
+        auto fetch = [&](int e0f, int (&slf)[R], int (&vvf)[R]) {
 #pragma unroll
             for (int k = 0; k < R; ++k) {
-                int e = e0 + k * 32 + lane;
-                sl[k] = -1;
-                vv[k] = 0;
+                int e = e0f + k * 32 + lane;
+                slf[k] = -1;
+                vvf[k] = 0;
                 if (e < we) {
                     int s = slot_of(sm.cd, nslots, e);
-                    sl[k] = s;
-                    vv[k] = ld_stream(p.col + sm.rs[s] + (e - sm.cd[s]), pol);
-                    BC_CHECK(s >= 0 && s < nslots && vv[k] >= 0 && vv[k] < p.n);
+                    slf[k] = s;
+                    vvf[k] = ld_stream(p.col + sm.rs[s] + (e - sm.cd[s]), pol);
+                    BC_CHECK(s >= 0 && s < nslots && vvf[k] >= 0 && vvf[k] < p.n);
                 }
+            }
+        };
+        constexpr bool COLPF = BC_FWD_COLPF && !BWD;
+        int sln[R], vvn[R];
+        if constexpr (COLPF) fetch(ws, sln, vvn);
+        for (int e0 = ws; e0 < we; e0 += 32 * R) {
+            int sl[R], vv[R];
+            if constexpr (COLPF) {
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+                    sl[k] = sln[k];
+                    vv[k] = vvn[k];
+                }
+                if (e0 + 32 * R < we) fetch(e0 + 32 * R, sln, vvn);  // uniform
+            } else {
+                fetch(e0, sl, vv);
             }
             uint64_t cc[R][W];
 #pragma unroll
