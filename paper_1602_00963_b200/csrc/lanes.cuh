@@ -131,7 +131,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 #ifndef BC_FWD_MASK_HINT
-#define BC_FWD_MASK_HINT 0  // L2 policy of the forward's item mask loads (lvl[L][v]): 0 none, 2 evict_last
+#define BC_FWD_MASK_HINT 1  // L2 policy of the forward's item mask loads (lvl[L][v]): 0 none, else evict_last (forward 85.0 -> 84.65 ms, profiles/exp_r2_hints3.txt)
 #endif
 #ifndef BC_FWD_ROW_HINT
 #define BC_FWD_ROW_HINT 2  // L2 policy of the 16-bit forward's sigma-row gathers: 0 none, 1 evict_first, 2 evict_last (~1 %, profiles/exp_r2_fwd_rowhint.txt)
