@@ -85,3 +85,17 @@ def test_no_gpu_means_cuda_error_not_fallback(lib):
 
     with pytest.raises(bcb.BCError):
         bcb.Graph(g.row_ptr, g.col)
+
+
+def test_distributed_pruning_entry_points_reject_bad_arguments(lib):
+    """bc_prune_degree1_share / _apply (NEXT-4) fail with BC_ERR_INVALID on a
+    NULL handle, before touching any device."""
+    from paper_1602_00963_b200 import _lib
+
+    fn = lib.bc_prune_degree1_share
+    fn.restype, fn.argtypes = _lib.SIGNATURES["bc_prune_degree1_share"]
+    assert fn(None, 0, 1, None, None, None) == 1
+    fn = lib.bc_prune_degree1_apply
+    fn.restype, fn.argtypes = _lib.SIGNATURES["bc_prune_degree1_apply"]
+    r = ctypes.c_int64(0)
+    assert fn(None, None, None, None, ctypes.byref(r)) == 1
